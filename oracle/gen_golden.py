@@ -1,0 +1,297 @@
+"""Generate tests/golden/*.npz from the LIVE reference (run in the build container).
+
+TEST INFRASTRUCTURE.  Usage (the reference tree is read-only, numba needs a
+writable cache):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python oracle/gen_golden.py
+
+Every fixture is produced by calling the reference's own public API
+(``find_closest_stencils``, ``compute_weights`` with the batched
+``RbfFd(Polyharmonic(k), solver="lu")`` engine, ``WeightStore.matrix``,
+``apply_all``, ``run_heat_explicit``) on seeded synthetic inputs.  The
+environment versions are stored alongside (``meta`` entries).  The CPU tests
+then pin the C oracle to these vectors bit-for-bit, and the GPU tests compare
+the CUDA path with both.
+"""
+
+from __future__ import annotations
+
+import os
+import platform
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, REPO)
+
+import meshfree  # noqa: E402  (the reference, from PYTHONPATH)
+import numba  # noqa: E402
+import scipy  # noqa: E402
+from meshfree import (  # noqa: E402
+    InstabilityError,
+    NodeSet,
+    Polyharmonic,
+    RbfFd,
+    WeightError,
+    compute_weights,
+    find_closest_stencils,
+)
+from meshfree.drivers import run_heat_explicit  # noqa: E402
+
+from paper_1912_13282_b200 import workloads  # noqa: E402
+
+OUT = os.path.join(REPO, "tests", "golden")
+
+
+def meta():
+    return dict(
+        meta_numpy=np.array(np.__version__),
+        meta_scipy=np.array(scipy.__version__),
+        meta_numba=np.array(numba.__version__),
+        meta_python=np.array(platform.python_version()),
+        meta_libc=np.array(" ".join(platform.libc_ver())),
+        meta_backend=np.array(meshfree.backend_name()),
+    )
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays, **meta())
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def cloud(n, d, seed, lo=-1.0, hi=1.0):
+    return np.random.default_rng(seed).uniform(lo, hi, (n, d))
+
+
+# -- kNN -------------------------------------------------------------------
+
+def knn_cases():
+    """Small clouds mirroring reference tests/test_stencils.py + edge cases."""
+    cases = []
+
+    def add(name, pts, n, types=None, for_which=None, search_among=None):
+        N = pts.shape[0]
+        types = np.ones(N, dtype=np.int64) if types is None else types
+        nodes = NodeSet(pts, types)
+        out = find_closest_stencils(nodes, n, for_which, search_among)
+        tg = nodes.select(for_which)
+        pool = nodes.select(search_among)
+        st = np.stack([out.stencil(int(i)) for i in tg]) if tg.size else np.zeros((0, n), np.int64)
+        cases.append(dict(name=name, pts=pts, types=types, n=n, targets=tg, pool=pool, stencils=st))
+
+    add("random2d_60_n7", cloud(60, 2, 0), 7)
+    add("random3d_40_n5", cloud(40, 3, 3), 5)
+    g = np.stack(np.meshgrid(np.arange(5.0), np.arange(5.0), indexing="ij"), axis=-1).reshape(-1, 2)
+    add("grid5x5_ties_n4", g, 4)
+    g3 = np.stack(np.meshgrid(np.arange(4.0), np.arange(4.0), np.arange(4.0), indexing="ij"), axis=-1).reshape(-1, 3)
+    add("grid4x4x4_ties_n9", g3, 9)
+    add("grid4x4x4_ties_n27", g3, 27)
+    types = np.ones(30, dtype=np.int64)
+    types[:6] = -1
+    add("for_which_interior", cloud(30, 2, 1), 4, types=types.copy(), for_which="interior")
+    add("search_among_interior", cloud(30, 2, 2), 4, types=types.copy(), search_among="interior")
+    idx = np.array([17, 3, 25, 3, 9], dtype=np.int64)
+    add("explicit_targets_unsorted", cloud(30, 3, 4), 6, for_which=idx, search_among=np.arange(5, 30))
+    for s in range(24):
+        rng = np.random.default_rng(1000 + s)
+        d = 2 + (s % 2)
+        n = 1 + (s * 5) % 12
+        add(f"prop_seed{s}_d{d}_n{n}", rng.uniform(-1, 1, (16, d)), n)
+    # coincident nodes: self cannot lead by distance alone
+    dup = cloud(20, 2, 7)
+    dup[5] = dup[3]
+    dup[6] = dup[3]
+    dup[11] = dup[3]
+    add("duplicates_n3", dup, 3)
+    add("duplicates_n6", dup, 6)
+    add("line1d_n5", np.sort(cloud(25, 1, 8), axis=0), 5)
+    add("pool_equals_n", cloud(12, 2, 9), 12)
+    add("single_n1", cloud(15, 3, 10), 1)
+    return cases
+
+
+def dump_knn():
+    cases = knn_cases()
+    arrs = {}
+    for i, c in enumerate(cases):
+        for k, v in c.items():
+            arrs[f"c{i}_{k}"] = np.asarray(v)
+    arrs["count"] = np.array(len(cases))
+    save("knn_small.npz", **arrs)
+
+
+def config_subset(w, n_targets, stride=1):
+    nodes = NodeSet(w.positions, w.types)
+    tg = np.arange(0, w.N, stride, dtype=np.int64)[:n_targets]
+    nodes = find_closest_stencils(nodes, w.n, for_which=tg)
+    st = np.stack([nodes.stencil(int(i)) for i in tg])
+    return nodes, tg, st
+
+
+def dump_configs():
+    """Per-config stencils + weights for a prefix/strided subset of targets."""
+    specs = [("C1", workloads.c1(), 2000, 1), ("C2", workloads.c2(), 400, 499),
+             ("C3", workloads.c3(), 300, 3331), ("C4", workloads.c4(), 400, 2477),
+             ("C5", workloads.c5(), 60, 66_667)]
+    for name, w, cnt, stride in specs:
+        nodes, tg, st = config_subset(w, cnt, stride)
+        eng = RbfFd(Polyharmonic(3), degree=w.degree, scale="support", solver="lu")
+        store = compute_weights(nodes, eng, w.families, for_which=tg)
+        arrs = dict(targets=tg, stencils=st.astype(np.int32), n=np.array(w.n),
+                    degree=np.array(w.degree), families=np.array(store.families))
+        for f in store.families:
+            arrs[f"w_{f}"] = store.values[f].reshape(len(tg), w.n)
+        save(f"config_{name}.npz", **arrs)
+
+
+# -- weight variants ---------------------------------------------------------
+
+def dump_weight_variants():
+    """Engine/family variants through the batched path (storage.py:310-322)."""
+    arrs = {}
+    variants = [
+        # name, d, N, n, k, degree, scale, families
+        ("k3_deg2_support_2d", 2, 400, 12, 3, 2, "support", ["laplacian", "gradient", "hessian", "identity"]),
+        ("k3_deg2_nearest_2d", 2, 400, 12, 3, 2, "nearest", ["laplacian", "gradient"]),
+        ("k3_deg2_none_2d", 2, 400, 12, 3, 2, "none", ["laplacian"]),
+        ("k5_deg2_support_3d", 3, 500, 20, 5, 2, "support", ["laplacian", "gradient", "hessian"]),
+        ("k4_even_deg1_2d", 2, 300, 9, 4, 1, "support", ["laplacian", "d1_0"]),
+        ("k3_nodeg_2d", 2, 300, 9, 3, -1, "support", ["laplacian", "identity"]),
+        ("k3_deg3_3d", 3, 600, 30, 3, 3, "support", ["laplacian", "d2_0_2"]),
+        ("k7_deg2_1d", 1, 100, 7, 7, 2, "nearest", ["laplacian", "d1_0", "d2_0_0"]),
+        ("k3_deg2_3d_n45", 3, 500, 45, 3, 2, "support", ["laplacian", "gradient"]),
+        ("k3_deg2_2d_n31", 2, 500, 31, 3, 2, "support", ["laplacian"]),
+    ]
+    arrs["names"] = np.array([v[0] for v in variants])
+    for vi, (name, d, N, n, k, deg, scale, fams) in enumerate(variants):
+        pts = cloud(N, d, 500 + vi, 0.0, 1.0)
+        nodes = find_closest_stencils(NodeSet(pts, np.ones(N, dtype=np.int64)), n)
+        eng = RbfFd(Polyharmonic(k), degree=deg, scale=scale, solver="lu")
+        store = compute_weights(nodes, eng, fams)
+        arrs[f"{name}_pts"] = pts
+        arrs[f"{name}_stencils"] = nodes.stencil_matrix().astype(np.int32)
+        arrs[f"{name}_params"] = np.array([d, N, n, k, deg])
+        arrs[f"{name}_scale"] = np.array(scale)
+        arrs[f"{name}_families"] = np.array(fams)
+        arrs[f"{name}_keys"] = np.array(store.families)
+        for f in store.families:
+            arrs[f"{name}_w_{f}"] = store.values[f].reshape(N, n)
+    save("weight_variants.npz", **arrs)
+
+
+def dump_weight_errors():
+    """Degenerate stencils: the lowest failing row's node id and message."""
+    arrs = {}
+    pts = cloud(50, 2, 21, 0.0, 1.0)
+    # node 13 and its stencil collapse onto one point -> scale degenerate
+    pts[[13, 30, 31, 32, 33]] = pts[13]
+    nodes = NodeSet(pts, np.ones(50, dtype=np.int64))
+    nodes = find_closest_stencils(nodes, 5, for_which=np.arange(13, 50))
+    eng = RbfFd(Polyharmonic(3), degree=1, scale="support", solver="lu")
+    try:
+        compute_weights(nodes, eng, ["laplacian"], for_which=np.arange(13, 50))
+        msg = ""
+    except WeightError as exc:
+        msg = str(exc)
+    arrs["scale_pts"] = pts
+    arrs["scale_msg"] = np.array(msg)
+    # collinear stencil with a 2D degree-1 basis -> singular system
+    pts2 = cloud(40, 2, 22, 0.0, 1.0)
+    pts2[:8, 1] = 0.5
+    pts2[:8, 0] = np.linspace(0.1, 0.2, 8)
+    nodes2 = find_closest_stencils(NodeSet(pts2, np.ones(40, dtype=np.int64)), 4, for_which=np.arange(8))
+    try:
+        compute_weights(nodes2, eng, ["laplacian"], for_which=np.arange(8))
+        msg2 = ""
+    except WeightError as exc:
+        msg2 = str(exc)
+    arrs["singular_pts"] = pts2
+    arrs["singular_msg"] = np.array(msg2)
+    save("weight_errors.npz", **arrs)
+
+
+# -- CSR, apply, heat ----------------------------------------------------------
+
+def dump_csr_apply():
+    arrs = {}
+    pts = cloud(700, 2, 31, 0.0, 1.0)
+    types = np.ones(700, dtype=np.int64)
+    types[::7] = -1
+    nodes = find_closest_stencils(NodeSet(pts, types), 12)
+    eng = RbfFd(Polyharmonic(3), degree=2, scale="support", solver="lu")
+    # only interior rows stored: boundary rows of the CSR stay empty
+    store = compute_weights(nodes, eng, ["laplacian", "gradient"], for_which="interior")
+    u = np.random.default_rng(5).standard_normal(700)
+    arrs["pts"] = pts
+    arrs["types"] = types
+    arrs["rows"] = store.rows
+    arrs["stencils"] = np.stack([nodes.stencil(int(i)) for i in store.rows]).astype(np.int32)
+    arrs["u"] = u
+    for f in store.families:
+        m = store.matrix(f)
+        arrs[f"{f}_indptr"] = m.indptr
+        arrs[f"{f}_indices"] = m.indices
+        arrs[f"{f}_data"] = m.data
+        arrs[f"{f}_w"] = store.values[f]
+        arrs[f"{f}_y"] = store.apply_all(f, u)
+    save("csr_apply.npz", **arrs)
+
+
+def dump_heat():
+    arrs = {}
+    N = 3000
+    pts = cloud(N, 2, 41, 0.0, 1.0)
+    h = 1.0 / np.sqrt(N)
+    edge = np.minimum(np.minimum(pts[:, 0], pts[:, 1]), np.minimum(1 - pts[:, 0], 1 - pts[:, 1]))
+    types = np.where(edge < h, -1, 1).astype(np.int64)
+    nodes = find_closest_stencils(NodeSet(pts, types), 15)
+    eng = RbfFd(Polyharmonic(3), degree=2, scale="support", solver="lu")
+    store = compute_weights(nodes, eng, ["laplacian"])
+    d = pts - 0.5
+    u0 = np.exp(-50.0 * (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]))
+    from scipy.spatial import cKDTree
+    hmin = float(cKDTree(pts).query(pts, k=2)[0][:, 1].min())
+    dt = 0.1 * hmin * hmin
+    u = run_heat_explicit(nodes, store, dt=dt, steps=40, dirichlet={-1: 0.0}, initial=u0)
+    arrs.update(pts=pts, types=types, u0=u0, dt=np.array(dt), steps=np.array(40), u_final=u,
+                stencils=nodes.stencil_matrix().astype(np.int32), w=store.values["laplacian"].reshape(N, 15))
+    # source + diffusivity + a Dirichlet value != 0
+    u2 = run_heat_explicit(nodes, store, dt=dt, steps=25, diffusivity=0.7, source=lambda p, t: 2.0,
+                           dirichlet={-1: 0.25}, initial=u0)
+    arrs["u_final_src"] = u2
+    # literal dt = 0.1 h^2 diverges: parity of the failure
+    try:
+        run_heat_explicit(nodes, store, dt=0.1 * h * h, steps=400, dirichlet={-1: 0.0}, initial=u0)
+        arrs["unstable_msg"] = np.array("")
+        arrs["unstable_step"] = np.array(0)
+    except InstabilityError as exc:
+        arrs["unstable_msg"] = np.array(str(exc))
+        arrs["unstable_step"] = np.array(exc.step)
+    arrs["dt_literal"] = np.array(0.1 * h * h)
+    try:
+        run_heat_explicit(nodes, store, dt=0.5, steps=50, dirichlet={-1: 0.0}, initial=u0)
+        arrs["unstable2_msg"] = np.array("")
+    except InstabilityError as exc:
+        arrs["unstable2_msg"] = np.array(str(exc))
+    save("heat.npz", **arrs)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat"]
+    if "knn" in which:
+        dump_knn()
+    if "variants" in which:
+        dump_weight_variants()
+    if "errors" in which:
+        dump_weight_errors()
+    if "csr" in which:
+        dump_csr_apply()
+    if "heat" in which:
+        dump_heat()
+    if "configs" in which:
+        dump_configs()
