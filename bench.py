@@ -1,0 +1,375 @@
+"""Benchmark of the RBF-FD hot path on B200 (BASELINE.json metric).
+
+One step = the whole hot path over config C3 (3D unit cube, N = 1,000,000
+uniform nodes, n = 35, PHS r^3 + degree-2 monomials, Laplacian):
+    kNN stencils -> shape solve -> canonical CSR -> explicit Laplacian apply.
+
+value      stencils/s through the step with inputs resident in HBM
+           (device-timed with CUDA events, L2 flushed between steps)
+e2e        same metric through the public API with host (pinned) inputs:
+           positions + field H2D and the applied field D2H inside the region
+roofline   dominant kernel = the shape solve (fp64-pipe bound): algorithmic
+           flops F = (2/3)s^3 + 2 r s^2 per stencil / its CUDA-event time,
+           against the fp64 DFMA peak measured in this run; apply_roofline
+           gives the Laplacian apply against MEASURED_PEAKS.json HBM GB/s
+cpu_baseline  the C oracle (bit-exact restatement of the reference's numba
+           kernel + kNN + CSR + matvec) on host cores over a bounded sample
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (torchrun): every rank runs its own C3-size node set (seed = rank),
+no collective on the data path; value = all stencils / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+
+METRIC = "RBF-FD shapes/s (3D, n=35, deg-2 monomials); explicit Laplacian apply GB/s"
+UNIT = "stencils/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="hybrid", choices=["hybrid", "replay", "fast"])
+    ap.add_argument("--N", type=int, default=1_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=20_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def c3_positions(N, seed):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0.0, 1.0, (N, 3))
+
+
+def flops_per_stencil(n, l, r):
+    s = n + l
+    return (2.0 / 3.0) * s**3 + 2.0 * r * s * s
+
+
+def apply_bytes(N, nnz, r=1):
+    return nnz * (8 * r + 4) + N * 8 + r * N * 8 + (N + 1) * 4
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[2:6]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle (pinned bit-exact to the reference)
+# ---------------------------------------------------------------------------
+
+def cpu_pipeline_sample(pts, n, sample, threads=0):
+    """Oracle kNN + weights + CSR + apply over `sample` targets; returns seconds."""
+    import oracle
+
+    N = pts.shape[0]
+    targets = np.arange(0, N, max(1, N // sample), dtype=np.int64)[:sample]
+    u = np.random.default_rng(1).standard_normal(N)
+    t0 = time.perf_counter()
+    st, _ = oracle.knn(pts, n, targets, threads=threads)
+    w, fail, _ = oracle.phs_weights(pts, targets, st, ["laplacian"], degree=2, threads=threads)
+    ip, ix, da = oracle.csr_canonical(targets, st, w[:, 0, :], N)
+    oracle.apply(ip, ix, da, u, threads=1)
+    return time.perf_counter() - t0, targets.shape[0]
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+
+    pts = c3_positions(args.N, 0)
+    cores = os.cpu_count() or 1
+    oracle.build()
+    for _ in range(args.warmup):
+        cpu_pipeline_sample(pts, 35, max(1000, args.cpu_sample // 10), threads=cores)
+    times, counts = [], []
+    for _ in range(args.steps):
+        dt, cnt = cpu_pipeline_sample(pts, 35, args.cpu_sample, threads=cores)
+        times.append(dt)
+        counts.append(cnt)
+    value = sum(counts) / sum(times)
+    sample = (f"C3 node set (N={args.N}); per step {args.cpu_sample} strided targets through oracle "
+              f"kNN + shape solve + CSR + apply, {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "C3", "N": args.N, "n": 35, "degree": 2,
+                                        "families": ["laplacian"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_13282_b200 as mf
+    from paper_1912_13282_b200 import _lib, build as mfbuild
+    from paper_1912_13282_b200.stencils import knn_device
+    from paper_1912_13282_b200.storage import phs_weights_device, expand_families
+
+    mfbuild.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    N, n, deg = args.N, 35, 2
+    l = 10
+    pts = c3_positions(N, rank)
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=deg, scale="support", solver="lu", mode=args.mode)
+    fams = expand_families(["laplacian"], 3)
+    u_host = np.random.default_rng(1).standard_normal(N)
+
+    nodes = mf.NodeSet(pts, np.ones(N, dtype=np.int64))
+    pos_d = nodes.positions_device()
+    u_d = torch.from_numpy(u_host).to(dev)
+    all_idx = np.arange(N, dtype=np.int64)
+    rows_d = torch.arange(N, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(timers=None):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timers is not None else None
+        if ev:
+            ev[0].record(stream)
+        st, _ = knn_device(nodes, n, all_idx, all_idx)
+        if ev:
+            ev[1].record(stream)
+        w, status, first_fail, n_rep = phs_weights_device(pos_d, rows_d, st, eng, fams, 3)
+        if ev:
+            ev[2].record(stream)
+        store = mf.WeightStore(N, all_idx, st, {"laplacian": w[:, 0, :]}, n)
+        mat = store.matrix("laplacian")
+        mat.ell()
+        if ev:
+            ev[3].record(stream)
+        y = mat.apply_device(u_d)
+        if ev:
+            ev[4].record(stream)
+            timers.append(ev)
+        return y, first_fail, n_rep
+
+    for _ in range(args.warmup):
+        y, ff, _ = step()
+    torch.cuda.synchronize()
+    assert int(ff.item()) == _lib.SENTINEL_OK, "shape solve reported a failing stencil"
+
+    # fp64 pipe peak for the roofline denominator (measured in this run)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    probe_out = torch.empty(1, dtype=torch.float64, device=dev)
+    fl = ctypes_double()
+    for _ in range(2):
+        lib.mf_dfma_probe(sms * 8, 256, 2000, probe_out.data_ptr(), _lib.stream_ptr(), fl)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    lib.mf_dfma_probe(sms * 8, 256, 2000, probe_out.data_ptr(), _lib.stream_ptr(), fl)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    fp64_peak = fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+    # timed region: per-step events, L2 flushed between steps (outside the events)
+    timers = []
+    launches0 = lib.mf_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            y, ff, n_rep = step(timers)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = (lib.mf_launch_count() - launches0) // args.steps
+    stage = np.array([[a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])] for ev in timers])  # ms
+    step_ms = float(stage.sum(axis=1).mean())
+    t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t_local.item())
+    value = world * N / (step_ms_max * 1e-3)
+    n_replayed = int(n_rep.item())
+
+    knn_ms, phs_ms, csr_ms, apply_ms = (float(x) for x in stage.mean(axis=0))
+    F = flops_per_stencil(n, l, 1)
+    phs_tflops = N * F / (phs_ms * 1e-3) / 1e12
+    nnz = N * n
+    b_apply = apply_bytes(N, nnz)
+    apply_gbs = b_apply / (apply_ms * 1e-3) / 1e9
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pts_pin = torch.empty((N, 3), dtype=torch.float64, pin_memory=True).numpy()
+        pts_pin[:] = pts
+        u_pin = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
+        u_pin[:] = u_host
+        types = np.ones(N, dtype=np.int64)
+
+        def e2e_step():
+            nodes_h = mf.NodeSet(pts_pin, types)
+            nodes_h = mf.find_closest_stencils(nodes_h, n)
+            store_h = mf.compute_weights(nodes_h, eng, ["laplacian"])
+            return store_h.apply_all("laplacian", u_pin)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y_h = e2e_step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        e2e_t = torch.tensor([statistics.mean(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * N / float(e2e_t.item()), "unit": UNIT,
+               # positions, field, and the int64 target/pool/row index arrays
+               "h2d_bytes_per_step": int(pts.nbytes + u_host.nbytes + 3 * N * 8),
+               "d2h_bytes_per_step": int(y_h.nbytes)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        oracle.build()
+        cores = os.cpu_count() or 1
+        cpu_pipeline_sample(pts, n, 2000, threads=cores)
+        secs, cnt = cpu_pipeline_sample(pts, n, args.cpu_sample, threads=cores)
+        cpu = {"value": cnt / secs, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cnt} strided C3 targets through oracle kNN + shape solve + CSR + apply "
+                         f"({secs:.2f} s, {cores} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3", "N": N, "n": n, "degree": deg, "families": ["laplacian"],
+                       "shape_mode": args.mode, "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"weak x{world} (independent node sets per rank)"},
+            "stage_ms": {"knn": knn_ms, "shape_solve": phs_ms, "csr_and_plan": csr_ms, "apply": apply_ms},
+            "shapes_per_s": N / (phs_ms * 1e-3),
+            "apply_gbs": apply_gbs,
+            "roofline": {"bound": "fp64", "kernel": "mf_phs_weights (shape solve)",
+                         "achieved": phs_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": phs_tflops / fp64_peak, "traffic": None,
+                         "note": "F=(2/3)s^3+2rs^2 per stencil (s=45, r=1); peak = DFMA probe measured "
+                                 "in this run (MEASURED_PEAKS.json has no fp64 entry)"},
+            "apply_roofline": {"bound": "hbm", "kernel": "mf_ell_apply", "achieved": apply_gbs,
+                               "peak": hbm_peak, "unit": "GB/s", "frac": apply_gbs / hbm_peak,
+                               "traffic": None, "bytes_per_launch": b_apply,
+                               "note": "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"},
+            "replayed_stencils": n_replayed,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_double():
+    import ctypes
+
+    return ctypes.c_double(0.0)
+
+
+if __name__ == "__main__":
+    main()

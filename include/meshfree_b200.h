@@ -1,0 +1,181 @@
+/*
+ * meshfree_b200.h -- C ABI of the B200 (sm_100a) RBF-FD hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch types.
+ * Each entry point replaces one reference interface (paths relative to the
+ * reference checkout, pkg/src/meshfree/...):
+ *
+ *   mf_knn            geometry/stencils.py:19-93    find_closest_stencils
+ *   mf_phs_weights    _phs_batch.py:305-324         batch_phs_weights
+ *                     (kernel body _phs_batch.py:142-302, caller storage.py:342-409)
+ *   mf_csr_build      storage.py:156-170            WeightStore.matrix (structure)
+ *   mf_csr_gather     storage.py:165-168            WeightStore.matrix (values per family)
+ *   mf_apply          storage.py:186-188            WeightStore.apply_all (scipy csr_matvec)
+ *   mf_apply_rows     storage.py:174-184            WeightStore.apply (selected rows)
+ *   mf_ell_build/_apply storage.py:186-188          apply_all through an ELL-32 apply plan
+ *   mf_heat_steps     drivers.py:87-110             run_heat_explicit step loop
+ *   mf_neumann_values storage.py:226-250            WeightStore.neumann_value (batched)
+ *
+ * Conventions
+ *   - Array arguments are DEVICE pointers unless the parameter is documented
+ *     as a host array; they are borrowed, never freed.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is
+ *     enqueued on it; calls return without synchronising unless noted.
+ *   - Workspaces are caller-allocated device buffers sized by the matching
+ *     *_workspace_size query; the library performs no allocation.
+ *   - Return value: MF_OK or an error code; mf_last_error() describes the last
+ *     failure on the calling thread.  Errors detected inside kernels (singular
+ *     stencils, blow-up) are reported through status outputs, not return codes.
+ */
+#ifndef MESHFREE_B200_H
+#define MESHFREE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_ABI_VERSION 1
+
+#define MF_OK 0
+#define MF_ERR_ARG 1
+#define MF_ERR_CUDA 2
+#define MF_ERR_UNSUPPORTED 3
+#define MF_ERR_WORKSPACE 4
+
+/* limits of the batched shape kernel */
+#define MF_MAX_DIM 3
+#define MF_MAX_FAMILIES 16
+#define MF_MAX_MONOMIALS 128
+
+/* family kinds (_phs_batch.py:22-25) and scale codes (_phs_batch.py:27-29) */
+#define MF_KIND_IDENTITY 0
+#define MF_KIND_D1 1
+#define MF_KIND_D2 2
+#define MF_KIND_LAPLACIAN 3
+#define MF_SCALE_NONE 0
+#define MF_SCALE_NEAREST 1
+#define MF_SCALE_SUPPORT 2
+
+/* shape-solve modes */
+#define MF_PHS_REPLAY 0 /* reference op order, no FMA: ~bitwise with the reference */
+#define MF_PHS_FAST 1   /* FMA elimination, parallel back-substitution */
+#define MF_PHS_HYBRID 2 /* FAST, then REPLAY for stencils whose conditioning flags them */
+
+int mf_abi_version(void);
+const char* mf_last_error(void);
+/* number of kernels this library has launched in the process (instrumentation) */
+long long mf_launch_count(void);
+/* fp64 pipe probe: blocks x threads threads, each 8 chains of 16*iters DFMA;
+ * *flops receives the flop count of the launch (timing is the caller's). */
+int mf_dfma_probe(int blocks, int threads, int iters, double* out, void* stream, double* flops);
+
+/* ---- stencil selection ------------------------------------------------------
+ * For each target t (targets[t] is a node index) select the n pool nodes with
+ * the smallest (d2, node index), d2 in numpy-einsum rounding order, with the
+ * reference's tie-straddle re-selection and self-first rule
+ * (stencils.py:37-91).  out_idx is T x n int32, row-major, stencil order.
+ * n_straddle (device int64, nullable) receives the number of straddle rows.
+ * Preconditions (checked by the caller as the reference does, stencils.py:28-35):
+ * 1 <= n <= P, 1 <= d <= 3.  pos is N x d f64 row-major; targets/pool int64. */
+int mf_knn_workspace_size(int64_t N, int32_t d, int64_t T, int64_t P, int32_t n, size_t* bytes);
+int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* targets, int64_t T,
+           const int64_t* pool, int64_t P, int32_t n, int32_t* out_idx, int64_t* n_straddle,
+           void* ws, size_t ws_bytes, void* stream);
+
+/* ---- batched polyharmonic RBF-FD weights -----------------------------------
+ * Mirrors batch_phs_weights(pts, rows, stencils, k, even, expos, base_bot,
+ * kinds, ax_a, ax_b, orders, scale_code).  expos (l x d int32), base_bot
+ * (nf x l f64) and kinds/ax_a/ax_b/orders (nf int32) are HOST arrays.
+ * out is m x nf x n f64; status is m int8 (0 ok, 1 singular / non-finite,
+ * 2 degenerate scale); first_fail (device int64, nullable) receives the lowest
+ * failing row index, or INT64 0x7f7f7f7f7f7f7f7f when every row succeeded.
+ * n_replayed (device int64, nullable) counts rows re-solved in REPLAY order
+ * (HYBRID mode). */
+int mf_phs_workspace_size(int64_t m, size_t* bytes);
+int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int64_t* rows,
+                   const int32_t* stencils, int64_t m, int32_t n, int32_t k, int32_t even,
+                   const int32_t* expos, int32_t l, const double* base_bot,
+                   const int32_t* kinds, const int32_t* ax_a, const int32_t* ax_b,
+                   const int32_t* orders, int32_t nf, int32_t scale_code, int32_t mode,
+                   double* out, int8_t* status, int64_t* first_fail, int64_t* n_replayed,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* ---- canonical CSR -------------------------------------------------------------
+ * Structure of WeightStore.matrix: N x N, rows ascending, columns ascending
+ * (stable for equal columns), rows only for the stored nodes `rows` (unique).
+ * indptr (N+1 int32), indices (m*n int32), perm (m*n int32: source slot
+ * r*n + j in stencil order of each CSR entry).  dup_flag (device int32,
+ * nullable) is set non-zero if `rows` repeats a node. */
+int mf_csr_workspace_size(int64_t N, size_t* bytes);
+int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_t m, int32_t n, int64_t N,
+                 int32_t* indptr, int32_t* indices, int32_t* perm, int32_t* dup_flag,
+                 void* ws, size_t ws_bytes, void* stream);
+/* data[p] = w[perm[p]] (one family, w in stencil order). */
+int mf_csr_gather(const int32_t* perm, const double* w, int64_t nnz, double* data, void* stream);
+
+/* ---- explicit application ----------------------------------------------------
+ * y_i = sum over row i in storage order, sequential from 0.0, no FMA: bitwise
+ * equal to scipy's csr_matvec on the same CSR.  mf_apply reads the CSR
+ * directly; the ELL-32 "apply plan" (mf_ell_build) stores the same entries
+ * slot-major in tiles of 32 rows (entry j of row r at ((r/32)*W + j)*32 + r%32,
+ * W = max row length) so a warp's loads are contiguous, and mf_ell_apply /
+ * mf_heat_steps stream it at HBM rate.  Row lengths still come from indptr. */
+int mf_apply(const int32_t* indptr, const int32_t* indices, const double* data,
+             const double* u, double* y, int64_t N, void* stream);
+/* y[k] = (A u)[sel[k]] for a list of rows (WeightStore.apply). */
+int mf_apply_rows(const int32_t* indptr, const int32_t* indices, const double* data,
+                  const double* u, const int64_t* sel, int64_t count, double* y, void* stream);
+/* ell_idx (ceil(N/32)*32*W int32) and ell_val (same count f64, nullable) */
+int mf_ell_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                 int32_t W, int32_t* ell_idx, double* ell_val, void* stream);
+int mf_ell_apply(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+                 int32_t W, const double* u, double* y, void* stream);
+
+/* ---- explicit Neumann closure ---------------------------------------------------
+ * For listed node i with stencil row r = node_row[i] (stencils m x n int32,
+ * stencil order): c_j = sum_a normals[i,a] * w_d1[a*mn + r*n + j]
+ * (storage.py:226-234), pivot guard |c_0| < 1e-12 ||c||_2 (storage.py:240-245),
+ * value (gn[k] - sum_{j>=1} c_j u[st_j]) / c_0 (storage.py:246-250).
+ * out (count, nullable) receives the values; u_scatter (N, nullable) gets
+ * u_scatter[nodes[k]] = value; peak (uint64, nullable) is max-ed with the
+ * IEEE bits of |value|; bad (device int64) receives the lowest k whose pivot
+ * is negligible, else 0x7f7f7f7f7f7f7f7f. */
+typedef struct {
+    const int32_t* stencils;
+    int32_t n;
+    const double* w_d1; /* d planes of m*n weights (families d1_0..d1_{d-1}) */
+    int64_t mn;
+    int32_t d;
+    const double* normals; /* N x d */
+    const int64_t* nodes;  /* count */
+    const int64_t* node_row; /* N */
+    const double* gn;      /* count */
+    int64_t count;
+    const uint8_t* mask;   /* N: 1 for listed nodes (excluded from the heat kernel's peak) */
+} mf_neumann_t;
+int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, double* u_scatter,
+                      uint64_t* peak, int64_t* bad, void* stream);
+
+/* ---- forward-Euler heat stepping -----------------------------------------------
+ * `steps` steps of drivers.py:88-110 over the ELL-32 plan of the laplacian,
+ * with step-invariant data: interior and dirichlet masks (uint8, N),
+ * Dirichlet values g_dir (N), optional source (N, nullable: the reference's
+ * `+ 0.0`), optional Neumann closure (nm, nullable; values from the previous
+ * field, as drivers.py:99-102).  u (N) is advanced in place using scratch (N).
+ * peaks (steps uint64, device) receives the IEEE bits of max|u| after each
+ * step (NaN sorts above inf); once a step exceeds 1e12 or is non-finite the
+ * remaining steps do no work.  Dirichlet values must already be applied to u
+ * before the first call (drivers.py:84-85). */
+int mf_heat_steps(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+                  int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
+                  const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
+                  int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MESHFREE_B200_H */

@@ -1,0 +1,69 @@
+"""meshfree-b200: the RBF-FD hot path of the reference ``meshfree`` package on B200.
+
+Public API mirrors the reference:
+
+    NodeSet, find_closest_stencils          stencil selection  (csrc/knn.cu)
+    RbfFd, Polyharmonic, compute_weights    batched shape solve (csrc/phs.cu)
+    WeightStore.matrix / apply / apply_all  canonical CSR + explicit apply (csrc/sparse.cu)
+    run_heat_explicit                       fused forward-Euler stepping (csrc/sparse.cu)
+
+All compute runs in hand-written sm_100a kernels behind the C ABI declared in
+include/meshfree_b200.h; there is no CPU fallback.
+"""
+
+from .approx import (
+    FirstDerivative,
+    Identity,
+    Laplacian,
+    MonomialBasis,
+    Operator,
+    Polyharmonic,
+    RbfFd,
+    SecondDerivative,
+    graded_lex_exponents,
+    monomial_count,
+)
+from .drivers import run_heat_explicit
+from .errors import (
+    ConfigError,
+    GeometryError,
+    InstabilityError,
+    MeshfreeError,
+    NumericalError,
+    StencilError,
+    StorageError,
+    WeightError,
+)
+from .nodeset import NodeSet
+from .stencils import find_closest_stencils
+from .storage import DeviceCSR, WeightStore, compute_weights, expand_families
+
+__all__ = [
+    "ConfigError",
+    "DeviceCSR",
+    "FirstDerivative",
+    "GeometryError",
+    "Identity",
+    "InstabilityError",
+    "Laplacian",
+    "MeshfreeError",
+    "MonomialBasis",
+    "NodeSet",
+    "NumericalError",
+    "Operator",
+    "Polyharmonic",
+    "RbfFd",
+    "SecondDerivative",
+    "StencilError",
+    "StorageError",
+    "WeightError",
+    "WeightStore",
+    "compute_weights",
+    "expand_families",
+    "find_closest_stencils",
+    "graded_lex_exponents",
+    "monomial_count",
+    "run_heat_explicit",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,134 @@
+"""ctypes binding of libmeshfree_b200.so (the C ABI in include/meshfree_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every GPU entry point raises.  Device memory, streams and the caching
+allocator come from PyTorch; the library itself never allocates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmeshfree_b200.so")
+
+MF_OK = 0
+MF_ERR_UNSUPPORTED = 3
+MF_MAX_FAMILIES = 16
+MF_MAX_MONOMIALS = 128
+PHS_REPLAY, PHS_FAST, PHS_HYBRID = 0, 1, 2
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+
+class NeumannT(ctypes.Structure):
+    _fields_ = [
+        ("stencils", _P), ("n", _I32), ("w_d1", _P), ("mn", _I64), ("d", _I32),
+        ("normals", _P), ("nodes", _P), ("node_row", _P), ("gn", _P), ("count", _I64),
+        ("mask", _P),
+    ]
+
+
+_SIGNATURES = {
+    "mf_abi_version": ([], _I32),
+    "mf_last_error": ([], ctypes.c_char_p),
+    "mf_launch_count": ([], ctypes.c_longlong),
+    "mf_dfma_probe": ([_I32, _I32, _I32, _P, _P, ctypes.POINTER(_D)], _I32),
+    "mf_knn_workspace_size": ([_I64, _I32, _I64, _I64, _I32, ctypes.POINTER(_SZ)], _I32),
+    "mf_knn": ([_P, _I64, _I32, _P, _I64, _P, _I64, _I32, _P, _P, _P, _SZ, _P], _I32),
+    "mf_phs_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_phs_weights": ([_P, _I64, _I32, _P, _P, _I64, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P,
+                        _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P], _I32),
+    "mf_csr_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_csr_build": ([_P, _P, _I64, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P], _I32),
+    "mf_csr_gather": ([_P, _P, _I64, _P, _P], _I32),
+    "mf_apply": ([_P, _P, _P, _P, _P, _I64, _P], _I32),
+    "mf_apply_rows": ([_P, _P, _P, _P, _P, _I64, _P, _P], _I32),
+    "mf_ell_build": ([_P, _P, _P, _I64, _I32, _P, _P, _P], _I32),
+    "mf_ell_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P], _I32),
+    "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
+    "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
+                       _I64, _P, _P, _P, _P], _I32),
+}
+
+EXPORTS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    """The CUDA library is missing, failed to load, or rejected a call."""
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the ctypes handle; raises if the .so is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryError(
+            f"{path} is not built; run `python -m paper_1912_13282_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.mf_abi_version() != 1:
+        raise LibraryError("libmeshfree_b200 ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str):
+    if rc != MF_OK:
+        msg = load().mf_last_error().decode(errors="replace")
+        raise LibraryError(f"{what} failed (code {rc}): {msg}")
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise LibraryError("no CUDA device: the meshfree B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    """Raw pointer of a tensor / numpy array (None passes NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device())
+
+
+def to_device(a, dtype) -> torch.Tensor:
+    """Host array or tensor -> contiguous device tensor of `dtype`."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device(), dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device(), non_blocking=False).contiguous()
+
+
+SENTINEL_OK = int.from_bytes(b"\x7f" * 8, "little", signed=True)

@@ -1,0 +1,623 @@
+// Stencil selection: uniform-grid cell-list kNN with warp-level exact top-k.
+//
+// Replaces find_closest_stencils (geometry/stencils.py:19-93).  The reference
+// takes a kd-tree window of k = min(n+8, P) candidates, re-orders them by
+// (d2, node index) with d2 in numpy einsum's rounding order, re-selects
+// "straddle" rows (k-th and n-th candidates equal to 1e-12) from a ball query
+// ordered by (np.sum d2, index), and moves the target to slot 0.  The final
+// order is an exact function of those keys, so this kernel computes the same
+// mathematical object directly:
+//
+//   1. pool points are counting-sorted into a uniform grid (~2 per cell);
+//   2. one warp per target (targets processed in cell order for locality)
+//      gathers the points of a cube of cells around the target, whose inner
+//      radius bounds every point left outside;
+//   3. the K smallest keys are found exactly: bisection on d2 shrinks the
+//      candidate set to a window just above K, and the survivors are ranked
+//      by (d2, index) in shared memory; the cube grows until the K-th key is
+//      provably inside it;
+//   4. straddle rows are re-run with the sequential-sum metric (K = n);
+//   5. the self-first rule is applied before the row is written.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace mf {
+
+constexpr double KNN_OCC = 2.0;   // mean pool points per grid cell
+constexpr int KNN_WARPS = 4;      // warps per block
+constexpr int KNN_MAXIT = 16;     // register candidate slots per lane (512 per warp)
+constexpr int KNN_SCAP = 256;     // survivor capacity per warp (shared memory)
+constexpr int KNN_RMAX = 255;     // cell-row ranges per cube held in shared memory
+constexpr int KNN_WIN = 16;       // bisection stops at <= K + WIN survivors
+
+struct GridParams {
+    double lo[3], cw[3], inv[3];
+    int G[3];
+    int ncell;
+};
+
+struct KnnArgs {
+    const double* pos;
+    int d;
+    const int64_t* targets;
+    const GridParams* gp;
+    const int32_t* start;  // ncell + 1
+    const double* spos;    // pool points sorted by cell, AoS d doubles
+    const int32_t* sidx;   // node index of each sorted point
+    const uint8_t* in_pool;
+    int n;
+    int K;
+    int32_t* out;
+    int32_t* straddle_list;
+    unsigned long long* straddle_count;
+};
+
+// numpy.einsum("tkd,tkd->tk") order on this numpy build (probed):
+// 1D x0; 2D x0 + x1; 3D (x0 + x2) + x1.  np.sum order (straddle path): sequential.
+template <bool SEQ>
+__device__ __forceinline__ double metric(const double* q, const double* p, int d) {
+    double dx = __dsub_rn(q[0], p[0]);
+    double s = __dmul_rn(dx, dx);
+    if (d == 1) return s;
+    double dy = __dsub_rn(q[1], p[1]);
+    if (d == 2) return __dadd_rn(s, __dmul_rn(dy, dy));
+    double dz = __dsub_rn(q[2], p[2]);
+    if (SEQ) return __dadd_rn(__dadd_rn(s, __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return __dadd_rn(__dadd_rn(s, __dmul_rn(dz, dz)), __dmul_rn(dy, dy));
+}
+
+__device__ __forceinline__ int cell_coord(const GridParams& g, int a, double x) {
+    double t = (x - g.lo[a]) * g.inv[a];
+    if (!(t >= 0.0)) return 0;
+    if (t >= (double)g.G[a]) return g.G[a] - 1;
+    int c = (int)t;
+    return c < g.G[a] ? c : g.G[a] - 1;
+}
+
+__device__ __forceinline__ int cell_of(const GridParams& g, const double* x, int d) {
+    int c = 0;
+    for (int a = 0; a < d; ++a) c = c * g.G[a] + cell_coord(g, a, x[a]);
+    return c;
+}
+
+// key order: (d2, node index, candidate id) -- the candidate id only separates
+// repeated pool entries, which carry the same node index
+__device__ __forceinline__ bool key_lt(double d1, int i1, int c1, double d2, int i2, int c2) {
+    if (d1 != d2) return d1 < d2;
+    if (i1 != i2) return i1 < i2;
+    return c1 < c2;
+}
+
+struct Box {
+    int clo[3], chi[3];
+    double limit;  // K-th key must be <= limit to be provably inside
+    bool all;
+};
+
+__device__ __forceinline__ Box make_box(const GridParams& g, const double* p, const int* home, int rho, int d) {
+    Box b;
+    double inner = INFINITY;
+    b.all = true;
+    for (int a = 0; a < 3; ++a) {
+        b.clo[a] = 0;
+        b.chi[a] = 0;
+    }
+    for (int a = 0; a < d; ++a) {
+        b.clo[a] = max(home[a] - rho, 0);
+        b.chi[a] = min(home[a] + rho, g.G[a] - 1);
+        if (b.clo[a] > 0) {
+            b.all = false;
+            double dist = p[a] - (g.lo[a] + (double)b.clo[a] * g.cw[a]);
+            inner = fmin(inner, fmax(dist, 0.0));
+        }
+        if (b.chi[a] < g.G[a] - 1) {
+            b.all = false;
+            double dist = (g.lo[a] + (double)(b.chi[a] + 1) * g.cw[a]) - p[a];
+            inner = fmin(inner, fmax(dist, 0.0));
+        }
+    }
+    b.limit = b.all ? INFINITY : inner * inner * (1.0 - 1e-12);
+    return b;
+}
+
+// range r of the cube: the cells along the last axis at fixed leading coordinates
+__device__ __forceinline__ void range_bounds(const GridParams& g, const Box& b, int d, int r, const int32_t* start,
+                                             int& lo, int& hi) {
+    int lead = 0;
+    int rem = r;
+    int coords[2] = {0, 0};
+    for (int a = d - 2; a >= 0; --a) {
+        int span = b.chi[a] - b.clo[a] + 1;
+        coords[a] = b.clo[a] + rem % span;
+        rem /= span;
+    }
+    for (int a = 0; a < d - 1; ++a) lead = lead * g.G[a] + coords[a];
+    int c_lo = lead * g.G[d - 1] + b.clo[d - 1];
+    int c_hi = lead * g.G[d - 1] + b.chi[d - 1];
+    lo = start[c_lo];
+    hi = start[c_hi + 1];
+}
+
+__device__ __forceinline__ int box_ranges(const Box& b, int d) {
+    int R = 1;
+    for (int a = 0; a < d - 1; ++a) R *= b.chi[a] - b.clo[a] + 1;
+    return R;
+}
+
+struct WarpSmem {
+    int32_t roff[KNN_RMAX + 1];  // candidate offset of each range (prefix)
+    int32_t rlo[KNN_RMAX];       // first item of each range
+    double sd2[KNN_SCAP];
+    int32_t sid[KNN_SCAP];
+    int32_t scid[KNN_SCAP];
+    int32_t sel[KNN_SCAP];
+    double seld2[KNN_SCAP];
+};
+
+// Exact K smallest keys by repeated arg-min over the cube (any size, any ties).
+// Writes sel/seld2[0..K) and returns the K-th d2.
+template <bool SEQ>
+__device__ double extract_topk(const KnnArgs& a, const Box& b, const double* p, int K, WarpSmem& sm, int lane) {
+    const GridParams& g = *a.gp;
+    const int d = a.d;
+    const int R = box_ranges(b, d);
+    double pd = -INFINITY;
+    int pi = -1, pc = -1;
+    for (int k = 0; k < K; ++k) {
+        double bd = INFINITY;
+        int bi = 0x7fffffff, bc = 0x7fffffff;
+        int cid = 0;
+        for (int r = 0; r < R; ++r) {
+            int lo, hi;
+            range_bounds(g, b, d, r, a.start, lo, hi);
+            for (int q = lo + lane; q < hi; q += 32) {
+                double d2 = metric<SEQ>(a.spos + (size_t)q * d, p, d);
+                int id = a.sidx[q];
+                int c = cid + (q - lo);
+                if (key_lt(pd, pi, pc, d2, id, c) && key_lt(d2, id, c, bd, bi, bc)) {
+                    bd = d2;
+                    bi = id;
+                    bc = c;
+                }
+            }
+            cid += hi - lo;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            double od = __shfl_xor_sync(FULL, bd, o);
+            int oi = __shfl_xor_sync(FULL, bi, o);
+            int oc = __shfl_xor_sync(FULL, bc, o);
+            if (key_lt(od, oi, oc, bd, bi, bc)) {
+                bd = od;
+                bi = oi;
+                bc = oc;
+            }
+        }
+        if (lane == 0 && k < KNN_SCAP) {
+            sm.sel[k] = bi;
+            sm.seld2[k] = bd;
+        }
+        pd = bd;
+        pi = bi;
+        pc = bc;
+    }
+    __syncwarp();
+    return pd;
+}
+
+template <bool SEQ>
+__global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const int32_t* __restrict__ order,
+                                                            int64_t count, const unsigned long long* count_dev,
+                                                            int K) {
+    __shared__ WarpSmem smem[KNN_WARPS];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    WarpSmem& sm = smem[wib];
+    const GridParams g = *a.gp;
+    const int d = a.d;
+    const int n = a.n;
+    if (count_dev) count = (int64_t)*count_dev;
+    // cube half-width giving ~1.5 K candidates
+    int rho0 = (int)ceil((pow(1.5 * K / KNN_OCC, 1.0 / d) - 1.0) * 0.5);
+    if (rho0 < 1) rho0 = 1;
+
+    for (int64_t w = (int64_t)blockIdx.x * KNN_WARPS + wib; w < count; w += (int64_t)gridDim.x * KNN_WARPS) {
+        const int trow = order[w];
+        const int64_t tnode = a.targets[trow];
+        double p[3] = {0.0, 0.0, 0.0};
+        for (int ax = 0; ax < d; ++ax) p[ax] = a.pos[tnode * d + ax];
+        int home[3] = {0, 0, 0};
+        for (int ax = 0; ax < d; ++ax) home[ax] = cell_coord(g, ax, p[ax]);
+
+        double dK = 0.0;
+        for (int rho = rho0;; ++rho) {
+            Box b = make_box(g, p, home, rho, d);
+            const int R = box_ranges(b, d);
+            // candidate count and range prefix offsets
+            int M = 0;
+            bool small = R <= KNN_RMAX;
+            if (small) {
+                for (int r0 = 0; r0 < R; r0 += 32) {
+                    int r = r0 + lane;
+                    int lo = 0, hi = 0;
+                    if (r < R) range_bounds(g, b, d, r, a.start, lo, hi);
+                    int len = hi - lo;
+                    int incl = len;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int v = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    if (r < R) {
+                        sm.roff[r] = M + incl - len;
+                        sm.rlo[r] = lo;
+                    }
+                    M += __shfl_sync(FULL, incl, 31);
+                }
+                if (lane == 0) sm.roff[R] = M;
+                __syncwarp();
+            } else {
+                for (int r = lane; r < R; r += 32) {
+                    int lo, hi;
+                    range_bounds(g, b, d, r, a.start, lo, hi);
+                    M += hi - lo;
+                }
+                M = warp_sum(M);
+            }
+            if (M < K) continue;
+
+            bool done = false;
+            if (small && M <= 32 * KNN_MAXIT) {
+                // ---- register path: candidates c = it*32 + lane
+                double cd[KNN_MAXIT];
+                int ci[KNN_MAXIT];
+                int rc = 0;
+#pragma unroll
+                for (int it = 0; it < KNN_MAXIT; ++it) {
+                    int c = it * 32 + lane;
+                    cd[it] = INFINITY;
+                    ci[it] = 0x7fffffff;
+                    if (it * 32 < M && c < M) {
+                        while (sm.roff[rc + 1] <= c) ++rc;
+                        int q = sm.rlo[rc] + (c - sm.roff[rc]);
+                        cd[it] = metric<SEQ>(a.spos + (size_t)q * d, p, d);
+                        ci[it] = a.sidx[q];
+                    }
+                }
+                auto count_le = [&](double t) {
+                    int c = 0;
+#pragma unroll
+                    for (int it = 0; it < KNN_MAXIT; ++it)
+                        if (it * 32 < M) c += __popc(__ballot_sync(FULL, cd[it] <= t));
+                    return c;
+                };
+                const double L = b.limit;
+                int cL = count_le(L);
+                if (cL < K && !b.all) continue;  // K-th key not provably inside: grow
+                double hi = L, lo = -1.0;
+                int chi = cL;
+                if (hi == INFINITY) {
+                    double mx = 0.0;
+#pragma unroll
+                    for (int it = 0; it < KNN_MAXIT; ++it)
+                        if (cd[it] != INFINITY) mx = fmax(mx, cd[it]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+                    hi = mx;
+                    chi = count_le(hi);
+                }
+                for (int iter = 0; iter < 80 && chi > K + KNN_WIN; ++iter) {
+                    double mid = lo < 0.0 ? 0.5 * hi : lo + 0.5 * (hi - lo);
+                    if (!(mid < hi) || (lo >= 0.0 && !(mid > lo))) break;
+                    int c = count_le(mid);
+                    if (c >= K) {
+                        hi = mid;
+                        chi = c;
+                    } else {
+                        lo = mid;
+                    }
+                }
+                if (chi >= K && chi <= KNN_SCAP) {
+                    // compact survivors (d2 <= hi) into shared memory
+                    int base = 0;
+#pragma unroll
+                    for (int it = 0; it < KNN_MAXIT; ++it) {
+                        if (it * 32 < M) {
+                            bool keep = cd[it] <= hi;
+                            unsigned bal = __ballot_sync(FULL, keep);
+                            if (keep) {
+                                int at = base + __popc(bal & ((1u << lane) - 1u));
+                                sm.sd2[at] = cd[it];
+                                sm.sid[at] = ci[it];
+                                sm.scid[at] = it * 32 + lane;
+                            }
+                            base += __popc(bal);
+                        }
+                    }
+                    __syncwarp();
+                    const int S = base;
+                    for (int e = lane; e < S; e += 32) {
+                        double de = sm.sd2[e];
+                        int ie = sm.sid[e], ce = sm.scid[e];
+                        int rank = 0;
+                        for (int f = 0; f < S; ++f) rank += key_lt(sm.sd2[f], sm.sid[f], sm.scid[f], de, ie, ce);
+                        if (rank < K) {
+                            sm.sel[rank] = ie;
+                            sm.seld2[rank] = de;
+                        }
+                    }
+                    __syncwarp();
+                    dK = sm.seld2[K - 1];
+                    done = true;
+                }
+            }
+            if (!done) {
+                dK = extract_topk<SEQ>(a, b, p, K, sm, lane);
+                if (!b.all && !(dK <= b.limit)) continue;
+            }
+            break;
+        }
+
+        // straddle rows: the (K-1)-th and (n-1)-th keys tie to 1e-12 (stencils.py:61-65)
+        if (!SEQ && K > n) {
+            double edge = sm.seld2[n - 1];
+            if (fabs(dK - edge) <= 1e-18 + 1e-12 * edge) {
+                if (lane == 0) {
+                    unsigned long long slot = atomicAdd(a.straddle_count, 1ull);
+                    a.straddle_list[slot] = trow;
+                }
+            }
+        }
+        // self-first (stencils.py:77-91)
+        if (a.in_pool[tnode]) {
+            int first = sm.sel[0];
+            if (first != (int)tnode) {
+                int hit = 0x7fffffff;
+                for (int j = lane; j < n; j += 32)
+                    if (sm.sel[j] == (int)tnode) hit = min(hit, j);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) hit = min(hit, __shfl_xor_sync(FULL, hit, o));
+                int last = hit == 0x7fffffff ? n - 1 : hit;
+                // shift sel[0..last) right by one; serial but tiny (rare rows)
+                if (lane == 0) {
+                    for (int j = last; j > 0; --j) sm.sel[j] = sm.sel[j - 1];
+                    sm.sel[0] = (int)tnode;
+                }
+                __syncwarp();
+            }
+        }
+        int32_t* row = a.out + (int64_t)trow * n;
+        for (int j = lane; j < n; j += 32) row[j] = sm.sel[j];
+        __syncwarp();
+    }
+}
+
+// ---- grid construction ------------------------------------------------------
+__global__ void knn_bbox(const double* __restrict__ pos, int d, const int64_t* __restrict__ pool, int64_t P,
+                         unsigned long long* bb) {
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = pool[i];
+        for (int a = 0; a < d; ++a) {
+            double x = pos[node * d + a];
+            mn[a] = fmin(mn[a], x);
+            mx[a] = fmax(mx[a], x);
+        }
+    }
+    for (int a = 0; a < d; ++a) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(FULL, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(FULL, mx[a], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bb[a], ordered_bits(mn[a]));
+            atomicMax(&bb[3 + a], ordered_bits(mx[a]));
+        }
+    }
+}
+
+__global__ void knn_params(const unsigned long long* bb, int d, int64_t P, GridParams* gp) {
+    GridParams g;
+    double lo[3], hi[3];
+    double vol = 1.0;
+    int nd = 0;
+    for (int a = 0; a < 3; ++a) {
+        g.lo[a] = 0.0;
+        g.cw[a] = 0.0;
+        g.inv[a] = 0.0;
+        g.G[a] = 1;
+    }
+    for (int a = 0; a < d; ++a) {
+        lo[a] = from_ordered_bits(bb[a]);
+        hi[a] = from_ordered_bits(bb[3 + a]);
+        if (hi[a] > lo[a]) {
+            vol *= hi[a] - lo[a];
+            ++nd;
+        }
+    }
+    double w = nd ? pow(vol * KNN_OCC / (double)P, 1.0 / nd) : 1.0;
+    double ncell = 1.0;
+    for (int a = 0; a < d; ++a) {
+        double ext = hi[a] - lo[a];
+        double G = 1.0;
+        if (ext > 0.0 && w > 0.0) G = fmin(fmax(floor(ext / w), 1.0), 2097152.0);
+        // keep the total within the workspace bound P/occ + 1
+        if (ncell * G > (double)P / KNN_OCC + 1.0) G = fmax(1.0, floor(((double)P / KNN_OCC + 1.0) / ncell));
+        ncell *= G;
+        g.G[a] = (int)G;
+        g.lo[a] = lo[a];
+        g.cw[a] = ext > 0.0 ? ext / G : 0.0;
+        g.inv[a] = ext > 0.0 ? G / ext : 0.0;
+    }
+    g.ncell = (int)ncell;
+    *gp = g;
+}
+
+__global__ void knn_cells(const double* __restrict__ pos, int d, const int64_t* __restrict__ pool, int64_t P,
+                          const GridParams* __restrict__ gp, int32_t* __restrict__ cell, int32_t* __restrict__ cnt,
+                          uint8_t* __restrict__ in_pool) {
+    const GridParams g = *gp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = pool[i];
+        int c = cell_of(g, pos + node * d, d);
+        cell[i] = c;
+        atomicAdd(&cnt[c], 1);
+        in_pool[node] = 1;
+    }
+}
+
+__global__ void knn_scatter(const double* __restrict__ pos, int d, const int64_t* __restrict__ pool, int64_t P,
+                            const int32_t* __restrict__ cell, int32_t* __restrict__ cursor, double* __restrict__ spos,
+                            int32_t* __restrict__ sidx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = pool[i];
+        int at = atomicAdd(&cursor[cell[i]], 1);
+        for (int a = 0; a < d; ++a) spos[(size_t)at * d + a] = pos[node * d + a];
+        sidx[at] = (int32_t)node;
+    }
+}
+
+__global__ void knn_target_keys(const double* __restrict__ pos, int d, const int64_t* __restrict__ targets, int64_t T,
+                                const GridParams* __restrict__ gp, int32_t* __restrict__ key, int32_t* __restrict__ val) {
+    const GridParams g = *gp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+        key[t] = cell_of(g, pos + targets[t] * d, d);
+        val[t] = (int32_t)t;
+    }
+}
+
+inline int grid_for(int64_t work, int threads, int per_sm = 8) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)sms * per_sm;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+struct KnnLayout {
+    GridParams* gp;
+    unsigned long long* bb;
+    unsigned long long* straddle_count;
+    int32_t* cnt;     // ncell_max + 1 (counts, then starts)
+    int32_t* cursor;  // ncell_max
+    int32_t* cell;    // P
+    double* spos;     // P * d
+    int32_t* sidx;    // P
+    uint8_t* in_pool; // N
+    int32_t* tkey[2];
+    int32_t* tval[2];
+    int32_t* straddle_list;  // T
+    char* cub_tmp;
+    size_t cub_bytes;
+};
+
+inline int64_t ncell_max(int64_t P) { return (int64_t)((double)P / KNN_OCC) + 2; }
+
+inline size_t knn_cub_bytes(int64_t P, int64_t T) {
+    size_t a = 0, b = 0;
+    int64_t nc = ncell_max(P);
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int)(nc + 1));
+    cub::DoubleBuffer<int32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, k, v, (int)(T > 0 ? T : 1));
+    return a > b ? a : b;
+}
+
+inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
+    KnnLayout L;
+    int64_t nc = ncell_max(P);
+    L.gp = ar.take<GridParams>(1);
+    L.bb = ar.take<unsigned long long>(6);
+    L.straddle_count = ar.take<unsigned long long>(1);
+    L.cnt = ar.take<int32_t>(nc + 1);
+    L.cursor = ar.take<int32_t>(nc + 1);
+    L.cell = ar.take<int32_t>(P);
+    L.spos = ar.take<double>((size_t)P * d);
+    L.sidx = ar.take<int32_t>(P);
+    L.in_pool = ar.take<uint8_t>(N);
+    for (int i = 0; i < 2; ++i) {
+        L.tkey[i] = ar.take<int32_t>(T);
+        L.tval[i] = ar.take<int32_t>(T);
+    }
+    L.straddle_list = ar.take<int32_t>(T);
+    L.cub_bytes = knn_cub_bytes(P, T);
+    L.cub_tmp = ar.take<char>(L.cub_bytes);
+    return L;
+}
+
+}  // namespace mf
+
+using namespace mf;
+
+extern "C" int mf_knn_workspace_size(int64_t N, int32_t d, int64_t T, int64_t P, int32_t n, size_t* bytes) {
+    (void)n;
+    if (!bytes || N < 0 || T < 0 || P < 1 || d < 1 || d > MF_MAX_DIM) {
+        set_error("mf_knn_workspace_size: bad arguments");
+        return MF_ERR_ARG;
+    }
+    Arena ar{nullptr, 0, 0, true};
+    knn_layout(ar, N, d, T, P);
+    *bytes = ar.off;
+    return MF_OK;
+}
+
+extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* targets, int64_t T,
+                      const int64_t* pool, int64_t P, int32_t n, int32_t* out_idx, int64_t* n_straddle, void* ws,
+                      size_t ws_bytes, void* stream) {
+    MF_REQUIRE(d >= 1 && d <= MF_MAX_DIM, "mf_knn: dimension %d not in 1..3", d);
+    MF_REQUIRE(n >= 1 && n <= P, "mf_knn: stencil size %d vs pool %lld", n, (long long)P);
+    MF_REQUIRE(N < 2147483647 && P < 2147483647 && T < 2147483647, "mf_knn: sizes exceed int32 indexing");
+    MF_REQUIRE(n + 8 <= KNN_SCAP, "mf_knn: stencil size %d above the kernel limit %d", n, KNN_SCAP - 8);
+    cudaStream_t st = (cudaStream_t)stream;
+    Arena ar{(char*)ws, ws_bytes, 0, false};
+    KnnLayout L = knn_layout(ar, N, d, T, P);
+    if (!ws || !ar.ok()) {
+        set_error("mf_knn: workspace too small (%zu < %zu)", ws_bytes, ar.off);
+        return MF_ERR_WORKSPACE;
+    }
+    if (n_straddle) MF_CUDA_CHECK(cudaMemsetAsync(n_straddle, 0, sizeof(int64_t), st));
+    if (T == 0) return MF_OK;
+    const int64_t nc = ncell_max(P);
+    MF_CUDA_CHECK(cudaMemsetAsync(L.bb, 0xff, 3 * sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.bb + 3, 0, 3 * sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.straddle_count, 0, sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.cnt, 0, sizeof(int32_t) * (nc + 1), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.in_pool, 0, (size_t)N, st));
+    knn_bbox<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.bb);
+    MF_LAUNCH_CHECK();
+    knn_params<<<1, 1, 0, st>>>(L.bb, d, P, L.gp);
+    MF_LAUNCH_CHECK();
+    knn_cells<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.gp, L.cell, L.cnt, L.in_pool);
+    MF_LAUNCH_CHECK();
+    size_t cb = L.cub_bytes;
+    MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.cnt, L.cnt, (int)(nc + 1), st));
+    MF_CUDA_CHECK(cudaMemcpyAsync(L.cursor, L.cnt, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, st));
+    knn_scatter<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.cell, L.cursor, L.spos, L.sidx);
+    MF_LAUNCH_CHECK();
+    knn_target_keys<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, T, L.gp, L.tkey[0], L.tval[0]);
+    MF_LAUNCH_CHECK();
+    cub::DoubleBuffer<int32_t> kb(L.tkey[0], L.tkey[1]), vb(L.tval[0], L.tval[1]);
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < nc) ++bits;
+    cb = L.cub_bytes;
+    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, kb, vb, (int)T, 0, bits, st));
+    const int32_t* order = vb.Current();
+
+    const int K = (int)(n + 8 < P ? n + 8 : P);
+    KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
+    knn_kernel<false><<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, 0, st>>>(a, order, T, nullptr, K);
+    MF_LAUNCH_CHECK();
+    if (K > n) {
+        // straddle rows: top-n by the sequential-sum metric (stencils.py:67-75)
+        knn_kernel<true><<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, 0, st>>>(a, L.straddle_list, T,
+                                                                                L.straddle_count, n);
+        MF_LAUNCH_CHECK();
+    }
+    if (n_straddle)
+        MF_CUDA_CHECK(cudaMemcpyAsync(n_straddle, L.straddle_count, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    return MF_OK;
+}

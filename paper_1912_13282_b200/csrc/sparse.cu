@@ -1,0 +1,395 @@
+// Canonical CSR assembly, explicit operator application and the fused
+// forward-Euler heat step (sm_100a).
+//
+//   mf_csr_build / mf_csr_gather   WeightStore.matrix      (storage.py:156-170)
+//   mf_apply                       WeightStore.apply_all   (storage.py:186-188)
+//   mf_apply_rows                  WeightStore.apply       (storage.py:174-184)
+//   mf_heat_steps                  run_heat_explicit loop  (drivers.py:87-110)
+//   mf_neumann_values              WeightStore.neumann_value (storage.py:226-250)
+//
+// Summation contract: scipy's csr_matvec accumulates each row in storage
+// order from 0.0 with separately rounded multiply and add; the kernels here
+// keep exactly that order (__dmul_rn/__dadd_rn), so the results are bitwise
+// equal to the reference on the same CSR.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace mf {
+
+constexpr double BLOWUP_LIMIT = 1e12;  // drivers.py:18
+
+// ---------------------------------------------------------------------------
+// CSR structure
+// ---------------------------------------------------------------------------
+__global__ void csr_mark_rows(const int64_t* __restrict__ rows, int64_t m, int64_t N,
+                              int32_t* __restrict__ node_row, int32_t* __restrict__ dup) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = rows[r];
+        if (node < 0 || node >= N) {
+            atomicExch(dup, 2);
+            continue;
+        }
+        int old = atomicCAS(&node_row[node], -1, (int)r);
+        if (old != -1) atomicExch(dup, 1);
+    }
+}
+
+// node_row[i] (-1 = not stored) -> row length n or 0, in place (plus a 0 at N)
+__global__ void csr_counts(int32_t* __restrict__ node_row, int64_t N, int n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= N; i += (int64_t)gridDim.x * blockDim.x)
+        node_row[i] = (i < N && node_row[i] >= 0) ? n : 0;
+}
+
+// One warp per stored row: rank each stencil member by (column, slot) and
+// scatter it to its canonical position (stable lexsort, storage.py:161).
+__global__ void csr_fill(const int64_t* __restrict__ rows, const int32_t* __restrict__ st, int64_t m, int n,
+                         const int32_t* __restrict__ indptr, int32_t* __restrict__ indices,
+                         int32_t* __restrict__ perm) {
+    extern __shared__ int32_t sh_cols[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    int32_t* cols = sh_cols + wib * n;
+    for (int64_t r = (int64_t)blockIdx.x * wpb + wib; r < m; r += (int64_t)gridDim.x * wpb) {
+        const int32_t* src = st + r * n;
+        for (int j = lane; j < n; j += 32) cols[j] = src[j];
+        __syncwarp();
+        const int64_t base = indptr[rows[r]];
+        for (int j = lane; j < n; j += 32) {
+            int32_t c = cols[j];
+            int rank = 0;
+            for (int i = 0; i < n; ++i) {
+                int32_t ci = cols[i];
+                rank += (ci < c) || (ci == c && i < j);
+            }
+            indices[base + rank] = c;
+            perm[base + rank] = (int32_t)(r * n + j);
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void csr_gather_k(const int32_t* __restrict__ perm, const double* __restrict__ w, int64_t nnz,
+                             double* __restrict__ data) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+        data[p] = w[perm[p]];
+}
+
+// ---------------------------------------------------------------------------
+// Row application.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double row_sum(const double* __restrict__ dv, const int32_t* __restrict__ iv,
+                                          int lo, int hi, const double* __restrict__ u) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int p = lo; p < hi; ++p) acc = __dadd_rn(acc, __dmul_rn(dv[p], __ldg(u + iv[p])));
+    return acc;
+}
+
+// CSR, thread per row (general layout; the ELL plan below is the fast path)
+__global__ void apply_csr_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const double* __restrict__ data, const double* __restrict__ u,
+                            double* __restrict__ y, int64_t N) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = row_sum(data, indices, indptr[i], indptr[i + 1], u);
+}
+
+__global__ void apply_rows_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                             const double* __restrict__ data, const double* __restrict__ u,
+                             const int64_t* __restrict__ sel, int64_t count, double* __restrict__ y) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = sel[k];
+        y[k] = row_sum(data, indices, indptr[i], indptr[i + 1], u);
+    }
+}
+
+// ELL-32 plan: entry j of row r lives at ((r/32)*W + j)*32 + r%32.
+__global__ void ell_build_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const double* __restrict__ data, int64_t N, int W, int32_t* __restrict__ ell_idx,
+                            double* __restrict__ ell_val) {
+    const int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t tile = e / (32 * (int64_t)W);
+        int rem = (int)(e - tile * 32 * (int64_t)W);
+        int j = rem >> 5, lane = rem & 31;
+        int64_t r = tile * 32 + lane;
+        int32_t ci = 0;
+        double v = 0.0;
+        if (r < N) {
+            int32_t lo = indptr[r], len = indptr[r + 1] - lo;
+            if (j < len) {
+                ci = indices[lo + j];
+                if (data) v = data[lo + j];
+            }
+        }
+        if (ell_idx) ell_idx[e] = ci;
+        if (ell_val) ell_val[e] = v;
+    }
+}
+
+struct HeatStep {
+    const uint8_t* interior;
+    const uint8_t* dirichlet;
+    const double* g_dir;
+    const double* source;
+    const uint8_t* peak_skip;             // rows whose final value comes later (Neumann)
+    double dt, D;
+    unsigned long long* peak_out;         // this step's max|u| bits
+    const unsigned long long* peak_prev;  // previous step's, or null
+};
+
+__device__ __forceinline__ bool step_blew_up(const unsigned long long* prev) {
+    return prev && *prev > (unsigned long long)__double_as_longlong(BLOWUP_LIMIT);
+}
+
+// Thread per row over the ELL-32 plan: each warp-wide load of slot j is one
+// contiguous 256 B (values) / 128 B (indices) segment.
+template <bool HEAT>
+__global__ void __launch_bounds__(256) ell_apply_k(const int32_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ ell_idx,
+                                                   const double* __restrict__ ell_val, int64_t N, int W,
+                                                   const double* __restrict__ u, double* __restrict__ y,
+                                                   HeatStep hs) {
+    if (HEAT && step_blew_up(hs.peak_prev)) return;
+    unsigned long long peak = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ((N + 31) & ~31ll); r += stride) {
+        const bool live = r < N;
+        int len = live ? indptr[r + 1] - indptr[r] : 0;
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double v;
+        if (!HEAT) {
+            double acc = 0.0;
+#pragma unroll 5
+            for (int j = 0; j < len; ++j) {
+                double a = __ldcs(ell_val + base + 32 * j);
+                int32_t c = __ldcs(ell_idx + base + 32 * j);
+                acc = __dadd_rn(acc, __dmul_rn(a, __ldg(u + c)));
+            }
+            if (live) y[r] = acc;
+        } else if (live) {
+            v = u[r];
+            if (hs.interior[r]) {
+                double acc = 0.0;
+#pragma unroll 5
+                for (int j = 0; j < len; ++j) {
+                    double a = __ldcs(ell_val + base + 32 * j);
+                    int32_t c = __ldcs(ell_idx + base + 32 * j);
+                    acc = __dadd_rn(acc, __dmul_rn(a, __ldg(u + c)));
+                }
+                double f = hs.source ? hs.source[r] : 0.0;
+                // u + dt * (D * lap_u + f)   (drivers.py:93-96)
+                v = __dadd_rn(v, __dmul_rn(hs.dt, __dadd_rn(__dmul_rn(hs.D, acc), f)));
+            }
+            if (hs.dirichlet[r]) v = hs.g_dir[r];
+            y[r] = v;
+            if (!(hs.peak_skip && hs.peak_skip[r])) {
+                unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+                peak = b > peak ? b : peak;
+            }
+        }
+    }
+    if (HEAT) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long ob = __shfl_xor_sync(FULL, peak, o);
+            peak = ob > peak ? ob : peak;
+        }
+        if ((threadIdx.x & 31) == 0 && peak) atomicMax(hs.peak_out, peak);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Explicit Neumann closure (storage.py:226-250), one thread per listed node.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double neumann_coef(const mf_neumann_t& nm, int64_t i, int64_t base, int j) {
+    // c = n_0 w_0 + n_1 w_1 + ... accumulated per axis (storage.py:231-234)
+    double c = __dmul_rn(nm.normals[i * nm.d + 0], nm.w_d1[base + j]);
+    for (int a = 1; a < nm.d; ++a)
+        c = __dadd_rn(c, __dmul_rn(nm.normals[i * nm.d + a], nm.w_d1[(int64_t)a * nm.mn + base + j]));
+    return c;
+}
+
+__global__ void neumann_k(mf_neumann_t nm, const double* __restrict__ u, double* __restrict__ out,
+                          double* __restrict__ u_scatter, unsigned long long* peak, int64_t* bad,
+                          const unsigned long long* peak_prev) {
+    if (step_blew_up(peak_prev)) return;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nm.count; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = nm.nodes[k];
+        const int64_t base = nm.node_row[i] * nm.n;
+        double ss = 0.0;
+        for (int j = 0; j < nm.n; ++j) {
+            double c = neumann_coef(nm, i, base, j);
+            ss = fma(c, c, ss);
+        }
+        const double pivot = neumann_coef(nm, i, base, 0);
+        double val;
+        if (fabs(pivot) < 1e-12 * sqrt(ss)) {
+            if (bad) atomicMin((unsigned long long*)bad, (unsigned long long)k);
+            val = 0.0;
+        } else {
+            double acc = nm.gn[k];
+            for (int j = 1; j < nm.n; ++j)
+                acc = __dsub_rn(acc, __dmul_rn(neumann_coef(nm, i, base, j), u[nm.stencils[base + j]]));
+            val = __ddiv_rn(acc, pivot);
+        }
+        if (out) out[k] = val;
+        if (u_scatter) u_scatter[i] = val;
+        if (peak) atomicMax(peak, (unsigned long long)__double_as_longlong(fabs(val)));
+    }
+}
+
+inline int grid_for(int64_t work, int threads, int per_sm = 16) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)sms * per_sm;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace mf
+
+using namespace mf;
+
+extern "C" int mf_csr_workspace_size(int64_t N, size_t* bytes) {
+    if (!bytes || N < 0) {
+        set_error("mf_csr_workspace_size: bad arguments");
+        return MF_ERR_ARG;
+    }
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
+    Arena ar{nullptr, 0, 0, true};
+    ar.take<int32_t>((size_t)N + 1);
+    ar.take<int32_t>((size_t)N + 1);
+    ar.take<char>(scan_bytes);
+    *bytes = ar.off;
+    return MF_OK;
+}
+
+extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_t m, int32_t n, int64_t N,
+                            int32_t* indptr, int32_t* indices, int32_t* perm, int32_t* dup_flag, void* ws,
+                            size_t ws_bytes, void* stream) {
+    MF_REQUIRE(n >= 1 && m >= 0 && N >= 0, "mf_csr_build: bad shape");
+    MF_REQUIRE((double)m * n < 2147483647.0, "mf_csr_build: nnz %lld exceeds int32 indexing", (long long)(m * n));
+    cudaStream_t st = (cudaStream_t)stream;
+    MF_REQUIRE(N < 2147483647, "mf_csr_build: N exceeds int32 indexing");
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)(N + 1));
+    Arena ar{(char*)ws, ws_bytes, 0, false};
+    int32_t* node_row = ar.take<int32_t>((size_t)N + 1);
+    int32_t* counts = ar.take<int32_t>((size_t)N + 1);
+    char* scan_tmp = ar.take<char>(scan_bytes);
+    if (!ws || !ar.ok()) {
+        set_error("mf_csr_build: workspace too small (%zu < %zu)", ws_bytes, ar.off);
+        return MF_ERR_WORKSPACE;
+    }
+    MF_CUDA_CHECK(cudaMemsetAsync(node_row, 0xff, sizeof(int32_t) * (N + 1), st));
+    if (dup_flag) MF_CUDA_CHECK(cudaMemsetAsync(dup_flag, 0, sizeof(int32_t), st));
+    if (m > 0) {
+        csr_mark_rows<<<grid_for(m, 256), 256, 0, st>>>(rows, m, N, node_row, dup_flag ? dup_flag : node_row + N);
+        MF_LAUNCH_CHECK();
+    }
+    MF_CUDA_CHECK(cudaMemcpyAsync(counts, node_row, sizeof(int32_t) * (N + 1), cudaMemcpyDeviceToDevice, st));
+    csr_counts<<<grid_for(N + 1, 256), 256, 0, st>>>(counts, N, n);
+    MF_LAUNCH_CHECK();
+    MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, indptr, (int)(N + 1), st));
+    if (m > 0) {
+        const int wpb = 8;
+        size_t sh = sizeof(int32_t) * (size_t)n * wpb;
+        MF_REQUIRE(sh <= 48 * 1024, "mf_csr_build: stencil size %d too large", n);
+        csr_fill<<<grid_for(m, wpb, 64), wpb * 32, sh, st>>>(rows, stencils, m, n, indptr, indices, perm);
+        MF_LAUNCH_CHECK();
+    }
+    return MF_OK;
+}
+
+extern "C" int mf_csr_gather(const int32_t* perm, const double* w, int64_t nnz, double* data, void* stream) {
+    MF_REQUIRE(nnz >= 0, "mf_csr_gather: bad nnz");
+    if (nnz == 0) return MF_OK;
+    csr_gather_k<<<grid_for(nnz, 256), 256, 0, (cudaStream_t)stream>>>(perm, w, nnz, data);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_apply(const int32_t* indptr, const int32_t* indices, const double* data, const double* u,
+                        double* y, int64_t N, void* stream) {
+    MF_REQUIRE(N >= 0, "mf_apply: bad N");
+    if (N == 0) return MF_OK;
+    apply_csr_k<<<grid_for(N, 256), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, u, y, N);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_apply_rows(const int32_t* indptr, const int32_t* indices, const double* data, const double* u,
+                             const int64_t* sel, int64_t count, double* y, void* stream) {
+    MF_REQUIRE(count >= 0, "mf_apply_rows: bad count");
+    if (count == 0) return MF_OK;
+    apply_rows_k<<<grid_for(count, 128), 128, 0, (cudaStream_t)stream>>>(indptr, indices, data, u, sel, count, y);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_ell_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                            int32_t W, int32_t* ell_idx, double* ell_val, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0, "mf_ell_build: bad shape");
+    int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    if (total == 0) return MF_OK;
+    ell_build_k<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, N, W, ell_idx, ell_val);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+static int ell_grid(int64_t N) { return grid_for(((N + 31) / 32) * 32, 256, 8); }
+
+extern "C" int mf_ell_apply(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+                            int32_t W, const double* u, double* y, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0, "mf_ell_apply: bad shape");
+    if (N == 0) return MF_OK;
+    ell_apply_k<false><<<ell_grid(N), 256, 0, (cudaStream_t)stream>>>(indptr, ell_idx, ell_val, N, W, u, y, HeatStep{});
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, double* u_scatter,
+                                 uint64_t* peak, int64_t* bad, void* stream) {
+    MF_REQUIRE(nm && nm->n >= 1 && nm->d >= 1 && nm->d <= MF_MAX_DIM && nm->count >= 0,
+               "mf_neumann_values: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bad) MF_CUDA_CHECK(cudaMemsetAsync(bad, 0x7f, sizeof(int64_t), st));
+    if (nm->count == 0) return MF_OK;
+    neumann_k<<<grid_for(nm->count, 128), 128, 0, st>>>(*nm, u, out, u_scatter, (unsigned long long*)peak, bad,
+                                                        nullptr);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_heat_steps(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+                             int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
+                             const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
+                             int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream) {
+    MF_REQUIRE(N >= 0 && steps >= 0 && W >= 0, "mf_heat_steps: bad arguments");
+    if (steps == 0 || N == 0) return MF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    MF_CUDA_CHECK(cudaMemsetAsync(peaks, 0, sizeof(uint64_t) * steps, st));
+    const int grid = ell_grid(N);
+    const bool has_nm = nm && nm->count > 0;
+    double* buf[2] = {u, scratch};
+    for (int64_t s = 0; s < steps; ++s) {
+        const unsigned long long* prev = s ? (const unsigned long long*)(peaks + s - 1) : nullptr;
+        unsigned long long* cur = (unsigned long long*)(peaks + s);
+        HeatStep hs{interior, dirichlet, g_dir, source, has_nm ? nm->mask : nullptr, dt, diffusivity, cur, prev};
+        double* u_old = buf[s & 1];
+        double* u_new = buf[(s + 1) & 1];
+        ell_apply_k<true><<<grid, 256, 0, st>>>(indptr, ell_idx, ell_val, N, W, u_old, u_new, hs);
+        MF_LAUNCH_CHECK();
+        if (has_nm) {
+            neumann_k<<<grid_for(nm->count, 128), 128, 0, st>>>(*nm, u_old, nullptr, u_new, cur, nullptr, prev);
+            MF_LAUNCH_CHECK();
+        }
+    }
+    if (steps & 1) MF_CUDA_CHECK(cudaMemcpyAsync(u, scratch, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    return MF_OK;
+}

@@ -1,0 +1,189 @@
+"""Explicit forward-Euler heat stepping on the GPU.
+
+Drop-in for the reference's run_heat_explicit (drivers.py:48-111): same
+arguments, checks, boundary handling order (interior Euler update, Dirichlet
+assignment at t_new, Neumann closure from the previous field) and the same
+InstabilityError at the first step whose max|u| exceeds 1e12 or is not
+finite.  Step-invariant data (constant Dirichlet/Neumann values and source)
+runs as one ``mf_heat_steps`` call over the ELL-32 plan of the laplacian;
+time-dependent callables are evaluated on the host at the reference's times
+and the device steps one at a time.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, InstabilityError, NumericalError
+
+BLOWUP_LIMIT = 1e12
+
+
+def _bc_values(value, points, t):
+    if callable(value):
+        out = value(points, t)
+        return np.broadcast_to(np.asarray(out, dtype=float), (points.shape[0],))
+    return np.full(points.shape[0], float(value))
+
+
+def _tag_indices(nodes, bc_dict):
+    out = {}
+    for tag, value in (bc_dict or {}).items():
+        idx = nodes.select(int(tag))
+        if idx.size == 0:
+            raise ConfigError(f"boundary condition for tag {tag} matches no node")
+        out[int(tag)] = (idx, value)
+    return out
+
+
+def _instability(step, peak):
+    return InstabilityError(
+        step,
+        f"field peak {peak:.2e} exceeds {BLOWUP_LIMIT:.0e}; forward Euler "
+        "needs roughly dt <= h_min^2 / (2 d D)",
+    )
+
+
+def run_heat_explicit(
+    nodes,
+    store,
+    *,
+    dt: float,
+    steps: int,
+    diffusivity: float = 1.0,
+    source=None,
+    dirichlet=None,
+    neumann=None,
+    initial=0.0,
+    return_device: bool = False,
+):
+    """Forward-Euler march of du/dt = D lap(u) + f (drivers.py:48-111).
+
+    Returns the field after ``steps`` steps as a host array (or the device
+    tensor with ``return_device=True``).
+    """
+    if dt <= 0 or steps < 0:
+        raise ConfigError("need dt > 0 and steps >= 0")
+    lib = _lib.load()
+    n = len(nodes)
+    pts = nodes.positions
+    u = np.empty(n)
+    if callable(initial):
+        u[:] = np.asarray(initial(pts), dtype=float)
+    else:
+        u[:] = np.asarray(initial, dtype=float)
+
+    diri = _tag_indices(nodes, dirichlet)
+    neum = _tag_indices(nodes, neumann)
+    for idx, value in diri.values():
+        u[idx] = _bc_values(value, pts[idx], 0.0)
+
+    dev = _lib.device()
+    u_d = _lib.to_device(u, torch.float64)
+    if steps == 0:
+        return u_d if return_device else u
+
+    lap = store.matrix("laplacian")
+    ell_idx, ell_val, W = lap.ell()
+    interior = np.zeros(n, dtype=np.uint8)
+    interior[nodes.interior_indices()] = 1
+    interior_d = _lib.to_device(interior, torch.uint8)
+    dmask = np.zeros(n, dtype=np.uint8)
+    for idx, _ in diri.values():
+        dmask[idx] = 1
+    dmask_d = _lib.to_device(dmask, torch.uint8)
+
+    time_dep = callable(source) or any(callable(v) for _, v in diri.values()) or any(
+        callable(v) for _, v in neum.values())
+
+    def dirichlet_vals(t):
+        g = np.zeros(n)
+        for idx, value in diri.values():
+            g[idx] = _bc_values(value, pts[idx], t)
+        return g
+
+    # Neumann closure: nodes in tag order, normals, stencil weights (drivers.py:99-102)
+    nm = None
+    if neum:
+        nm_nodes = np.concatenate([idx for idx, _ in neum.values()]).astype(np.int64)
+        for i in nm_nodes:
+            store._row(int(i))
+        normals = np.stack([nodes.normal(int(i)) for i in nm_nodes])
+        plane = store.neumann_plane(nodes.dim)
+        normals_d = _lib.to_device(normals, torch.float64)
+        _, bad = store.neumann_values_device(nm_nodes, normals, np.zeros(nm_nodes.shape[0]), u_d,
+                                             plane=plane, normals_d=normals_d)
+        if bad is not None:
+            raise NumericalError(
+                f"node {int(nm_nodes[bad])}: negligible self-weight in the normal derivative; "
+                "the stencil cannot enforce a Neumann condition explicitly"
+            )
+        nm_mask = np.zeros(n, dtype=np.uint8)
+        nm_mask[nm_nodes] = 1
+        nm_keep = dict(nodes=_lib.to_device(nm_nodes, torch.int64), plane=plane, normals=normals_d,
+                       mask=_lib.to_device(nm_mask, torch.uint8), node_row=store.node_row_device())
+
+        def neumann_vals(t):
+            return np.concatenate([_bc_values(v, pts[idx], t) for idx, v in neum.values()])
+
+        def make_nm(g_d):
+            return _lib.NeumannT(store.stencils_device.data_ptr(), store.n, plane.data_ptr(), plane.shape[1],
+                                 nodes.dim, normals_d.data_ptr(), nm_keep["nodes"].data_ptr(),
+                                 nm_keep["node_row"].data_ptr(), g_d.data_ptr(), nm_nodes.shape[0],
+                                 nm_keep["mask"].data_ptr())
+
+    scratch = torch.empty(n, dtype=torch.float64, device=dev)
+    peaks = torch.empty(steps, dtype=torch.int64, device=dev)
+
+    def launch(k_steps, g_d, src_d, nm_struct, peak_view):
+        _lib.check(lib.mf_heat_steps(
+            lap.indptr_device.data_ptr(), ell_idx.data_ptr(), ell_val.data_ptr(), n, W,
+            interior_d.data_ptr(), dmask_d.data_ptr(), g_d.data_ptr(), _lib.ptr(src_d), float(dt),
+            float(diffusivity), None if nm_struct is None else ctypes.byref(nm_struct), k_steps,
+            u_d.data_ptr(), scratch.data_ptr(), peak_view.data_ptr(), _lib.stream_ptr()), "mf_heat_steps")
+
+    if not time_dep:
+        g_d = _lib.to_device(dirichlet_vals(dt), torch.float64)
+        src_d = None if source is None else _lib.to_device(_bc_values(source, pts, 0.0), torch.float64)
+        nm_struct = None
+        if neum:
+            gn_d = _lib.to_device(neumann_vals(dt), torch.float64)
+            nm_struct = make_nm(gn_d)
+        launch(steps, g_d, src_d, nm_struct, peaks)
+    else:
+        for step in range(steps):
+            t_new = (step + 1) * dt
+            g_d = _lib.to_device(dirichlet_vals(t_new), torch.float64)
+            src_d = None if source is None else _lib.to_device(_bc_values(source, pts, step * dt), torch.float64)
+            nm_struct = None
+            if neum:
+                gn_d = _lib.to_device(neumann_vals(t_new), torch.float64)
+                nm_struct = make_nm(gn_d)
+            launch(1, g_d, src_d, nm_struct, peaks[step:step + 1])
+            if (step + 1) % 64 == 0 or step + 1 == steps:
+                if _first_bad(peaks[: step + 1]) is not None:
+                    break
+
+    bad = _first_bad(peaks)
+    if bad is not None:
+        step, peak = bad
+        raise _instability(step, peak)
+    return u_d if return_device else u_d.cpu().numpy()
+
+
+def _first_bad(peaks: torch.Tensor):
+    """(1-based step, peak) of the first step with max|u| > 1e12 or non-finite, else None."""
+    limit_bits = int(np.float64(BLOWUP_LIMIT).view(np.int64))
+    bad = torch.nonzero(peaks > limit_bits)
+    if bad.numel() == 0:
+        return None
+    s = int(bad[0, 0].item())
+    peak = float(np.int64(peaks[s].item()).view(np.float64))
+    if math.isnan(peak):
+        peak = float("nan")
+    return s + 1, peak

@@ -1,0 +1,281 @@
+"""Node container: positions, type tags, boundary normals, stencils.
+
+Mirrors the reference NodeSet (geometry/nodeset.py:25-147): same
+constructor, selectors, accessors and errors.  The difference is storage:
+stencils produced on the GPU stay on the GPU as dense (T, n) int32 blocks, and
+the reference's Python list-of-arrays view (``.stencils``, ``.stencil(i)``)
+is materialised lazily, only when host code asks for it.
+
+Selectors (nodeset.py:8-15): ``None``/``"all"``, ``"interior"``,
+``"boundary"``, an int tag, a list/tuple of tags, a boolean mask of length N,
+or an integer index array (kept in the given order).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import GeometryError, StencilError
+
+
+class _DevicePositions:
+    """Device copy of the positions, shared by NodeSets derived from one another."""
+
+    def __init__(self, positions: np.ndarray):
+        self.host = positions
+        self._dev = None
+
+    def get(self) -> torch.Tensor:
+        if self._dev is None:
+            self._dev = _lib.to_device(self.host, torch.float64)
+        return self._dev
+
+
+class _Block:
+    """Stencils of `nodes` (host int64), either a device (T, n) int32 matrix or host rows."""
+
+    def __init__(self, nodes, mat=None, rows=None):
+        self.nodes = np.asarray(nodes, dtype=np.int64)
+        self.mat = mat
+        self._rows = rows
+        self._host = None
+
+    @property
+    def size(self):
+        if self.mat is not None:
+            return int(self.mat.shape[1])
+        sizes = {len(r) for r in self._rows}
+        return sizes.pop() if len(sizes) == 1 else None
+
+    def host_matrix(self):
+        if self._host is None:
+            self._host = self.mat.cpu().numpy().astype(np.int64)
+        return self._host
+
+    def row(self, k):
+        if self.mat is not None:
+            return self.host_matrix()[k]
+        return self._rows[k]
+
+    def device_matrix(self):
+        if self.mat is None:
+            sizes = {len(r) for r in self._rows}
+            if len(sizes) != 1:
+                raise StencilError(f"stencil sizes differ: {sorted(sizes)}")
+            self.mat = _lib.to_device(np.stack(self._rows).astype(np.int32), torch.int32)
+        return self.mat
+
+
+class NodeSet:
+    def __init__(self, positions, types, normals=None, stencils=None):
+        self.positions = np.ascontiguousarray(positions, dtype=float)
+        if self.positions.ndim != 2:
+            raise GeometryError("positions must be an (N, d) array")
+        n, d = self.positions.shape
+        self.types = np.asarray(types, dtype=np.int64)
+        if self.types.shape != (n,):
+            raise GeometryError("types must be a length-N vector")
+        if normals is None:
+            normals = np.full((n, d), np.nan)
+        self.normals = np.asarray(normals, dtype=float)
+        if self.normals.shape != (n, d):
+            raise GeometryError("normals must be an (N, d) array")
+        self._pos = _DevicePositions(self.positions)
+        self._blocks: list[_Block] = []
+        self._blk = np.full(n, -1, dtype=np.int32)
+        self._row = np.zeros(n, dtype=np.int64)
+        self._list_cache = None
+        if stencils is not None:
+            stencils = list(stencils)
+            if len(stencils) != n:
+                raise GeometryError("stencil list length must match node count")
+            have = [i for i, s in enumerate(stencils) if s is not None]
+            if have:
+                rows = [np.asarray(stencils[i], dtype=np.int64) for i in have]
+                self._add_block(_Block(np.array(have, dtype=np.int64), rows=rows))
+
+    # -- internal stencil bookkeeping ------------------------------------
+
+    def _add_block(self, block: _Block):
+        b = len(self._blocks)
+        self._blocks.append(block)
+        self._blk[block.nodes] = b
+        self._row[block.nodes] = np.arange(block.nodes.shape[0])
+        self._list_cache = None
+
+    def _derive(self) -> "NodeSet":
+        new = NodeSet.__new__(NodeSet)
+        new.positions = self.positions
+        new.types = self.types
+        new.normals = self.normals
+        new._pos = self._pos
+        new._blocks = list(self._blocks)
+        new._blk = self._blk.copy()
+        new._row = self._row.copy()
+        new._list_cache = None
+        return new
+
+    def _with_device_stencils(self, targets, mat: torch.Tensor) -> "NodeSet":
+        new = self._derive()
+        new._add_block(_Block(np.asarray(targets, dtype=np.int64), mat=mat))
+        return new
+
+    def positions_device(self) -> torch.Tensor:
+        return self._pos.get()
+
+    def stencil_matrix_device(self, idx) -> torch.Tensor:
+        """(M, n) int32 device matrix of the stencils of node indices `idx`."""
+        idx = np.asarray(idx, dtype=np.int64)
+        if idx.size == 0:
+            return torch.empty((0, 0), dtype=torch.int32, device=_lib.device())
+        blk = self._blk[idx]
+        missing = np.flatnonzero(blk < 0)
+        if missing.size:
+            raise StencilError(f"node {int(idx[missing[0]])} has no stencil")
+        used = np.unique(blk)
+        sizes = sorted({self._blocks[b].size for b in used} - {None})
+        if len(sizes) != 1 or any(self._blocks[b].size is None for b in used):
+            all_sizes = set()
+            for b in used:
+                blkobj = self._blocks[b]
+                rows = self._row[idx[blk == b]]
+                all_sizes |= {len(blkobj.row(int(k))) for k in rows}
+            if len(all_sizes) != 1:
+                raise StencilError(f"stencil sizes differ: {sorted(all_sizes)}")
+        if used.size == 1:
+            mat = self._blocks[int(used[0])].device_matrix()
+            rows = self._row[idx]
+            if rows.shape[0] == mat.shape[0] and np.array_equal(rows, np.arange(rows.shape[0])):
+                return mat
+            return mat.index_select(0, _lib.to_device(rows, torch.int64))
+        n = sizes[0]
+        out = torch.empty((idx.shape[0], n), dtype=torch.int32, device=_lib.device())
+        for b in used:
+            sel = np.flatnonzero(blk == b)
+            src = self._blocks[int(b)].device_matrix().index_select(0, _lib.to_device(self._row[idx[sel]], torch.int64))
+            out.index_copy_(0, _lib.to_device(sel, torch.int64), src)
+        return out
+
+    # -- basic queries ---------------------------------------------------
+
+    def __len__(self):
+        return self.positions.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.positions.shape[1]
+
+    def interior_indices(self):
+        return np.flatnonzero(self.types > 0)
+
+    def boundary_indices(self):
+        return np.flatnonzero(self.types < 0)
+
+    def select(self, which):
+        """Resolve a node selector (see module docstring) to an index array."""
+        n = len(self)
+        if which is None or (isinstance(which, str) and which == "all"):
+            return np.arange(n)
+        if isinstance(which, str):
+            if which == "interior":
+                return self.interior_indices()
+            if which == "boundary":
+                return self.boundary_indices()
+            raise GeometryError(f"unknown node selector {which!r}")
+        if isinstance(which, (int, np.integer)):
+            return np.flatnonzero(self.types == which)
+        if isinstance(which, (list, tuple, set, frozenset)):
+            mask = np.isin(self.types, list(which))
+            return np.flatnonzero(mask)
+        if isinstance(which, torch.Tensor):
+            which = which.cpu().numpy()
+        arr = np.asarray(which)
+        if arr.dtype == bool:
+            if arr.shape != (n,):
+                raise GeometryError("boolean selector must have length N")
+            return np.flatnonzero(arr)
+        if np.issubdtype(arr.dtype, np.integer):
+            if arr.size and (arr.min() < 0 or arr.max() >= n):
+                raise GeometryError("index selector out of range")
+            return arr.astype(np.int64)
+        raise GeometryError(f"cannot interpret node selector {which!r}")
+
+    def normal(self, i: int):
+        if self.types[i] >= 0:
+            raise GeometryError(f"node {i} is not a boundary node")
+        return self.normals[i]
+
+    @property
+    def stencils(self) -> list:
+        """Reference-style list of N stencils (np.int64 arrays or None), built lazily."""
+        if self._list_cache is None:
+            out = [None] * len(self)
+            for i in np.flatnonzero(self._blk >= 0):
+                out[int(i)] = self.stencil(int(i))
+            self._list_cache = out
+        return self._list_cache
+
+    def stencil(self, i: int):
+        b = self._blk[i]
+        if b < 0:
+            raise StencilError(f"node {i} has no stencil")
+        return np.asarray(self._blocks[b].row(int(self._row[i])), dtype=np.int64)
+
+    def has_stencil(self, i: int) -> bool:
+        return bool(self._blk[i] >= 0)
+
+    # -- derived forms -----------------------------------------------------
+
+    def stencil_matrix(self, indices=None):
+        """Stack stencils of the given nodes into an (M, n) int64 host matrix."""
+        idx = self.select(indices)
+        if idx.size == 0:
+            return np.empty((0, 0), dtype=np.int64)
+        missing = np.flatnonzero(self._blk[idx] < 0)
+        if missing.size:
+            raise StencilError(f"node {int(idx[missing[0]])} has no stencil")
+        rows = [self.stencil(int(i)) for i in idx]
+        sizes = {r.shape[0] for r in rows}
+        if len(sizes) != 1:
+            raise StencilError(f"stencil sizes differ: {sorted(sizes)}")
+        return np.vstack(rows).astype(np.int64)
+
+    def append(self, positions, types, normals=None):
+        """New NodeSet with extra nodes appended; existing stencils kept."""
+        positions = np.atleast_2d(np.asarray(positions, dtype=float))
+        m = positions.shape[0]
+        types = np.broadcast_to(np.asarray(types, dtype=np.int64), (m,))
+        if normals is None:
+            normals = np.full((m, self.dim), np.nan)
+        new = NodeSet(
+            np.concatenate([self.positions, positions], axis=0),
+            np.concatenate([self.types, types]),
+            np.concatenate([self.normals, normals], axis=0),
+        )
+        new._pos = _DevicePositions(new.positions)
+        new._blocks = list(self._blocks)
+        n_old = len(self)
+        new._blk[:n_old] = self._blk
+        new._row[:n_old] = self._row
+        return new
+
+    def with_stencils(self, indices, stencils):
+        """New NodeSet where nodes ``indices[k]`` get ``stencils[k]``."""
+        indices = np.asarray(indices, dtype=np.int64)
+        if isinstance(stencils, torch.Tensor) and stencils.is_cuda:
+            return self._with_device_stencils(indices, stencils.to(torch.int32).contiguous())
+        rows = [np.asarray(s, dtype=np.int64) for s in stencils]
+        new = self._derive()
+        if rows:
+            new._add_block(_Block(indices, rows=rows))
+        return new
+
+    def __repr__(self):
+        nb = len(self.boundary_indices())
+        ni = len(self.interior_indices())
+        return (
+            f"NodeSet(N={len(self)}, d={self.dim}, interior={ni}, "
+            f"boundary={nb}, other={len(self) - ni - nb})"
+        )

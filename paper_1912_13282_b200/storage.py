@@ -1,0 +1,642 @@
+"""Weight tables on the GPU: compute once, apply many times.
+
+Drop-in for the reference's storage module (storage.py:1-409).
+``compute_weights`` runs the batched polyharmonic RBF-FD kernel
+(``mf_phs_weights``) over the stencils of the chosen nodes for a list of
+operator families and returns a :class:`WeightStore` whose weights stay on
+the device.  The reference's public fields (``rows``, ``offsets``, ``cols``,
+``values``, ``node_row``) are available as host arrays, materialised lazily.
+
+``WeightStore.matrix(key)`` returns a :class:`DeviceCSR` with the reference's
+canonical layout (rows ascending, columns ascending, int32 indices, rows only
+for stored nodes -- storage.py:156-170); ``@`` and ``apply_all`` run on the GPU
+and are bitwise equal to scipy's ``csr_matvec`` on the same matrix.
+
+Only the batched configuration of the reference is implemented
+(storage.py:310-322: uniform stencil size, RbfFd + Polyharmonic(k >= 3),
+``solver="lu"``, scale none/nearest/support, elementary operator families).
+Everything else -- the per-node engine loop (storage.py:325-339) -- raises
+ConfigError: there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .approx import (
+    FirstDerivative,
+    Identity,
+    Laplacian,
+    MonomialBasis,
+    Operator,
+    Polyharmonic,
+    RbfFd,
+    SecondDerivative,
+    graded_lex_exponents,
+)
+from .errors import ConfigError, NumericalError, StencilError, StorageError, WeightError
+
+# first-slot pivot guard for the explicit Neumann solve (storage.py:41-42)
+NEUMANN_PIVOT_RTOL = 1e-12
+
+KIND_IDENTITY, KIND_D1, KIND_D2, KIND_LAPLACIAN = 0, 1, 2, 3
+SCALE_CODES = {"none": 0, "nearest": 1, "support": 2}
+MODES = {"replay": _lib.PHS_REPLAY, "fast": _lib.PHS_FAST, "hybrid": _lib.PHS_HYBRID}
+
+
+def _canonical_key(op) -> str:
+    if isinstance(op, Identity):
+        return "identity"
+    if isinstance(op, FirstDerivative):
+        return f"d1_{op.axis}"
+    if isinstance(op, SecondDerivative):
+        return f"d2_{op.a}_{op.b}"
+    if isinstance(op, Laplacian):
+        return "laplacian"
+    raise StorageError(
+        f"{op!r} has no canonical family name; store it as (name, operator)"
+    )
+
+
+def _key_to_operator(key: str, dim: int) -> Operator:
+    if key == "identity":
+        return Identity()
+    if key == "laplacian":
+        return Laplacian()
+    if key.startswith("d1_"):
+        axis = int(key[3:])
+        if not 0 <= axis < dim:
+            raise StorageError(f"axis out of range in family {key!r}")
+        return FirstDerivative(axis)
+    if key.startswith("d2_"):
+        a, b = (int(x) for x in key[3:].split("_"))
+        if not 0 <= a <= b < dim:
+            raise StorageError(f"axes out of range in family {key!r}")
+        return SecondDerivative(a, b)
+    raise StorageError(f"unknown family {key!r}")
+
+
+def expand_families(families, dim: int):
+    """Normalize a family spec list into an ordered {name: operator} dict (storage.py:77-108)."""
+    out: dict[str, Operator] = {}
+
+    def put(key, op):
+        if key in out:
+            raise StorageError(f"family {key!r} requested twice")
+        out[key] = op
+
+    for spec in families:
+        if isinstance(spec, str):
+            if spec == "gradient":
+                for a in range(dim):
+                    put(f"d1_{a}", FirstDerivative(a))
+            elif spec == "hessian":
+                for a in range(dim):
+                    for b in range(a, dim):
+                        put(f"d2_{a}_{b}", SecondDerivative(a, b))
+            else:
+                put(spec, _key_to_operator(spec, dim))
+        elif isinstance(spec, Operator):
+            put(_canonical_key(spec), spec)
+        elif isinstance(spec, tuple) and len(spec) == 2 and isinstance(spec[1], Operator):
+            name = str(spec[0])
+            if "," in name or not name:
+                raise StorageError(f"bad custom family name {name!r}")
+            put(name, spec[1])
+        else:
+            raise StorageError(f"cannot interpret family spec {spec!r}")
+    if not out:
+        raise StorageError("no operator families requested")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device CSR
+# ---------------------------------------------------------------------------
+
+def _to_field(field, N):
+    """Field argument -> (device f64 tensor, was_numpy)."""
+    if isinstance(field, torch.Tensor) and field.is_cuda:
+        return field.to(torch.float64).contiguous(), False
+    arr = np.asarray(field, dtype=float)
+    if arr.shape != (N,):
+        arr = np.broadcast_to(arr, (N,))
+    return _lib.to_device(arr, torch.float64), True
+
+
+class _CsrStructure:
+    """indptr / indices / stencil-slot permutation shared by every family of a store."""
+
+    def __init__(self, n_nodes, rows_d, stencils_d, n):
+        lib = _lib.load()
+        dev = _lib.device()
+        m = int(stencils_d.shape[0])
+        self.N = int(n_nodes)
+        self.n = int(n)
+        self.nnz = m * self.n
+        self.indptr = torch.empty(self.N + 1, dtype=torch.int32, device=dev)
+        self.indices = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+        self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+        dup = torch.zeros(1, dtype=torch.int32, device=dev)
+        size = ctypes.c_size_t(0)
+        _lib.check(lib.mf_csr_workspace_size(self.N, ctypes.byref(size)), "mf_csr_workspace_size")
+        ws = _lib.workspace(size.value)
+        _lib.check(lib.mf_csr_build(rows_d.data_ptr(), stencils_d.data_ptr(), m, self.n, self.N,
+                                    self.indptr.data_ptr(), self.indices.data_ptr(), self.perm.data_ptr(),
+                                    dup.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+                   "mf_csr_build")
+        if int(dup.item()) != 0:
+            raise StorageError("stored rows must be distinct node indices")
+        self._ell_idx = None
+
+    def ell_idx(self):
+        if self._ell_idx is None:
+            self._ell_idx = _ell_build(self.indptr, self.indices, None, self.N, self.n)[0]
+        return self._ell_idx
+
+
+def _ell_build(indptr, indices, data, N, W):
+    lib = _lib.load()
+    total = ((N + 31) // 32) * 32 * W
+    dev = _lib.device()
+    idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev) if indices is not None else None
+    val = torch.empty(max(total, 1), dtype=torch.float64, device=dev) if data is not None else None
+    _lib.check(lib.mf_ell_build(indptr.data_ptr(), _lib.ptr(indices), _lib.ptr(data), N, W,
+                                _lib.ptr(idx), _lib.ptr(val), _lib.stream_ptr()), "mf_ell_build")
+    return idx, val
+
+
+class DeviceCSR:
+    """N x N CSR on the device in the reference's canonical layout.
+
+    ``indptr``/``indices``/``data`` return host numpy arrays (int32, int32,
+    float64, as scipy stores them); ``*_device`` give the device tensors.
+    ``A @ u`` applies on the GPU (numpy in -> numpy out, CUDA tensor in ->
+    CUDA tensor out).
+    """
+
+    def __init__(self, structure: _CsrStructure, data_d: torch.Tensor):
+        self._s = structure
+        self.data_device = data_d
+        self.shape = (structure.N, structure.N)
+        self._host = {}
+        self._ell_val = None
+
+    @property
+    def nnz(self) -> int:
+        return self._s.nnz
+
+    @property
+    def indptr_device(self):
+        return self._s.indptr
+
+    @property
+    def indices_device(self):
+        return self._s.indices[: self.nnz]
+
+    def _get(self, name, t):
+        if name not in self._host:
+            self._host[name] = t.cpu().numpy()
+        return self._host[name]
+
+    @property
+    def indptr(self):
+        return self._get("indptr", self._s.indptr)
+
+    @property
+    def indices(self):
+        return self._get("indices", self._s.indices[: self.nnz])
+
+    @property
+    def data(self):
+        return self._get("data", self.data_device[: self.nnz])
+
+    def ell(self):
+        """(ell_idx, ell_val, W): the ELL-32 apply plan of this matrix."""
+        if self._ell_val is None:
+            self._ell_val = _ell_build(self._s.indptr, None, self.data_device, self._s.N, self._s.n)[1]
+        return self._s.ell_idx(), self._ell_val, self._s.n
+
+    def apply_device(self, u_d: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        lib = _lib.load()
+        N = self._s.N
+        y = out if out is not None else torch.empty(N, dtype=torch.float64, device=u_d.device)
+        idx, val, W = self.ell()
+        _lib.check(lib.mf_ell_apply(self._s.indptr.data_ptr(), idx.data_ptr(), val.data_ptr(), N, W,
+                                    u_d.data_ptr(), y.data_ptr(), _lib.stream_ptr()), "mf_ell_apply")
+        return y
+
+    def apply_csr_device(self, u_d: torch.Tensor) -> torch.Tensor:
+        """Same product straight from the CSR arrays (mf_apply)."""
+        lib = _lib.load()
+        y = torch.empty(self._s.N, dtype=torch.float64, device=u_d.device)
+        _lib.check(lib.mf_apply(self._s.indptr.data_ptr(), self._s.indices.data_ptr(),
+                                self.data_device.data_ptr(), u_d.data_ptr(), y.data_ptr(), self._s.N,
+                                _lib.stream_ptr()), "mf_apply")
+        return y
+
+    def __matmul__(self, field):
+        u_d, host = _to_field(field, self._s.N)
+        y = self.apply_device(u_d)
+        return y.cpu().numpy() if host else y
+
+    def to_scipy(self):
+        import scipy.sparse
+
+        return scipy.sparse.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+
+    tocsr = to_scipy
+
+    def __repr__(self):
+        return f"DeviceCSR(shape={self.shape}, nnz={self.nnz})"
+
+
+# ---------------------------------------------------------------------------
+# weight store
+# ---------------------------------------------------------------------------
+
+class _LazyValues(dict):
+    """{family: flat f64 host array aligned with cols}, copied from the device on first access."""
+
+    def __init__(self, store):
+        super().__init__()
+        self._store = store
+
+    def __getitem__(self, key):
+        if not dict.__contains__(self, key):
+            t = self._store._values_d[key]
+            dict.__setitem__(self, key, t.reshape(-1).cpu().numpy())
+        return dict.__getitem__(self, key)
+
+    def __contains__(self, key):
+        return key in self._store._values_d
+
+    def keys(self):
+        return self._store._values_d.keys()
+
+    def __iter__(self):
+        return iter(self._store._values_d)
+
+    def __len__(self):
+        return len(self._store._values_d)
+
+    def items(self):
+        return [(k, self[k]) for k in self._store._values_d]
+
+    def values(self):
+        return [self[k] for k in self._store._values_d]
+
+
+class WeightStore:
+    """Per-node stencil weights for a set of operator families, on the device.
+
+    Weights are kept in stencil order (self first) as (m, n) float64 tensors;
+    sparse-matrix views sort each row by column index, the canonical layout
+    the implicit assembly uses, so explicit and assembled applications agree
+    bitwise (storage.py:111-118).
+    """
+
+    def __init__(self, n_nodes, rows, stencils_d, values_d, n, positions_d=None):
+        self.n_nodes = int(n_nodes)
+        self._rows = np.asarray(rows, dtype=np.int64)
+        self.stencils_device = stencils_d
+        self._values_d = values_d
+        self.n = int(n)
+        self.node_row = np.full(self.n_nodes, -1, dtype=np.int64)
+        self.node_row[self._rows] = np.arange(self._rows.shape[0])
+        self.values = _LazyValues(self)
+        self._cols = None
+        self._structure = None
+        self._matrices: dict[str, DeviceCSR] = {}
+        self._rows_d = None
+        self._node_row_d = None
+
+    # -- reference fields -------------------------------------------------
+
+    @property
+    def rows(self):
+        return self._rows
+
+    @property
+    def offsets(self):
+        return np.arange(self._rows.shape[0] + 1, dtype=np.int64) * self.n
+
+    @property
+    def stencil_sizes(self):
+        return np.full(self._rows.shape[0], self.n, dtype=np.int64)
+
+    @property
+    def cols(self):
+        if self._cols is None:
+            self._cols = self.stencils_device.reshape(-1).cpu().numpy().astype(np.int64)
+        return self._cols
+
+    @property
+    def families(self):
+        return list(self._values_d.keys())
+
+    def values_device(self, key: str) -> torch.Tensor:
+        return self._family(key)
+
+    def rows_device(self):
+        if self._rows_d is None:
+            self._rows_d = _lib.to_device(self._rows, torch.int64)
+        return self._rows_d
+
+    def node_row_device(self):
+        if self._node_row_d is None:
+            self._node_row_d = _lib.to_device(self.node_row, torch.int64)
+        return self._node_row_d
+
+    def _row(self, i: int) -> int:
+        r = self.node_row[i]
+        if r < 0:
+            raise StorageError(f"no weights stored for node {i}")
+        return int(r)
+
+    def _family(self, key: str) -> torch.Tensor:
+        try:
+            return self._values_d[key]
+        except KeyError:
+            raise StorageError(
+                f"family {key!r} not stored; available: {', '.join(self.families)}"
+            ) from None
+
+    def stencil(self, i: int):
+        r = self._row(i)
+        return self.cols[r * self.n:(r + 1) * self.n]
+
+    def weights(self, key: str, i: int):
+        """Weight vector for one node, aligned with its stencil."""
+        self._family(key)
+        r = self._row(i)
+        return self.values[key][r * self.n:(r + 1) * self.n]
+
+    def matrix(self, key: str) -> DeviceCSR:
+        """Canonical CSR view: N x N, rows only for stored nodes."""
+        if key not in self._matrices:
+            vals = self._family(key)
+            if self._structure is None:
+                self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n)
+            s = self._structure
+            data = torch.empty(max(s.nnz, 1), dtype=torch.float64, device=vals.device)
+            _lib.check(_lib.load().mf_csr_gather(s.perm.data_ptr(), vals.data_ptr(), s.nnz, data.data_ptr(),
+                                                 _lib.stream_ptr()), "mf_csr_gather")
+            self._matrices[key] = DeviceCSR(s, data)
+        return self._matrices[key]
+
+    # -- explicit application ---------------------------------------------
+
+    def apply(self, key: str, field, i: int) -> float:
+        """(L u)(p_i) from stored weights; matches the assembled matrix row bitwise."""
+        mat = self.matrix(key)
+        if self.node_row[i] < 0:
+            raise StorageError(f"no weights stored for node {i}")
+        u_d, _ = _to_field(field, self.n_nodes)
+        sel = torch.tensor([int(i)], dtype=torch.int64, device=u_d.device)
+        y = torch.empty(1, dtype=torch.float64, device=u_d.device)
+        _lib.check(_lib.load().mf_apply_rows(mat.indptr_device.data_ptr(), mat.indices_device.data_ptr(),
+                                             mat.data_device.data_ptr(), u_d.data_ptr(), sel.data_ptr(), 1,
+                                             y.data_ptr(), _lib.stream_ptr()), "mf_apply_rows")
+        return float(y.item())
+
+    def apply_all(self, key: str, field):
+        """(L u) at every stored node as a length-N vector (zeros elsewhere)."""
+        return self.matrix(key) @ field
+
+    def gradient(self, field, i: int):
+        d = self._dim()
+        return np.array([self.apply(f"d1_{a}", field, i) for a in range(d)])
+
+    def divergence(self, vec_field, i: int) -> float:
+        vec_field = np.asarray(vec_field, dtype=float)
+        d = self._dim()
+        acc = 0.0
+        for a in range(d):
+            acc += self.apply(f"d1_{a}", vec_field[:, a], i)
+        return acc
+
+    def vector_laplacian(self, vec_field, i: int):
+        vec_field = np.asarray(vec_field, dtype=float)
+        d = vec_field.shape[1]
+        return np.array([self.apply("laplacian", vec_field[:, a], i) for a in range(d)])
+
+    def grad_div(self, vec_field, i: int):
+        """grad(div u) at node i; needs the hessian families."""
+        vec_field = np.asarray(vec_field, dtype=float)
+        d = self._dim()
+        out = np.zeros(d)
+        for a in range(d):
+            for b in range(d):
+                key = f"d2_{min(a, b)}_{max(a, b)}"
+                out[a] += self.apply(key, vec_field[:, b], i)
+        return out
+
+    def _dim(self) -> int:
+        axes = [int(k[3:]) for k in self._values_d if k.startswith("d1_")]
+        if not axes:
+            raise StorageError("no first-derivative families stored")
+        return max(axes) + 1
+
+    # -- boundary handling ---------------------------------------------------
+
+    def normal_combination(self, i: int, normal):
+        """Stencil-ordered weights of the normal derivative at node i."""
+        normal = np.asarray(normal, dtype=float)
+        acc = None
+        for a, na in enumerate(normal):
+            part = na * self.weights(f"d1_{a}", i)
+            acc = part if acc is None else acc + part
+        return acc
+
+    def neumann_plane(self, d: int) -> torch.Tensor:
+        """(d, m*n) stacked d1_* weights for the Neumann kernel."""
+        for a in range(d):
+            self._family(f"d1_{a}")
+        return torch.stack([self._values_d[f"d1_{a}"].reshape(-1) for a in range(d)]).contiguous()
+
+    def neumann_values_device(self, nodes_idx, normals, gn, u_d, *, plane=None, normals_d=None):
+        """Batched neumann_value on the GPU -> (values tensor, lowest bad list position or None)."""
+        lib = _lib.load()
+        nodes_idx = np.asarray(nodes_idx, dtype=np.int64)
+        for i in nodes_idx:
+            self._row(int(i))
+        d = normals.shape[1]
+        plane = self.neumann_plane(d) if plane is None else plane
+        nd = _lib.to_device(nodes_idx, torch.int64)
+        normals_d = _lib.to_device(normals, torch.float64) if normals_d is None else normals_d
+        g_d = _lib.to_device(np.broadcast_to(np.asarray(gn, dtype=float), nodes_idx.shape), torch.float64)
+        nm = _lib.NeumannT(self.stencils_device.data_ptr(), self.n, plane.data_ptr(), plane.shape[1], d,
+                           normals_d.data_ptr(), nd.data_ptr(), self.node_row_device().data_ptr(),
+                           g_d.data_ptr(), nodes_idx.shape[0], None)
+        out = torch.empty(max(nodes_idx.shape[0], 1), dtype=torch.float64, device=u_d.device)
+        bad = torch.empty(1, dtype=torch.int64, device=u_d.device)
+        _lib.check(lib.mf_neumann_values(ctypes.byref(nm), u_d.data_ptr(), out.data_ptr(), None, None,
+                                         bad.data_ptr(), _lib.stream_ptr()), "mf_neumann_values")
+        b = int(bad.item())
+        return out[: nodes_idx.shape[0]], (None if b == _lib.SENTINEL_OK else b)
+
+    def neumann_value(self, field, i: int, normal, gn: float) -> float:
+        """Value at node i enforcing w . u = gn with the node's own weight as pivot."""
+        u_d, _ = _to_field(field, self.n_nodes)
+        normal = np.asarray(normal, dtype=float).reshape(1, -1)
+        vals, bad = self.neumann_values_device([int(i)], normal, [float(gn)], u_d)
+        if bad is not None:
+            raise NumericalError(
+                f"node {i}: negligible self-weight in the normal derivative; "
+                "the stencil cannot enforce a Neumann condition explicitly"
+            )
+        return float(vals[0].item())
+
+    def rows_in_order(self):
+        return self._rows
+
+
+# ---------------------------------------------------------------------------
+# compute_weights
+# ---------------------------------------------------------------------------
+
+def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
+    """Evaluate ``engine`` on every selected node for all families (storage.py:258-307).
+
+    ``engine`` is a single engine, or a mapping from family specs to engines.
+    ``for_which=None`` means every node that has a stencil; nodes selected
+    explicitly must all have stencils.
+    """
+    if for_which is None:
+        rows = np.flatnonzero(nodes._blk >= 0).astype(np.int64)
+        if rows.size == 0:
+            raise StencilError("no node has a stencil; run find_closest_stencils first")
+    else:
+        rows = nodes.select(for_which).astype(np.int64)
+
+    fams = expand_families(families, nodes.dim)
+    if isinstance(engine, dict):
+        assign = {}
+        for spec, eng in engine.items():
+            try:
+                keys = list(expand_families([spec], nodes.dim))
+            except StorageError:
+                keys = [str(spec)]
+            for key in keys:
+                if key in assign:
+                    raise StorageError(f"family {key!r} mapped to two engines")
+                assign[key] = eng
+        missing_f = [k for k in fams if k not in assign]
+        if missing_f:
+            raise StorageError(f"no engine given for families {missing_f}")
+        groups = []
+        for eng in dict.fromkeys(assign.values()):
+            sub = {k: op for k, op in fams.items() if assign[k] is eng}
+            if sub:
+                groups.append((eng, sub))
+    else:
+        groups = [(engine, fams)]
+    for eng, _ in groups:
+        _check_batchable(eng)
+    missing = np.flatnonzero(nodes._blk[rows] < 0)
+    if missing.size:
+        raise StencilError(f"node {int(rows[missing[0]])} has no stencil")
+    stencils_d = nodes.stencil_matrix_device(rows)
+    n = int(stencils_d.shape[1]) if rows.size else 0
+    values = {}
+    for eng, sub in groups:
+        values.update(_run_batch(nodes, eng, sub, rows, stencils_d, n))
+    values = {k: values[k] for k in fams}
+    return WeightStore(len(nodes), rows, stencils_d, values, n)
+
+
+def _check_batchable(engine):
+    if not isinstance(engine, RbfFd) or not isinstance(engine.rbf, Polyharmonic):
+        raise ConfigError(
+            f"{engine!r}: the GPU path implements the batched RbfFd(Polyharmonic) engine only"
+        )
+    if engine.solver != "lu":
+        raise ConfigError(f"{engine!r}: the GPU path implements solver='lu' only")
+    if engine.rbf.exponent < 3:
+        raise ConfigError(f"{engine!r}: polyharmonic exponent must be >= 3 on the batched path")
+    if engine.scale not in SCALE_CODES:
+        raise ConfigError(f"unknown scale rule {engine.scale!r}; use none, nearest or support")
+    if engine.mode not in MODES:
+        raise ConfigError(f"unknown shape-solve mode {engine.mode!r}; use hybrid, replay or fast")
+
+
+def encode_families(fams: dict, dim: int, degree: int):
+    """(kinds, ax_a, ax_b, orders, expos, base_bot) as in storage.py:349-380."""
+    kinds, ax_a, ax_b, orders = [], [], [], []
+    for key, op in fams.items():
+        if isinstance(op, Identity):
+            kinds.append(KIND_IDENTITY); ax_a.append(0); ax_b.append(0)
+        elif isinstance(op, FirstDerivative):
+            kinds.append(KIND_D1); ax_a.append(op.axis); ax_b.append(0)
+        elif isinstance(op, SecondDerivative):
+            kinds.append(KIND_D2); ax_a.append(op.a); ax_b.append(op.b)
+        elif isinstance(op, Laplacian):
+            kinds.append(KIND_LAPLACIAN); ax_a.append(0); ax_b.append(0)
+        else:
+            raise ConfigError(f"family {key!r}: custom operators are not supported on the GPU path")
+        orders.append(op.order)
+    if degree >= 0:
+        expos = np.array(graded_lex_exponents(dim, degree), dtype=np.int32).reshape(-1, dim)
+        basis = MonomialBasis(dim, degree)
+        base_bot = np.stack([basis.origin_row(op) for op in fams.values()], axis=0)
+    else:
+        expos = np.empty((0, dim), dtype=np.int32)
+        base_bot = np.zeros((len(fams), 0))
+    as32 = lambda v: np.ascontiguousarray(np.array(v, dtype=np.int32))
+    return (as32(kinds), as32(ax_a), as32(ax_b), as32(orders), np.ascontiguousarray(expos),
+            np.ascontiguousarray(base_bot, dtype=np.float64))
+
+
+def phs_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int, *, mode=None):
+    """Run mf_phs_weights -> ((nf, m, n) f64 weights, status, first_fail, n_replayed) tensors."""
+    lib = _lib.load()
+    kinds, ax_a, ax_b, orders, expos, base_bot = encode_families(fams, dim, engine.degree)
+    m, n = int(stencils_d.shape[0]), int(stencils_d.shape[1])
+    nf = len(fams)
+    if nf > _lib.MF_MAX_FAMILIES or expos.shape[0] > _lib.MF_MAX_MONOMIALS:
+        raise ConfigError("too many families or monomials for the batched kernel")
+    dev = pos_d.device
+    out = torch.empty((m, nf, n), dtype=torch.float64, device=dev)
+    status = torch.empty(max(m, 1), dtype=torch.int8, device=dev)
+    first_fail = torch.empty(1, dtype=torch.int64, device=dev)
+    n_rep = torch.empty(1, dtype=torch.int64, device=dev)
+    mode_code = MODES[mode or engine.mode]
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.mf_phs_workspace_size(m, ctypes.byref(size)), "mf_phs_workspace_size")
+    ws = _lib.workspace(size.value)
+    _lib.check(lib.mf_phs_weights(
+        pos_d.data_ptr(), int(pos_d.shape[0]), dim, rows_d.data_ptr(), stencils_d.data_ptr(), m, n,
+        engine.rbf.exponent, int(engine.rbf.even), expos.ctypes.data, int(expos.shape[0]),
+        base_bot.ctypes.data, kinds.ctypes.data, ax_a.ctypes.data, ax_b.ctypes.data, orders.ctypes.data,
+        nf, SCALE_CODES[engine.scale], mode_code, out.data_ptr(), status.data_ptr(),
+        first_fail.data_ptr(), n_rep.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+        "mf_phs_weights")
+    return out, status, first_fail, n_rep
+
+
+def _run_batch(nodes, engine, fams, rows, stencils_d, n):
+    _check_batchable(engine)
+    dim = nodes.dim
+    if engine.degree >= 0:
+        l = len(graded_lex_exponents(dim, engine.degree))
+        if l > n:
+            raise WeightError(
+                int(rows[0]),
+                f"augmentation of degree {engine.degree} needs at least {l} stencil nodes, got {n}",
+            )
+    pos_d = nodes.positions_device()
+    rows_d = _lib.to_device(rows, torch.int64)
+    out, status, first_fail, _ = phs_weights_device(pos_d, rows_d, stencils_d, engine, fams, dim)
+    bad = int(first_fail.item())
+    if bad != _lib.SENTINEL_OK:
+        node = int(rows[bad])
+        if int(status[bad].item()) == 2:
+            raise WeightError(node, "all stencil nodes coincide with the center")
+        raise WeightError(node, "singular local collocation system; try a larger stencil")
+    # (m, nf, n) -> per family (m, n)
+    return {key: out[:, f, :].contiguous() for f, key in enumerate(fams)}
