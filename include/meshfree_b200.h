@@ -93,7 +93,18 @@ int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* targets, int6
  * 2 degenerate scale); first_fail (device int64, nullable) receives the lowest
  * failing row index, or INT64 0x7f7f7f7f7f7f7f7f when every row succeeded.
  * n_replayed (device int64, nullable) counts rows re-solved in REPLAY order
- * (HYBRID mode). */
+ * (HYBRID mode).  opts (host struct, nullable) sets the HYBRID threshold and
+ * an optional per-row conditioning-estimate output. */
+typedef struct {
+    double hybrid_threshold; /* HYBRID re-solve threshold on the sensitivity estimate
+                                ||A||_inf ||(A^-1 z)_w||_inf max_f ||x_f||_inf/||w_f||_inf; <= 0: default */
+    double* kappa;           /* device, 4*m, nullable: per row ||A||_inf, ||(A^-1 z)_w||_inf,
+                                ||A^-1 z||_inf, max_f ||x_f||/||w_f|| (FAST/HYBRID modes) */
+    double min_separation;   /* HYBRID also re-solves stencils whose closest node pair is nearer
+                                than this fraction of the stencil radius; <= 0: default */
+} mf_phs_options_t;
+#define MF_PHS_DEFAULT_THRESHOLD 1e8
+#define MF_PHS_DEFAULT_MIN_SEPARATION 1e-2
 int mf_phs_workspace_size(int64_t m, size_t* bytes);
 int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int64_t* rows,
                    const int32_t* stencils, int64_t m, int32_t n, int32_t k, int32_t even,
@@ -101,7 +112,7 @@ int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int64_t* rows,
                    const int32_t* kinds, const int32_t* ax_a, const int32_t* ax_b,
                    const int32_t* orders, int32_t nf, int32_t scale_code, int32_t mode,
                    double* out, int8_t* status, int64_t* first_fail, int64_t* n_replayed,
-                   void* ws, size_t ws_bytes, void* stream);
+                   const mf_phs_options_t* opts, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- canonical CSR -------------------------------------------------------------
  * Structure of WeightStore.matrix: N x N, rows ascending, columns ascending

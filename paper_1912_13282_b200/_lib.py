@@ -29,6 +29,10 @@ _D = ctypes.c_double
 _SZ = ctypes.c_size_t
 
 
+class PhsOptions(ctypes.Structure):
+    _fields_ = [("hybrid_threshold", _D), ("kappa", _P), ("min_separation", _D)]
+
+
 class NeumannT(ctypes.Structure):
     _fields_ = [
         ("stencils", _P), ("n", _I32), ("w_d1", _P), ("mn", _I64), ("d", _I32),
@@ -46,7 +50,8 @@ _SIGNATURES = {
     "mf_knn": ([_P, _I64, _I32, _P, _I64, _P, _I64, _I32, _P, _P, _P, _SZ, _P], _I32),
     "mf_phs_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
     "mf_phs_weights": ([_P, _I64, _I32, _P, _P, _I64, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P,
-                        _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P], _I32),
+                        _P, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.POINTER(PhsOptions), _P, _SZ, _P],
+                       _I32),
     "mf_csr_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
     "mf_csr_build": ([_P, _P, _I64, _I32, _I64, _P, _P, _P, _P, _P, _SZ, _P], _I32),
     "mf_csr_gather": ([_P, _P, _I64, _P, _P], _I32),

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(256) phs_generic(PhsArgs a, const int64_t* __r
 
     const int64_t count = list ? *list_count : a.m;
     const bool want_flag = PROBE && a.flag_list != nullptr;
+    const bool want_est = PROBE && (a.flag_list != nullptr || a.kappa != nullptr);
 
     for (int64_t it = (int64_t)blockIdx.x * wpb + wib; it < count; it += (int64_t)gridDim.x * wpb) {
         const int64_t idx = list ? list[it] : it;
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(256) phs_generic(PhsArgs a, const int64_t* __r
         int stat = 0;
         double sc = 1.0;
         double anorm = 0.0;
+        double r2min = INFINITY, rc2max = 0.0;
         if (a.P.scale_code != MF_SCALE_NONE) {
             const bool nearest = a.P.scale_code == MF_SCALE_NEAREST;
             double best = nearest ? INFINITY : -1.0;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(256) phs_generic(PhsArgs a, const int64_t* __r
                         r2 = __dadd_rn(r2, __dmul_rn(df, df));
                     }
                     v = phs_phi(__dsqrt_rn(r2), a.P.k, a.P.even);
+                    r2min = fmin(r2min, r2);
                 }
                 A[(size_t)i * lda + j] = v;
                 A[(size_t)j * lda + i] = v;
@@ -230,12 +233,52 @@ __global__ void __launch_bounds__(256) phs_generic(PhsArgs a, const int64_t* __r
                 a.out[((size_t)idx * nf + f) * n + j] = v;
             }
             if (__any_sync(FULL, bad)) stat = 1;
-            if (PROBE && want_flag && stat == 0) {
-                double xn = 0.0;
-                for (int r = lane; r < s; r += 32) xn = fmax(xn, fabs(A[(size_t)r * lda + s + nf]));
+            if (want_est && stat == 0) {
+                // same estimate as phs_reg.cuh
+                double zw = 0.0, za = 0.0, ratio = 0.0;
+                for (int r = lane; r < s; r += 32) {
+                    const double v = fabs(A[(size_t)r * lda + s + nf]);
+                    za = fmax(za, v);
+                    if (r < n) zw = fmax(zw, v);
+                }
+                for (int f = 0; f < nf; ++f) {
+                    double xa = 0.0, xw = 0.0;
+                    for (int r = lane; r < s; r += 32) {
+                        const double v = fabs(A[(size_t)r * lda + s + f]);
+                        xa = fmax(xa, v);
+                        if (r < n) xw = fmax(xw, v);
+                    }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) xn = fmax(xn, __shfl_xor_sync(FULL, xn, o));
-                if (lane == 0 && hybrid_flag(anorm * xn, a.hybrid_thresh)) {
+                    for (int o = 16; o > 0; o >>= 1) {
+                        xa = fmax(xa, __shfl_xor_sync(FULL, xa, o));
+                        xw = fmax(xw, __shfl_xor_sync(FULL, xw, o));
+                    }
+                    ratio = fmax(ratio, xa / xw);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    zw = fmax(zw, __shfl_xor_sync(FULL, zw, o));
+                    za = fmax(za, __shfl_xor_sync(FULL, za, o));
+                }
+                for (int j = lane; j < n; j += 32) {
+                    double rc2 = 0.0;
+                    for (int ax = 0; ax < d; ++ax) rc2 = fma(loc[j * d + ax], loc[j * d + ax], rc2);
+                    rc2max = fmax(rc2max, rc2);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    r2min = fmin(r2min, __shfl_xor_sync(FULL, r2min, o));
+                    rc2max = fmax(rc2max, __shfl_xor_sync(FULL, rc2max, o));
+                }
+                const double est = anorm * zw * ratio;
+                const bool close = r2min < a.min_sep2 * rc2max;
+                if (lane == 0 && a.kappa) {
+                    a.kappa[4 * idx + 0] = anorm;
+                    a.kappa[4 * idx + 1] = zw;
+                    a.kappa[4 * idx + 2] = za;
+                    a.kappa[4 * idx + 3] = ratio;
+                }
+                if (want_flag && lane == 0 && (close || hybrid_flag(est, a.hybrid_thresh))) {
                     unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
                     a.flag_list[slot] = idx;
                 }
@@ -318,7 +361,7 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
                               const int32_t* kinds, const int32_t* ax_a, const int32_t* ax_b,
                               const int32_t* orders, int32_t nf, int32_t scale_code, int32_t mode,
                               double* out, int8_t* status, int64_t* first_fail, int64_t* n_replayed,
-                              void* ws, size_t ws_bytes, void* stream) {
+                              const mf_phs_options_t* opts, void* ws, size_t ws_bytes, void* stream) {
     (void)N;
     MF_REQUIRE(d >= 1 && d <= MF_MAX_DIM, "mf_phs_weights: dimension %d not in 1..%d", d, MF_MAX_DIM);
     MF_REQUIRE(nf >= 1 && nf <= MF_MAX_FAMILIES, "mf_phs_weights: %d families (max %d)", nf, MF_MAX_FAMILIES);
@@ -340,11 +383,20 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
     a.out = out;
     a.status = status;
     a.first_fail = first_fail;
-    a.hybrid_thresh = 1e5;
+    a.hybrid_thresh = (opts && opts->hybrid_threshold > 0.0) ? opts->hybrid_threshold : MF_PHS_DEFAULT_THRESHOLD;
+    a.kappa = opts ? opts->kappa : nullptr;
+    {
+        const double sep = (opts && opts->min_separation > 0.0) ? opts->min_separation : MF_PHS_DEFAULT_MIN_SEPARATION;
+        a.min_sep2 = sep * sep;
+    }
     int rc = fill_phs_params(a.P, d, k, even, expos, l, base_bot, kinds, ax_a, ax_b, orders, nf, scale_code);
     if (rc != MF_OK) return rc;
 
-    if (mode == MF_PHS_REPLAY) return launch_generic<true>(a, nullptr, nullptr, m, st);
+    if (mode == MF_PHS_REPLAY) {
+        rc = launch_phs_replay_reg(a, nullptr, nullptr, m, st, sm_count());
+        if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<true>(a, nullptr, nullptr, m, st);
+        return rc;
+    }
 
     int64_t* flag_count = nullptr;
     int64_t* flag_list = nullptr;
@@ -364,7 +416,8 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
     if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<false>(a, nullptr, nullptr, m, st);
     if (rc != MF_OK) return rc;
     if (mode == MF_PHS_HYBRID) {
-        rc = launch_generic<true>(a, flag_list, flag_count, m, st);
+        rc = launch_phs_replay_reg(a, flag_list, flag_count, m, st, sm_count());
+        if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<true>(a, flag_list, flag_count, m, st);
         if (rc != MF_OK) return rc;
         if (n_replayed) MF_CUDA_CHECK(cudaMemcpyAsync(n_replayed, flag_count, sizeof(int64_t),
                                                       cudaMemcpyDeviceToDevice, st));

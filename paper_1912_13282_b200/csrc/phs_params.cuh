@@ -28,6 +28,8 @@ struct PhsArgs {
     int64_t* flag_list;   // HYBRID: rows to re-solve in REPLAY order
     int64_t* flag_count;
     double hybrid_thresh;
+    double* kappa;        // optional per-row conditioning diagnostics (FAST/HYBRID)
+    double min_sep2;      // HYBRID: (min node separation / stencil radius)^2 below which to re-solve
     PhsParams P;
 };
 
@@ -124,5 +126,7 @@ __device__ __forceinline__ double probe_sign(int64_t idx, int r) {
 }
 
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms);
+int launch_phs_replay_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
+                          cudaStream_t st, int sms);
 
 }  // namespace mf

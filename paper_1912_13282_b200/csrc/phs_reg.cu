@@ -1,8 +1,34 @@
-// Register-resident fast path of the PHS shape solve (filled in below).
+// Dispatch of the register-resident shape solve (kernel template in phs_reg.cuh;
+// each hot shape is instantiated in its own translation unit, phs_reg_<shape>.cu,
+// so nvcc builds them in parallel).
 #include "common.cuh"
 #include "phs_params.cuh"
 
 namespace mf {
-// Not specialised for any shape yet: the generic kernel handles everything.
-int launch_phs_fast(const PhsArgs&, cudaStream_t, int) { return MF_ERR_UNSUPPORTED; }
+
+template <int NN, int DEG, int DD, int NF, bool REPLAY>
+int launch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
+               cudaStream_t st, int sms);
+
+template <bool REPLAY>
+int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
+                 cudaStream_t st, int sms) {
+    const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
+    // hot shapes of the BASELINE configs (C1/C4, C2, C3) and their neighbours
+    // (launch_reg also checks that the exponent table is the graded-lex one)
+    if (d == 3 && n == 35 && l == 10 && nf == 1) return launch_reg<35, 2, 3, 1, REPLAY>(a, list, list_count, max_count, st, sms);
+    if (d == 2 && n == 15 && l == 6 && nf == 1) return launch_reg<15, 2, 2, 1, REPLAY>(a, list, list_count, max_count, st, sms);
+    if (d == 2 && n == 25 && l == 6 && nf == 3) return launch_reg<25, 2, 2, 3, REPLAY>(a, list, list_count, max_count, st, sms);
+    return MF_ERR_UNSUPPORTED;
+}
+
+int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms) {
+    return dispatch_reg<false>(a, nullptr, nullptr, a.m, st, sms);
+}
+
+int launch_phs_replay_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
+                          cudaStream_t st, int sms) {
+    return dispatch_reg<true>(a, list, list_count, max_count, st, sms);
+}
+
 }  // namespace mf

@@ -592,8 +592,13 @@ def encode_families(fams: dict, dim: int, degree: int):
             np.ascontiguousarray(base_bot, dtype=np.float64))
 
 
-def phs_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int, *, mode=None):
-    """Run mf_phs_weights -> ((nf, m, n) f64 weights, status, first_fail, n_replayed) tensors."""
+def phs_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int, *, mode=None,
+                       threshold: float = 0.0, kappa=None, min_separation: float = 0.0):
+    """Run mf_phs_weights -> ((m, nf, n) f64 weights, status, first_fail, n_replayed) tensors.
+
+    ``threshold`` overrides the HYBRID re-solve threshold; ``kappa`` (a device
+    f64 tensor of m entries) receives the per-stencil conditioning estimate.
+    """
     lib = _lib.load()
     kinds, ax_a, ax_b, orders, expos, base_bot = encode_families(fams, dim, engine.degree)
     m, n = int(stencils_d.shape[0]), int(stencils_d.shape[1])
@@ -609,12 +614,14 @@ def phs_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int, 
     size = ctypes.c_size_t(0)
     _lib.check(lib.mf_phs_workspace_size(m, ctypes.byref(size)), "mf_phs_workspace_size")
     ws = _lib.workspace(size.value)
+    opts = _lib.PhsOptions(float(threshold), _lib.ptr(kappa), float(min_separation))
     _lib.check(lib.mf_phs_weights(
         pos_d.data_ptr(), int(pos_d.shape[0]), dim, rows_d.data_ptr(), stencils_d.data_ptr(), m, n,
         engine.rbf.exponent, int(engine.rbf.even), expos.ctypes.data, int(expos.shape[0]),
         base_bot.ctypes.data, kinds.ctypes.data, ax_a.ctypes.data, ax_b.ctypes.data, orders.ctypes.data,
         nf, SCALE_CODES[engine.scale], mode_code, out.data_ptr(), status.data_ptr(),
-        first_fail.data_ptr(), n_rep.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+        first_fail.data_ptr(), n_rep.data_ptr(), ctypes.byref(opts), ws.data_ptr(), size.value,
+        _lib.stream_ptr()),
         "mf_phs_weights")
     return out, status, first_fail, n_rep
 
