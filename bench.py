@@ -228,9 +228,9 @@ def main():
         w, status, first_fail, n_rep = phs_weights_device(pos_d, rows_d, st, eng, fams, 3)
         if ev:
             ev[2].record(stream)
-        store = mf.WeightStore(N, all_idx, st, {"laplacian": w[:, 0, :]}, n)
+        store = mf.WeightStore(N, all_idx, st, {"laplacian": w[:, 0, :]}, n, rows_d=rows_d, positions_d=pos_d)
         mat = store.matrix("laplacian")
-        mat.ell()
+        mat.plan(True)
         if ev:
             ev[3].record(stream)
         y = mat.apply_device(u_d)
@@ -350,7 +350,7 @@ def main():
                          "frac": phs_tflops / fp64_peak, "traffic": None,
                          "note": "F=(2/3)s^3+2rs^2 per stencil (s=45, r=1); peak = DFMA probe measured "
                                  "in this run (MEASURED_PEAKS.json has no fp64 entry)"},
-            "apply_roofline": {"bound": "hbm", "kernel": "mf_ell_apply", "achieved": apply_gbs,
+            "apply_roofline": {"bound": "hbm", "kernel": "mf_plan_apply (Morton-ordered ELL-32 + u/y permutes)", "achieved": apply_gbs,
                                "peak": hbm_peak, "unit": "GB/s", "frac": apply_gbs / hbm_peak,
                                "traffic": None, "bytes_per_launch": b_apply,
                                "note": "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"},

@@ -12,7 +12,7 @@
  *   mf_csr_gather     storage.py:165-168            WeightStore.matrix (values per family)
  *   mf_apply          storage.py:186-188            WeightStore.apply_all (scipy csr_matvec)
  *   mf_apply_rows     storage.py:174-184            WeightStore.apply (selected rows)
- *   mf_ell_build/_apply storage.py:186-188          apply_all through an ELL-32 apply plan
+ *   mf_plan_*         storage.py:186-188            apply_all through a locality-ordered ELL plan
  *   mf_heat_steps     drivers.py:87-110             run_heat_explicit step loop
  *   mf_neumann_values storage.py:226-250            WeightStore.neumann_value (batched)
  *
@@ -130,20 +130,35 @@ int mf_csr_gather(const int32_t* perm, const double* w, int64_t nnz, double* dat
 /* ---- explicit application ----------------------------------------------------
  * y_i = sum over row i in storage order, sequential from 0.0, no FMA: bitwise
  * equal to scipy's csr_matvec on the same CSR.  mf_apply reads the CSR
- * directly; the ELL-32 "apply plan" (mf_ell_build) stores the same entries
- * slot-major in tiles of 32 rows (entry j of row r at ((r/32)*W + j)*32 + r%32,
- * W = max row length) so a warp's loads are contiguous, and mf_ell_apply /
- * mf_heat_steps stream it at HBM rate.  Row lengths still come from indptr. */
+ * directly (thread per row). */
 int mf_apply(const int32_t* indptr, const int32_t* indices, const double* data,
              const double* u, double* y, int64_t N, void* stream);
 /* y[k] = (A u)[sel[k]] for a list of rows (WeightStore.apply). */
 int mf_apply_rows(const int32_t* indptr, const int32_t* indices, const double* data,
                   const double* u, const int64_t* sel, int64_t count, double* y, void* stream);
-/* ell_idx (ceil(N/32)*32*W int32) and ell_val (same count f64, nullable) */
-int mf_ell_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
-                 int32_t W, int32_t* ell_idx, double* ell_val, void* stream);
-int mf_ell_apply(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
-                 int32_t W, const double* u, double* y, void* stream);
+
+/* ---- apply plan (HBM-rate explicit application) ---------------------------------
+ * The plan stores the CSR entries ELL-32 slot-major -- entry j of plan row r at
+ * ((r/32)*W + j)*32 + r%32, W = max row length -- with the rows renumbered
+ * along a Morton curve of the node positions (order: plan row -> node, inv:
+ * node -> plan row) so a warp's rows and their columns are spatial neighbours.
+ * The addend order inside each row is the CSR's, so sums stay bitwise equal to
+ * mf_apply.  order/inv may be NULL (identity).  ell_len (N int32) receives each
+ * plan row's length. */
+int mf_order_workspace_size(int64_t N, size_t* bytes);
+int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_t* order, int32_t* inv,
+                      void* ws, size_t ws_bytes, void* stream);
+/* ell_idx (ceil(N/32)*32*W int32, nullable), ell_val (same count f64, nullable) */
+int mf_plan_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                  int32_t W, const int32_t* order, const int32_t* inv, int32_t* ell_idx,
+                  double* ell_val, int32_t* ell_len, void* stream);
+/* y = A u in node order; with an order, u/y are permuted through scratch_u/scratch_y (N each) */
+int mf_plan_apply(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
+                  int32_t W, const int32_t* order, const double* u, double* y, double* scratch_u,
+                  double* scratch_y, void* stream);
+/* dst[i] = src[order[i]] (scatter = 0) or dst[order[i]] = src[i] (scatter = 1) */
+int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatter, double* dst,
+               void* stream);
 
 /* ---- explicit Neumann closure ---------------------------------------------------
  * For listed node i with stencil row r = node_row[i] (stencils m x n int32,
@@ -171,16 +186,18 @@ int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, doub
                       uint64_t* peak, int64_t* bad, void* stream);
 
 /* ---- forward-Euler heat stepping -----------------------------------------------
- * `steps` steps of drivers.py:88-110 over the ELL-32 plan of the laplacian,
- * with step-invariant data: interior and dirichlet masks (uint8, N),
+ * `steps` steps of drivers.py:88-110 over an apply plan of the laplacian
+ * (every per-node array below is in plan row order), with step-invariant
+ * data: interior and dirichlet masks (uint8, N),
  * Dirichlet values g_dir (N), optional source (N, nullable: the reference's
  * `+ 0.0`), optional Neumann closure (nm, nullable; values from the previous
- * field, as drivers.py:99-102).  u (N) is advanced in place using scratch (N).
+ * field, as drivers.py:99-102; node-order plans only).  u (N) is advanced in
+ * place using scratch (N).
  * peaks (steps uint64, device) receives the IEEE bits of max|u| after each
  * step (NaN sorts above inf); once a step exceeds 1e12 or is non-finite the
  * remaining steps do no work.  Dirichlet values must already be applied to u
  * before the first call (drivers.py:84-85). */
-int mf_heat_steps(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, const double* ell_val, int64_t N,
                   int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
                   const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
                   int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream);

@@ -57,8 +57,11 @@ _SIGNATURES = {
     "mf_csr_gather": ([_P, _P, _I64, _P, _P], _I32),
     "mf_apply": ([_P, _P, _P, _P, _P, _I64, _P], _I32),
     "mf_apply_rows": ([_P, _P, _P, _P, _P, _I64, _P, _P], _I32),
-    "mf_ell_build": ([_P, _P, _P, _I64, _I32, _P, _P, _P], _I32),
-    "mf_ell_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P], _I32),
+    "mf_order_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_locality_order": ([_P, _I64, _I32, _P, _P, _P, _SZ, _P], _I32),
+    "mf_plan_build": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "mf_plan_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "mf_permute": ([_P, _P, _I64, _I32, _P, _P], _I32),
     "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
                        _I64, _P, _P, _P, _P], _I32),

@@ -85,9 +85,10 @@ __device__ __forceinline__ int cell_of(const GridParams& g, const double* x, int
 // key order: (d2, node index, candidate id) -- the candidate id only separates
 // repeated pool entries, which carry the same node index
 __device__ __forceinline__ bool key_lt(double d1, int i1, int c1, double d2, int i2, int c2) {
-    if (d1 != d2) return d1 < d2;
-    if (i1 != i2) return i1 < i2;
-    return c1 < c2;
+    // branch-free: predicates combined with bitwise ops (no divergent short-circuit)
+    const bool dl = d1 < d2, de = d1 == d2;
+    const bool il = i1 < i2, ie = i1 == i2;
+    return dl | (de & (il | (ie & (c1 < c2))));
 }
 
 struct Box {

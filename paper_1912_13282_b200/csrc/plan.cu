@@ -1,0 +1,261 @@
+// Locality-ordered apply plan (sm_100a).
+//
+// The reference's node indices carry no spatial order (uniform random
+// clouds), so a row-per-thread SpMV gathers u from random cache lines and is
+// L2-bound.  The apply plan renumbers the rows/columns of the canonical CSR
+// along a Morton (Z-order) curve of the node positions and stores the entries
+// ELL-32 slot-major in that order: a warp's 32 rows are spatial neighbours,
+// their columns hit the same few L1 lines, and the value/index streams stay
+// contiguous.  Entry order inside each row is unchanged (ascending original
+// column), so every row sum keeps scipy's addend order and results stay
+// bitwise equal to the reference (storage.py:186-188).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace mf {
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {  // 21 bits -> every 3rd bit
+    x &= 0x1fffffull;
+    x = (x | (x << 32)) & 0x1f00000000ffffull;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+    x = (x | (x << 8)) & 0x100f00f00f00f00full;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+__device__ __forceinline__ unsigned long long spread2(unsigned long long x) {  // 32 bits -> every 2nd bit
+    x &= 0xffffffffull;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+
+__global__ void plan_bbox(const double* __restrict__ pos, int64_t N, int d, unsigned long long* bb) {
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < d; ++a) {
+            double x = pos[i * d + a];
+            mn[a] = fmin(mn[a], x);
+            mx[a] = fmax(mx[a], x);
+        }
+    for (int a = 0; a < d; ++a) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(FULL, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(FULL, mx[a], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bb[a], ordered_bits(mn[a]));
+            atomicMax(&bb[3 + a], ordered_bits(mx[a]));
+        }
+    }
+}
+
+__global__ void plan_keys(const double* __restrict__ pos, int64_t N, int d, const unsigned long long* __restrict__ bb,
+                          unsigned long long* __restrict__ key, int32_t* __restrict__ val) {
+    double lo[3], sc[3];
+    const int bits = d == 1 ? 63 : (d == 2 ? 32 : 21);
+    const double span = (double)((1ull << (bits > 62 ? 62 : bits)) - 1);
+    for (int a = 0; a < d; ++a) {
+        lo[a] = from_ordered_bits(bb[a]);
+        double ext = from_ordered_bits(bb[3 + a]) - lo[a];
+        sc[a] = ext > 0.0 ? span / ext : 0.0;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long q[3] = {0, 0, 0};
+        for (int a = 0; a < d; ++a) {
+            double t = (pos[i * d + a] - lo[a]) * sc[a];
+            t = t > 0.0 ? (t < span ? t : span) : 0.0;
+            q[a] = (unsigned long long)t;
+        }
+        unsigned long long k;
+        if (d == 1) k = q[0];
+        else if (d == 2) k = spread2(q[0]) | (spread2(q[1]) << 1);
+        else k = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+        key[i] = k;
+        val[i] = (int32_t)i;
+    }
+}
+
+__global__ void plan_invert(const int32_t* __restrict__ order, int64_t N, int32_t* __restrict__ inv) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        inv[order[i]] = (int32_t)i;
+}
+
+// ELL-32 plan in the new order: row i' = old row order[i'], column c -> inv[c]
+__global__ void plan_ell_build(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                               const double* __restrict__ data, int64_t N, int W, const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ inv, int32_t* __restrict__ ell_idx,
+                               double* __restrict__ ell_val, int32_t* __restrict__ ell_len) {
+    const int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t tile = e / (32 * (int64_t)W);
+        int rem = (int)(e - tile * 32 * (int64_t)W);
+        int j = rem >> 5, lane = rem & 31;
+        int64_t rn = tile * 32 + lane;
+        int32_t ci = 0;
+        double v = 0.0;
+        if (rn < N) {
+            const int64_t ro = order ? order[rn] : rn;
+            const int32_t lo = indptr[ro], len = indptr[ro + 1] - lo;
+            if (j == 0 && ell_len) ell_len[rn] = len;
+            if (j < len) {
+                const int32_t c = indices[lo + j];
+                ci = inv ? inv[c] : c;
+                if (data) v = data[lo + j];
+            }
+        }
+        if (ell_idx) ell_idx[e] = ci;
+        if (ell_val) ell_val[e] = v;
+    }
+}
+
+__global__ void plan_gather(const double* __restrict__ src, const int32_t* __restrict__ order, int64_t N,
+                            double* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[order[i]];
+}
+
+__global__ void plan_scatter(const double* __restrict__ src, const int32_t* __restrict__ order, int64_t N,
+                             double* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        dst[order[i]] = src[i];
+}
+
+// row sums over the plan (thread per row, slot-major loads)
+__global__ void __launch_bounds__(256) plan_apply_k(const int32_t* __restrict__ ell_idx,
+                                                    const double* __restrict__ ell_val,
+                                                    const int32_t* __restrict__ ell_len, int64_t N, int W,
+                                                    const double* __restrict__ u, double* __restrict__ y) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        const int len = ell_len[r];
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double acc = 0.0;
+#pragma unroll 5
+        for (int j = 0; j < len; ++j) {
+            const double a = __ldcs(ell_val + base + 32 * j);
+            const int32_t c = __ldcs(ell_idx + base + 32 * j);
+            acc = __dadd_rn(acc, __dmul_rn(a, __ldg(u + c)));
+        }
+        y[r] = acc;
+    }
+}
+
+inline int grid_of(int64_t work, int threads, int per_sm = 8) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)sms * per_sm;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace mf
+
+using namespace mf;
+
+extern "C" int mf_order_workspace_size(int64_t N, size_t* bytes) {
+    if (!bytes || N < 0) {
+        set_error("mf_order_workspace_size: bad arguments");
+        return MF_ERR_ARG;
+    }
+    size_t sort_bytes = 0;
+    cub::DoubleBuffer<unsigned long long> k(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k, v, (int)(N > 0 ? N : 1));
+    Arena ar{nullptr, 0, 0, true};
+    ar.take<unsigned long long>(6);
+    ar.take<unsigned long long>(N);
+    ar.take<unsigned long long>(N);
+    ar.take<int32_t>(N);
+    ar.take<char>(sort_bytes);
+    *bytes = ar.off;
+    return MF_OK;
+}
+
+extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_t* order, int32_t* inv, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    MF_REQUIRE(d >= 1 && d <= MF_MAX_DIM && N >= 0 && N < 2147483647, "mf_locality_order: bad arguments");
+    if (N == 0) return MF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t sort_bytes = 0;
+    cub::DoubleBuffer<unsigned long long> probe_k(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> probe_v(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, probe_k, probe_v, (int)N);
+    Arena ar{(char*)ws, ws_bytes, 0, false};
+    unsigned long long* bb = ar.take<unsigned long long>(6);
+    unsigned long long* k0 = ar.take<unsigned long long>(N);
+    unsigned long long* k1 = ar.take<unsigned long long>(N);
+    int32_t* v0 = ar.take<int32_t>(N);
+    char* tmp = ar.take<char>(sort_bytes);
+    if (!ws || !ar.ok()) {
+        set_error("mf_locality_order: workspace too small");
+        return MF_ERR_WORKSPACE;
+    }
+    MF_CUDA_CHECK(cudaMemsetAsync(bb, 0xff, 3 * sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(bb + 3, 0, 3 * sizeof(unsigned long long), st));
+    plan_bbox<<<grid_of(N, 256), 256, 0, st>>>(pos, N, d, bb);
+    MF_LAUNCH_CHECK();
+    plan_keys<<<grid_of(N, 256), 256, 0, st>>>(pos, N, d, bb, k0, v0);
+    MF_LAUNCH_CHECK();
+    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+    cub::DoubleBuffer<int32_t> vb(v0, order);
+    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, kb, vb, (int)N, 0, 64, st));
+    if (vb.Current() != order)
+        MF_CUDA_CHECK(cudaMemcpyAsync(order, vb.Current(), sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
+    if (inv) {
+        plan_invert<<<grid_of(N, 256), 256, 0, st>>>(order, N, inv);
+        MF_LAUNCH_CHECK();
+    }
+    return MF_OK;
+}
+
+extern "C" int mf_plan_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, int32_t W,
+                             const int32_t* order, const int32_t* inv, int32_t* ell_idx, double* ell_val,
+                             int32_t* ell_len, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0 && ((order == nullptr) == (inv == nullptr)), "mf_plan_build: bad arguments");
+    int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    if (total == 0 && N == 0) return MF_OK;
+    int64_t work = total > N ? total : N;
+    plan_ell_build<<<grid_of(work, 256, 16), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, N, W, order, inv,
+                                                                              ell_idx, ell_val, ell_len);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_plan_apply(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
+                             int32_t W, const int32_t* order, const double* u, double* y, double* scratch_u,
+                             double* scratch_y, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0, "mf_plan_apply: bad arguments");
+    if (N == 0) return MF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!order) {
+        plan_apply_k<<<grid_of(N, 256), 256, 0, st>>>(ell_idx, ell_val, ell_len, N, W, u, y);
+        MF_LAUNCH_CHECK();
+        return MF_OK;
+    }
+    MF_REQUIRE(scratch_u && scratch_y, "mf_plan_apply: an ordered plan needs two scratch vectors");
+    plan_gather<<<grid_of(N, 256), 256, 0, st>>>(u, order, N, scratch_u);
+    MF_LAUNCH_CHECK();
+    plan_apply_k<<<grid_of(N, 256), 256, 0, st>>>(ell_idx, ell_val, ell_len, N, W, scratch_u, scratch_y);
+    MF_LAUNCH_CHECK();
+    plan_scatter<<<grid_of(N, 256), 256, 0, st>>>(scratch_y, order, N, y);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+extern "C" int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatter, double* dst,
+                          void* stream) {
+    MF_REQUIRE(N >= 0, "mf_permute: bad N");
+    if (N == 0) return MF_OK;
+    if (scatter) plan_scatter<<<grid_of(N, 256), 256, 0, (cudaStream_t)stream>>>(src, order, N, dst);
+    else plan_gather<<<grid_of(N, 256), 256, 0, (cudaStream_t)stream>>>(src, order, N, dst);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}

@@ -4,7 +4,7 @@
 //   mf_csr_build / mf_csr_gather   WeightStore.matrix      (storage.py:156-170)
 //   mf_apply                       WeightStore.apply_all   (storage.py:186-188)
 //   mf_apply_rows                  WeightStore.apply       (storage.py:174-184)
-//   mf_heat_steps                  run_heat_explicit loop  (drivers.py:87-110)
+//   mf_heat_steps                  run_heat_explicit loop  (drivers.py:87-110), on an apply plan (plan.cu)
 //   mf_neumann_values              WeightStore.neumann_value (storage.py:226-250)
 //
 // Summation contract: scipy's csr_matvec accumulates each row in storage
@@ -41,32 +41,26 @@ __global__ void csr_counts(int32_t* __restrict__ node_row, int64_t N, int n) {
         node_row[i] = (i < N && node_row[i] >= 0) ? n : 0;
 }
 
-// One warp per stored row: rank each stencil member by (column, slot) and
-// scatter it to its canonical position (stable lexsort, storage.py:161).
+// One thread per stencil entry: its canonical slot is its rank by (column,
+// slot) within the row -- the stable lexsort of storage.py:161.  Threads of a
+// warp read the same row, so the inner loads are broadcasts.
 __global__ void csr_fill(const int64_t* __restrict__ rows, const int32_t* __restrict__ st, int64_t m, int n,
                          const int32_t* __restrict__ indptr, int32_t* __restrict__ indices,
                          int32_t* __restrict__ perm) {
-    extern __shared__ int32_t sh_cols[];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    const int wpb = blockDim.x >> 5;
-    int32_t* cols = sh_cols + wib * n;
-    for (int64_t r = (int64_t)blockIdx.x * wpb + wib; r < m; r += (int64_t)gridDim.x * wpb) {
+    const int64_t total = m * (int64_t)n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / n;
+        const int j = (int)(e - r * n);
         const int32_t* src = st + r * n;
-        for (int j = lane; j < n; j += 32) cols[j] = src[j];
-        __syncwarp();
-        const int64_t base = indptr[rows[r]];
-        for (int j = lane; j < n; j += 32) {
-            int32_t c = cols[j];
-            int rank = 0;
-            for (int i = 0; i < n; ++i) {
-                int32_t ci = cols[i];
-                rank += (ci < c) || (ci == c && i < j);
-            }
-            indices[base + rank] = c;
-            perm[base + rank] = (int32_t)(r * n + j);
+        const int32_t c = src[j];
+        int rank = 0;
+        for (int i = 0; i < n; ++i) {
+            const int32_t ci = __ldg(src + i);
+            rank += (ci < c) || (ci == c && i < j);
         }
-        __syncwarp();
+        const int64_t base = indptr[rows[r]];
+        indices[base + rank] = c;
+        perm[base + rank] = (int32_t)e;
     }
 }
 
@@ -104,30 +98,6 @@ __global__ void apply_rows_k(const int32_t* __restrict__ indptr, const int32_t* 
     }
 }
 
-// ELL-32 plan: entry j of row r lives at ((r/32)*W + j)*32 + r%32.
-__global__ void ell_build_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            const double* __restrict__ data, int64_t N, int W, int32_t* __restrict__ ell_idx,
-                            double* __restrict__ ell_val) {
-    const int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        int64_t tile = e / (32 * (int64_t)W);
-        int rem = (int)(e - tile * 32 * (int64_t)W);
-        int j = rem >> 5, lane = rem & 31;
-        int64_t r = tile * 32 + lane;
-        int32_t ci = 0;
-        double v = 0.0;
-        if (r < N) {
-            int32_t lo = indptr[r], len = indptr[r + 1] - lo;
-            if (j < len) {
-                ci = indices[lo + j];
-                if (data) v = data[lo + j];
-            }
-        }
-        if (ell_idx) ell_idx[e] = ci;
-        if (ell_val) ell_val[e] = v;
-    }
-}
-
 struct HeatStep {
     const uint8_t* interior;
     const uint8_t* dirichlet;
@@ -146,7 +116,7 @@ __device__ __forceinline__ bool step_blew_up(const unsigned long long* prev) {
 // Thread per row over the ELL-32 plan: each warp-wide load of slot j is one
 // contiguous 256 B (values) / 128 B (indices) segment.
 template <bool HEAT>
-__global__ void __launch_bounds__(256) ell_apply_k(const int32_t* __restrict__ indptr,
+__global__ void __launch_bounds__(256) ell_apply_k(const int32_t* __restrict__ ell_len,
                                                    const int32_t* __restrict__ ell_idx,
                                                    const double* __restrict__ ell_val, int64_t N, int W,
                                                    const double* __restrict__ u, double* __restrict__ y,
@@ -156,7 +126,7 @@ __global__ void __launch_bounds__(256) ell_apply_k(const int32_t* __restrict__ i
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ((N + 31) & ~31ll); r += stride) {
         const bool live = r < N;
-        int len = live ? indptr[r + 1] - indptr[r] : 0;
+        int len = live ? ell_len[r] : 0;
         const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
         double v;
         if (!HEAT) {
@@ -297,10 +267,7 @@ extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_
     MF_LAUNCH_CHECK();
     MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, indptr, (int)(N + 1), st));
     if (m > 0) {
-        const int wpb = 8;
-        size_t sh = sizeof(int32_t) * (size_t)n * wpb;
-        MF_REQUIRE(sh <= 48 * 1024, "mf_csr_build: stencil size %d too large", n);
-        csr_fill<<<grid_for(m, wpb, 64), wpb * 32, sh, st>>>(rows, stencils, m, n, indptr, indices, perm);
+        csr_fill<<<grid_for(m * (int64_t)n, 256, 16), 256, 0, st>>>(rows, stencils, m, n, indptr, indices, perm);
         MF_LAUNCH_CHECK();
     }
     return MF_OK;
@@ -332,26 +299,7 @@ extern "C" int mf_apply_rows(const int32_t* indptr, const int32_t* indices, cons
     return MF_OK;
 }
 
-extern "C" int mf_ell_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
-                            int32_t W, int32_t* ell_idx, double* ell_val, void* stream) {
-    MF_REQUIRE(N >= 0 && W >= 0, "mf_ell_build: bad shape");
-    int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
-    if (total == 0) return MF_OK;
-    ell_build_k<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, N, W, ell_idx, ell_val);
-    MF_LAUNCH_CHECK();
-    return MF_OK;
-}
-
 static int ell_grid(int64_t N) { return grid_for(((N + 31) / 32) * 32, 256, 8); }
-
-extern "C" int mf_ell_apply(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
-                            int32_t W, const double* u, double* y, void* stream) {
-    MF_REQUIRE(N >= 0 && W >= 0, "mf_ell_apply: bad shape");
-    if (N == 0) return MF_OK;
-    ell_apply_k<false><<<ell_grid(N), 256, 0, (cudaStream_t)stream>>>(indptr, ell_idx, ell_val, N, W, u, y, HeatStep{});
-    MF_LAUNCH_CHECK();
-    return MF_OK;
-}
 
 extern "C" int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, double* u_scatter,
                                  uint64_t* peak, int64_t* bad, void* stream) {
@@ -366,7 +314,7 @@ extern "C" int mf_neumann_values(const mf_neumann_t* nm, const double* u, double
     return MF_OK;
 }
 
-extern "C" int mf_heat_steps(const int32_t* indptr, const int32_t* ell_idx, const double* ell_val, int64_t N,
+extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, const double* ell_val, int64_t N,
                              int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
                              const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
                              int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream) {
@@ -383,7 +331,7 @@ extern "C" int mf_heat_steps(const int32_t* indptr, const int32_t* ell_idx, cons
         HeatStep hs{interior, dirichlet, g_dir, source, has_nm ? nm->mask : nullptr, dt, diffusivity, cur, prev};
         double* u_old = buf[s & 1];
         double* u_new = buf[(s + 1) & 1];
-        ell_apply_k<true><<<grid, 256, 0, st>>>(indptr, ell_idx, ell_val, N, W, u_old, u_new, hs);
+        ell_apply_k<true><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
         MF_LAUNCH_CHECK();
         if (has_nm) {
             neumann_k<<<grid_for(nm->count, 128), 128, 0, st>>>(*nm, u_old, nullptr, u_new, cur, nullptr, prev);

@@ -89,14 +89,21 @@ def run_heat_explicit(
         return u_d if return_device else u
 
     lap = store.matrix("laplacian")
-    ell_idx, ell_val, W = lap.ell()
+    # Morton-ordered plan unless a Neumann closure needs node-ordered fields
+    plan = lap.plan(ordered=not neum)
+    perm = plan.order.long() if plan.ordered else None
+
+    def to_plan(arr, dtype):
+        t = _lib.to_device(arr, dtype)
+        return t.index_select(0, perm) if perm is not None else t
+
     interior = np.zeros(n, dtype=np.uint8)
     interior[nodes.interior_indices()] = 1
-    interior_d = _lib.to_device(interior, torch.uint8)
+    interior_d = to_plan(interior, torch.uint8)
     dmask = np.zeros(n, dtype=np.uint8)
     for idx, _ in diri.values():
         dmask[idx] = 1
-    dmask_d = _lib.to_device(dmask, torch.uint8)
+    dmask_d = to_plan(dmask, torch.uint8)
 
     time_dep = callable(source) or any(callable(v) for _, v in diri.values()) or any(
         callable(v) for _, v in neum.values())
@@ -139,17 +146,22 @@ def run_heat_explicit(
 
     scratch = torch.empty(n, dtype=torch.float64, device=dev)
     peaks = torch.empty(steps, dtype=torch.int64, device=dev)
+    u_node = u_d
+    if perm is not None:
+        u_d = torch.empty_like(u_node)
+        _lib.check(lib.mf_permute(u_node.data_ptr(), plan.order.data_ptr(), n, 0, u_d.data_ptr(),
+                                  _lib.stream_ptr()), "mf_permute")
 
     def launch(k_steps, g_d, src_d, nm_struct, peak_view):
         _lib.check(lib.mf_heat_steps(
-            lap.indptr_device.data_ptr(), ell_idx.data_ptr(), ell_val.data_ptr(), n, W,
+            plan.ell_len.data_ptr(), plan.ell_idx.data_ptr(), plan.ell_val.data_ptr(), n, plan.W,
             interior_d.data_ptr(), dmask_d.data_ptr(), g_d.data_ptr(), _lib.ptr(src_d), float(dt),
             float(diffusivity), None if nm_struct is None else ctypes.byref(nm_struct), k_steps,
             u_d.data_ptr(), scratch.data_ptr(), peak_view.data_ptr(), _lib.stream_ptr()), "mf_heat_steps")
 
     if not time_dep:
-        g_d = _lib.to_device(dirichlet_vals(dt), torch.float64)
-        src_d = None if source is None else _lib.to_device(_bc_values(source, pts, 0.0), torch.float64)
+        g_d = to_plan(dirichlet_vals(dt), torch.float64)
+        src_d = None if source is None else to_plan(_bc_values(source, pts, 0.0), torch.float64)
         nm_struct = None
         if neum:
             gn_d = _lib.to_device(neumann_vals(dt), torch.float64)
@@ -158,8 +170,8 @@ def run_heat_explicit(
     else:
         for step in range(steps):
             t_new = (step + 1) * dt
-            g_d = _lib.to_device(dirichlet_vals(t_new), torch.float64)
-            src_d = None if source is None else _lib.to_device(_bc_values(source, pts, step * dt), torch.float64)
+            g_d = to_plan(dirichlet_vals(t_new), torch.float64)
+            src_d = None if source is None else to_plan(_bc_values(source, pts, step * dt), torch.float64)
             nm_struct = None
             if neum:
                 gn_d = _lib.to_device(neumann_vals(t_new), torch.float64)
@@ -173,6 +185,10 @@ def run_heat_explicit(
     if bad is not None:
         step, peak = bad
         raise _instability(step, peak)
+    if perm is not None:
+        _lib.check(lib.mf_permute(u_d.data_ptr(), plan.order.data_ptr(), n, 1, u_node.data_ptr(),
+                                  _lib.stream_ptr()), "mf_permute")
+        u_d = u_node
     return u_d if return_device else u_d.cpu().numpy()
 
 

@@ -131,43 +131,82 @@ def _to_field(field, N):
 class _CsrStructure:
     """indptr / indices / stencil-slot permutation shared by every family of a store."""
 
-    def __init__(self, n_nodes, rows_d, stencils_d, n):
+    def __init__(self, n_nodes, rows_d, stencils_d, n, positions_d=None):
         lib = _lib.load()
         dev = _lib.device()
         m = int(stencils_d.shape[0])
         self.N = int(n_nodes)
         self.n = int(n)
         self.nnz = m * self.n
+        self.positions_d = positions_d
         self.indptr = torch.empty(self.N + 1, dtype=torch.int32, device=dev)
         self.indices = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
         self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
-        dup = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._dup = torch.zeros(1, dtype=torch.int32, device=dev)
         size = ctypes.c_size_t(0)
         _lib.check(lib.mf_csr_workspace_size(self.N, ctypes.byref(size)), "mf_csr_workspace_size")
         ws = _lib.workspace(size.value)
         _lib.check(lib.mf_csr_build(rows_d.data_ptr(), stencils_d.data_ptr(), m, self.n, self.N,
                                     self.indptr.data_ptr(), self.indices.data_ptr(), self.perm.data_ptr(),
-                                    dup.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+                                    self._dup.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
                    "mf_csr_build")
-        if int(dup.item()) != 0:
-            raise StorageError("stored rows must be distinct node indices")
-        self._ell_idx = None
+        # checked lazily (no host sync on the build path): see check()
+        self._checked = False
+        self._plans = {}
 
-    def ell_idx(self):
-        if self._ell_idx is None:
-            self._ell_idx = _ell_build(self.indptr, self.indices, None, self.N, self.n)[0]
-        return self._ell_idx
+    def check(self):
+        if not self._checked:
+            if int(self._dup.item()) != 0:
+                raise StorageError("stored rows must be distinct node indices")
+            self._checked = True
+
+    def plan(self, ordered: bool):
+        """Apply-plan structure: (order, inv, ell_idx, ell_len); order/inv None when unordered."""
+        ordered = ordered and self.positions_d is not None
+        if ordered not in self._plans:
+            lib = _lib.load()
+            dev = self.indptr.device
+            order = inv = None
+            if ordered:
+                order = torch.empty(self.N, dtype=torch.int32, device=dev)
+                inv = torch.empty(self.N, dtype=torch.int32, device=dev)
+                size = ctypes.c_size_t(0)
+                _lib.check(lib.mf_order_workspace_size(self.N, ctypes.byref(size)), "mf_order_workspace_size")
+                ws = _lib.workspace(size.value)
+                pos = self.positions_d
+                _lib.check(lib.mf_locality_order(pos.data_ptr(), self.N, int(pos.shape[1]), order.data_ptr(),
+                                                 inv.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+                           "mf_locality_order")
+            total = ((self.N + 31) // 32) * 32 * self.n
+            ell_idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+            ell_len = torch.empty(max(self.N, 1), dtype=torch.int32, device=dev)
+            _lib.check(lib.mf_plan_build(self.indptr.data_ptr(), self.indices.data_ptr(), None, self.N, self.n,
+                                         _lib.ptr(order), _lib.ptr(inv), ell_idx.data_ptr(), None,
+                                         ell_len.data_ptr(), _lib.stream_ptr()), "mf_plan_build")
+            self._plans[ordered] = (order, inv, ell_idx, ell_len)
+        return self._plans[ordered]
+
+    def plan_values(self, data, ordered: bool):
+        order, inv, _, _ = self.plan(ordered)
+        total = ((self.N + 31) // 32) * 32 * self.n
+        val = torch.empty(max(total, 1), dtype=torch.float64, device=data.device)
+        _lib.check(_lib.load().mf_plan_build(self.indptr.data_ptr(), self.indices.data_ptr(), data.data_ptr(),
+                                             self.N, self.n, _lib.ptr(order), _lib.ptr(inv), None,
+                                             val.data_ptr(), None, _lib.stream_ptr()), "mf_plan_build")
+        return val
 
 
-def _ell_build(indptr, indices, data, N, W):
-    lib = _lib.load()
-    total = ((N + 31) // 32) * 32 * W
-    dev = _lib.device()
-    idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev) if indices is not None else None
-    val = torch.empty(max(total, 1), dtype=torch.float64, device=dev) if data is not None else None
-    _lib.check(lib.mf_ell_build(indptr.data_ptr(), _lib.ptr(indices), _lib.ptr(data), N, W,
-                                _lib.ptr(idx), _lib.ptr(val), _lib.stream_ptr()), "mf_ell_build")
-    return idx, val
+class ApplyPlan:
+    """A matrix's apply plan: Morton-ordered (or node-ordered) ELL-32 arrays."""
+
+    def __init__(self, order, inv, ell_idx, ell_val, ell_len, N, W):
+        self.order, self.inv = order, inv
+        self.ell_idx, self.ell_val, self.ell_len = ell_idx, ell_val, ell_len
+        self.N, self.W = N, W
+
+    @property
+    def ordered(self) -> bool:
+        return self.order is not None
 
 
 class DeviceCSR:
@@ -184,7 +223,8 @@ class DeviceCSR:
         self.data_device = data_d
         self.shape = (structure.N, structure.N)
         self._host = {}
-        self._ell_val = None
+        self._plan = {}
+        self._scratch = None
 
     @property
     def nnz(self) -> int:
@@ -199,6 +239,7 @@ class DeviceCSR:
         return self._s.indices[: self.nnz]
 
     def _get(self, name, t):
+        self._s.check()
         if name not in self._host:
             self._host[name] = t.cpu().numpy()
         return self._host[name]
@@ -215,19 +256,28 @@ class DeviceCSR:
     def data(self):
         return self._get("data", self.data_device[: self.nnz])
 
-    def ell(self):
-        """(ell_idx, ell_val, W): the ELL-32 apply plan of this matrix."""
-        if self._ell_val is None:
-            self._ell_val = _ell_build(self._s.indptr, None, self.data_device, self._s.N, self._s.n)[1]
-        return self._s.ell_idx(), self._ell_val, self._s.n
+    def plan(self, ordered: bool = True) -> ApplyPlan:
+        """The apply plan of this matrix (built once per ordering)."""
+        if ordered not in self._plan:
+            order, inv, idx, ln = self._s.plan(ordered)
+            val = self._s.plan_values(self.data_device, order is not None)
+            self._plan[ordered] = ApplyPlan(order, inv, idx, val, ln, self._s.N, self._s.n)
+        return self._plan[ordered]
 
     def apply_device(self, u_d: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """y = A u on the device through the locality-ordered plan (mf_plan_apply)."""
         lib = _lib.load()
         N = self._s.N
         y = out if out is not None else torch.empty(N, dtype=torch.float64, device=u_d.device)
-        idx, val, W = self.ell()
-        _lib.check(lib.mf_ell_apply(self._s.indptr.data_ptr(), idx.data_ptr(), val.data_ptr(), N, W,
-                                    u_d.data_ptr(), y.data_ptr(), _lib.stream_ptr()), "mf_ell_apply")
+        p = self.plan(True)
+        su = sy = None
+        if p.ordered:
+            if self._scratch is None or self._scratch.device != u_d.device:
+                self._scratch = torch.empty((2, N), dtype=torch.float64, device=u_d.device)
+            su, sy = self._scratch[0], self._scratch[1]
+        _lib.check(lib.mf_plan_apply(p.ell_idx.data_ptr(), p.ell_val.data_ptr(), p.ell_len.data_ptr(), N, p.W,
+                                     _lib.ptr(p.order), u_d.data_ptr(), y.data_ptr(), _lib.ptr(su), _lib.ptr(sy),
+                                     _lib.stream_ptr()), "mf_plan_apply")
         return y
 
     def apply_csr_device(self, u_d: torch.Tensor) -> torch.Tensor:
@@ -242,7 +292,10 @@ class DeviceCSR:
     def __matmul__(self, field):
         u_d, host = _to_field(field, self._s.N)
         y = self.apply_device(u_d)
-        return y.cpu().numpy() if host else y
+        if host:
+            self._s.check()
+            return y.cpu().numpy()
+        return y
 
     def to_scipy(self):
         import scipy.sparse
@@ -300,14 +353,15 @@ class WeightStore:
     bitwise (storage.py:111-118).
     """
 
-    def __init__(self, n_nodes, rows, stencils_d, values_d, n, positions_d=None):
+    def __init__(self, n_nodes, rows, stencils_d, values_d, n, rows_d=None, positions_d=None):
         self.n_nodes = int(n_nodes)
+        self.positions_device = positions_d
         self._rows = np.asarray(rows, dtype=np.int64)
+        self._rows_dev_hint = rows_d
         self.stencils_device = stencils_d
         self._values_d = values_d
         self.n = int(n)
-        self.node_row = np.full(self.n_nodes, -1, dtype=np.int64)
-        self.node_row[self._rows] = np.arange(self._rows.shape[0])
+        self._node_row = None
         self.values = _LazyValues(self)
         self._cols = None
         self._structure = None
@@ -316,6 +370,14 @@ class WeightStore:
         self._node_row_d = None
 
     # -- reference fields -------------------------------------------------
+
+    @property
+    def node_row(self):
+        if self._node_row is None:
+            nr = np.full(self.n_nodes, -1, dtype=np.int64)
+            nr[self._rows] = np.arange(self._rows.shape[0])
+            self._node_row = nr
+        return self._node_row
 
     @property
     def rows(self):
@@ -343,6 +405,8 @@ class WeightStore:
         return self._family(key)
 
     def rows_device(self):
+        if self._rows_d is None and isinstance(self._rows_dev_hint, torch.Tensor):
+            self._rows_d = self._rows_dev_hint
         if self._rows_d is None:
             self._rows_d = _lib.to_device(self._rows, torch.int64)
         return self._rows_d
@@ -381,7 +445,8 @@ class WeightStore:
         if key not in self._matrices:
             vals = self._family(key)
             if self._structure is None:
-                self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n)
+                self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n,
+                                                self.positions_device)
             s = self._structure
             data = torch.empty(max(s.nnz, 1), dtype=torch.float64, device=vals.device)
             _lib.check(_lib.load().mf_csr_gather(s.perm.data_ptr(), vals.data_ptr(), s.nnz, data.data_ptr(),
@@ -543,11 +608,13 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
         raise StencilError(f"node {int(rows[missing[0]])} has no stencil")
     stencils_d = nodes.stencil_matrix_device(rows)
     n = int(stencils_d.shape[1]) if rows.size else 0
+    rows_d = _lib.to_device(rows, torch.int64)
     values = {}
     for eng, sub in groups:
-        values.update(_run_batch(nodes, eng, sub, rows, stencils_d, n))
+        values.update(_run_batch(nodes, eng, sub, rows, rows_d, stencils_d, n))
     values = {k: values[k] for k in fams}
-    return WeightStore(len(nodes), rows, stencils_d, values, n)
+    return WeightStore(len(nodes), rows, stencils_d, values, n, rows_d=rows_d,
+                       positions_d=nodes.positions_device())
 
 
 def _check_batchable(engine):
@@ -626,7 +693,7 @@ def phs_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int, 
     return out, status, first_fail, n_rep
 
 
-def _run_batch(nodes, engine, fams, rows, stencils_d, n):
+def _run_batch(nodes, engine, fams, rows, rows_d, stencils_d, n):
     _check_batchable(engine)
     dim = nodes.dim
     if engine.degree >= 0:
@@ -637,7 +704,6 @@ def _run_batch(nodes, engine, fams, rows, stencils_d, n):
                 f"augmentation of degree {engine.degree} needs at least {l} stencil nodes, got {n}",
             )
     pos_d = nodes.positions_device()
-    rows_d = _lib.to_device(rows, torch.int64)
     out, status, first_fail, _ = phs_weights_device(pos_d, rows_d, stencils_d, engine, fams, dim)
     bad = int(first_fail.item())
     if bad != _lib.SENTINEL_OK:
