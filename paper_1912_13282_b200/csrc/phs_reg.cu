@@ -1,6 +1,9 @@
 // Dispatch of the register-resident shape solve (kernel template in phs_reg.cuh;
 // each hot shape is instantiated in its own translation unit, phs_reg_<shape>.cu,
 // so nvcc builds them in parallel).
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "phs_params.cuh"
 
@@ -9,6 +12,9 @@ namespace mf {
 template <int NN, int DEG, int DD, int NF, bool REPLAY>
 int launch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
                cudaStream_t st, int sms);
+
+template <int NN, int DEG, int DD, int NF>
+int launch_mma(const PhsArgs& a, cudaStream_t st, int sms);
 
 template <bool REPLAY>
 int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
@@ -22,7 +28,21 @@ int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     return MF_ERR_UNSUPPORTED;
 }
 
+// FAST/HYBRID first pass: the register rank-1 kernel (measured fastest so far);
+// MF_PHS_KERNEL=mma selects the tensor-core blocked LU (phs_mma.cuh)
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms) {
+    static const bool use_mma = [] {
+        const char* e = getenv("MF_PHS_KERNEL");
+        return e && strcmp(e, "mma") == 0;
+    }();
+    if (use_mma) {
+        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
+        int rc = MF_ERR_UNSUPPORTED;
+        if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_mma<35, 2, 3, 1>(a, st, sms);
+        else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_mma<15, 2, 2, 1>(a, st, sms);
+        else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_mma<25, 2, 2, 3>(a, st, sms);
+        if (rc != MF_ERR_UNSUPPORTED) return rc;
+    }
     return dispatch_reg<false>(a, nullptr, nullptr, a.m, st, sms);
 }
 

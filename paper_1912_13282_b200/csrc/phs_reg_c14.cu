@@ -1,6 +1,7 @@
-// Register shape solve instantiated for n=15, degree 2, d=2, 1 family.
-#include "phs_reg.cuh"
+// Register and tensor-core shape solves instantiated for n=15, degree 2, d=2, 1 family.
+#include "phs_mma.cuh"
 
 namespace mf {
 MF_INSTANTIATE_REG(15, 2, 2, 1)
+MF_INSTANTIATE_MMA(15, 2, 2, 1)
 }  // namespace mf
