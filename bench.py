@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="hybrid", choices=["hybrid", "replay", "fast"])
     ap.add_argument("--N", type=int, default=1_000_000)
-    ap.add_argument("--cpu-sample", type=int, default=20_000)
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -328,7 +328,7 @@ def main():
 
         oracle.build()
         cores = os.cpu_count() or 1
-        cpu_pipeline_sample(pts, n, 2000, threads=cores)
+        cpu_pipeline_sample(pts, n, 20_000, threads=cores)
         secs, cnt = cpu_pipeline_sample(pts, n, args.cpu_sample, threads=cores)
         cpu = {"value": cnt / secs, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{cnt} strided C3 targets through oracle kNN + shape solve + CSR + apply "
