@@ -215,14 +215,14 @@ def main():
     pos_d = nodes.positions_device()
     u_d = torch.from_numpy(u_host).to(dev)
     all_idx = np.arange(N, dtype=np.int64)
-    rows_d = torch.arange(N, dtype=torch.int64, device=dev)
+    rows_d = torch.arange(N, dtype=torch.int64, device=dev)  # targets = pool = rows, resident
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step(timers=None):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timers is not None else None
         if ev:
             ev[0].record(stream)
-        st, _ = knn_device(nodes, n, all_idx, all_idx)
+        st, _ = knn_device(nodes, n, rows_d, rows_d)
         if ev:
             ev[1].record(stream)
         w, status, first_fail, n_rep = phs_weights_device(pos_d, rows_d, st, eng, fams, 3)
@@ -242,6 +242,22 @@ def main():
     for _ in range(args.warmup):
         y, ff, _ = step()
     torch.cuda.synchronize()
+    if os.environ.get("MF_BENCH_DEBUG"):
+        # host-side stage times with a synchronize after each stage (diagnostics only)
+        import time as _t
+        marks = []
+        t0 = _t.perf_counter()
+        st_, _ = knn_device(nodes, n, rows_d, rows_d); torch.cuda.synchronize(); marks.append(_t.perf_counter())
+        w_, *_ = phs_weights_device(pos_d, rows_d, st_, eng, fams, 3); torch.cuda.synchronize(); marks.append(_t.perf_counter())
+        store_ = mf.WeightStore(N, all_idx, st_, {"laplacian": w_[:, 0, :]}, n, rows_d=rows_d, positions_d=pos_d)
+        mat_ = store_.matrix("laplacian"); torch.cuda.synchronize(); marks.append(_t.perf_counter())
+        mat_.plan(True); torch.cuda.synchronize(); marks.append(_t.perf_counter())
+        mat_.apply_device(u_d); torch.cuda.synchronize(); marks.append(_t.perf_counter())
+        names = ["knn", "phs", "csr", "plan", "apply"]
+        prev = t0
+        for nm_, mk in zip(names, marks):
+            print(f"[debug] {nm_}: {1e3 * (mk - prev):.2f} ms", file=sys.stderr)
+            prev = mk
     assert int(ff.item()) == _lib.SENTINEL_OK, "shape solve reported a failing stencil"
 
     # fp64 pipe peak for the roofline denominator (measured in this run)

@@ -91,6 +91,45 @@ __device__ __forceinline__ bool key_lt(double d1, int i1, int c1, double d2, int
     return dl | (de & (il | (ie & (c1 < c2))));
 }
 
+__device__ __forceinline__ bool key_lt2(double d1, int i1, double d2, int i2) {
+    return (d1 < d2) | ((d1 == d2) & (i1 < i2));
+}
+
+// Bitonic sort of 64 keys (d2, index) held two per lane: element lane (d0, i0)
+// and element lane + 32 (d1, i1); ascending.  21 compare-exchange stages.
+__device__ __forceinline__ void bitonic64(double& d0, int& i0, double& d1, int& i1, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                if (key_lt2(d1, i1, d0, i0)) {
+                    double td = d0; d0 = d1; d1 = td;
+                    int ti = i0; i0 = i1; i1 = ti;
+                }
+            } else {
+                const bool lower = (lane & j) == 0;
+                {
+                    const double dp = __shfl_xor_sync(FULL, d0, j);
+                    const int ip = __shfl_xor_sync(FULL, i0, j);
+                    const bool asc = k == 64 ? true : ((lane & k) == 0);
+                    const bool take = (lower == asc) ? key_lt2(dp, ip, d0, i0) : key_lt2(d0, i0, dp, ip);
+                    d0 = take ? dp : d0;
+                    i0 = take ? ip : i0;
+                }
+                {
+                    const double dp = __shfl_xor_sync(FULL, d1, j);
+                    const int ip = __shfl_xor_sync(FULL, i1, j);
+                    const bool asc = k == 64 ? true : (((lane + 32) & k) == 0);
+                    const bool take = (lower == asc) ? key_lt2(dp, ip, d1, i1) : key_lt2(d1, i1, dp, ip);
+                    d1 = take ? dp : d1;
+                    i1 = take ? ip : i1;
+                }
+            }
+        }
+    }
+}
+
 struct Box {
     int clo[3], chi[3];
     double limit;  // K-th key must be <= limit to be provably inside
@@ -159,10 +198,10 @@ struct WarpSmem {
 
 // Exact K smallest keys by repeated arg-min over the cube (any size, any ties).
 // Writes sel/seld2[0..K) and returns the K-th d2.
-template <bool SEQ>
+template <bool SEQ, int DD>
 __device__ double extract_topk(const KnnArgs& a, const Box& b, const double* p, int K, WarpSmem& sm, int lane) {
     const GridParams& g = *a.gp;
-    const int d = a.d;
+    constexpr int d = DD;
     const int R = box_ranges(b, d);
     double pd = -INFINITY;
     int pi = -1, pc = -1;
@@ -208,8 +247,8 @@ __device__ double extract_topk(const KnnArgs& a, const Box& b, const double* p, 
     return pd;
 }
 
-template <bool SEQ>
-__global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const int32_t* __restrict__ order,
+template <bool SEQ, int DD>
+__global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const int32_t* __restrict__ order,
                                                             int64_t count, const unsigned long long* count_dev,
                                                             int K) {
     __shared__ WarpSmem smem[KNN_WARPS];
@@ -217,7 +256,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const in
     const int wib = threadIdx.x >> 5;
     WarpSmem& sm = smem[wib];
     const GridParams g = *a.gp;
-    const int d = a.d;
+    constexpr int d = DD;
     const int n = a.n;
     if (count_dev) count = (int64_t)*count_dev;
     // cube half-width giving ~1.5 K candidates
@@ -309,8 +348,34 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const in
                     hi = mx;
                     chi = count_le(hi);
                 }
+                // first guess from the local density of the cube: K' = K + WIN/2 points
+                // lie within r with M/vol * c_d r^d = K'
+                if (chi > K + KNN_WIN) {
+                    double vol = 1.0;
+                    for (int ax = 0; ax < d; ++ax) vol *= (double)(b.chi[ax] - b.clo[ax] + 1) * g.cw[ax];
+                    const double cdim = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
+                    const double want = (double)K + 0.5 * KNN_WIN;
+                    double rg = pow(want * vol / ((double)M * cdim), 1.0 / d);
+                    double tg = rg * rg;
+                    if (tg > 0.0 && tg < hi) {
+                        int c = count_le(tg);
+                        if (c >= K) {
+                            hi = tg;
+                            chi = c;
+                        } else {
+                            lo = tg;
+                        }
+                    }
+                }
                 for (int iter = 0; iter < 80 && chi > K + KNN_WIN; ++iter) {
-                    double mid = lo < 0.0 ? 0.5 * hi : lo + 0.5 * (hi - lo);
+                    // interpolate in r^d (count ~ r^d), fall back to bisection
+                    double mid;
+                    if (lo >= 0.0) {
+                        mid = lo + 0.5 * (hi - lo);
+                    } else {
+                        const double scale = pow(((double)K + 0.5 * KNN_WIN) / (double)chi, 2.0 / d);
+                        mid = hi * fmin(fmax(scale, 0.25), 0.95);
+                    }
                     if (!(mid < hi) || (lo >= 0.0 && !(mid > lo))) break;
                     int c = count_le(mid);
                     if (c >= K) {
@@ -320,7 +385,42 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const in
                         lo = mid;
                     }
                 }
-                if (chi >= K && chi <= KNN_SCAP) {
+                if (chi >= K && chi <= 64) {
+                    // compact the survivors, then a 64-key bitonic sort in registers
+                    int base = 0;
+#pragma unroll
+                    for (int it = 0; it < KNN_MAXIT; ++it) {
+                        if (it * 32 < M) {
+                            bool keep = cd[it] <= hi;
+                            unsigned bal = __ballot_sync(FULL, keep);
+                            if (keep) {
+                                int at = base + __popc(bal & ((1u << lane) - 1u));
+                                sm.sd2[at] = cd[it];
+                                sm.sid[at] = ci[it];
+                            }
+                            base += __popc(bal);
+                        }
+                    }
+                    __syncwarp();
+                    double d0 = lane < base ? sm.sd2[lane] : INFINITY;
+                    int i0 = lane < base ? sm.sid[lane] : 0x7fffffff;
+                    double d1 = lane + 32 < base ? sm.sd2[lane + 32] : INFINITY;
+                    int i1 = lane + 32 < base ? sm.sid[lane + 32] : 0x7fffffff;
+                    __syncwarp();
+                    bitonic64(d0, i0, d1, i1, lane);
+                    if (lane < K) {
+                        sm.sel[lane] = i0;
+                        sm.seld2[lane] = d0;
+                    }
+                    if (lane + 32 < K) {
+                        sm.sel[lane + 32] = i1;
+                        sm.seld2[lane + 32] = d1;
+                    }
+                    __syncwarp();
+                    dK = sm.seld2[K - 1];
+                    done = true;
+                }
+                if (!done && chi >= K && chi <= KNN_SCAP) {
                     // compact survivors (d2 <= hi) into shared memory
                     int base = 0;
 #pragma unroll
@@ -355,7 +455,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnArgs a, const in
                 }
             }
             if (!done) {
-                dK = extract_topk<SEQ>(a, b, p, K, sm, lane);
+                dK = extract_topk<SEQ, DD>(a, b, p, K, sm, lane);
                 if (!b.all && !(dK <= b.limit)) continue;
             }
             break;
@@ -610,12 +710,13 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
 
     const int K = (int)(n + 8 < P ? n + 8 : P);
     KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
-    knn_kernel<false><<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, 0, st>>>(a, order, T, nullptr, K);
+    auto main_k = d == 1 ? knn_kernel<false, 1> : (d == 2 ? knn_kernel<false, 2> : knn_kernel<false, 3>);
+    auto strd_k = d == 1 ? knn_kernel<true, 1> : (d == 2 ? knn_kernel<true, 2> : knn_kernel<true, 3>);
+    main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, 0, st>>>(a, order, T, nullptr, K);
     MF_LAUNCH_CHECK();
     if (K > n) {
         // straddle rows: top-n by the sequential-sum metric (stencils.py:67-75)
-        knn_kernel<true><<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, 0, st>>>(a, L.straddle_list, T,
-                                                                                L.straddle_count, n);
+        strd_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, 0, st>>>(a, L.straddle_list, T, L.straddle_count, n);
         MF_LAUNCH_CHECK();
     }
     if (n_straddle)

@@ -27,7 +27,7 @@ def knn_device(nodes: NodeSet, n: int, targets: np.ndarray, pool: np.ndarray):
     N, d = nodes.positions.shape
     if d > 3:
         raise ConfigError(f"GPU stencil selection supports d <= 3, got {d}")
-    T, P = int(targets.shape[0]), int(pool.shape[0])
+    T, P = int(targets.shape[0]), int(pool.shape[0])  # host arrays or resident device tensors
     pos = nodes.positions_device()
     t_d = _lib.to_device(targets, torch.int64)
     p_d = _lib.to_device(pool, torch.int64)
