@@ -16,6 +16,9 @@ int launch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count,
 template <int NN, int DEG, int DD, int NF>
 int launch_mma(const PhsArgs& a, cudaStream_t st, int sms);
 
+template <int NN, int DEG, int DD, int NF>
+int launch_split(const PhsArgs& a, cudaStream_t st, int sms);
+
 template <bool REPLAY>
 int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
                  cudaStream_t st, int sms) {
@@ -28,14 +31,24 @@ int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     return MF_ERR_UNSUPPORTED;
 }
 
-// FAST/HYBRID first pass: the register rank-1 kernel (measured fastest so far);
-// MF_PHS_KERNEL=mma selects the tensor-core blocked LU (phs_mma.cuh)
+// FAST/HYBRID first pass.  Default: the register rank-1 kernel (phs_reg.cuh),
+// measured fastest.  MF_PHS_KERNEL=split selects the split-row variant
+// (phs_split.cuh), =mma the tensor-core blocked LU (phs_mma.cuh).
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms) {
-    static const bool use_mma = [] {
+    static const int which = [] {
         const char* e = getenv("MF_PHS_KERNEL");
-        return e && strcmp(e, "mma") == 0;
+        if (e && strcmp(e, "mma") == 0) return 2;
+        if (e && strcmp(e, "split") == 0) return 3;
+        return 1;
     }();
-    if (use_mma) {
+    if (which == 3) {
+        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
+        if (d == 3 && n == 35 && l == 10 && nf == 1) {
+            int rc = launch_split<35, 2, 3, 1>(a, st, sms);
+            if (rc != MF_ERR_UNSUPPORTED) return rc;
+        }
+    }
+    if (which == 2) {
         const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
         int rc = MF_ERR_UNSUPPORTED;
         if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_mma<35, 2, 3, 1>(a, st, sms);

@@ -1,7 +1,8 @@
-// Register and tensor-core shape solves instantiated for n=35, degree 2, d=3, 1 family.
-#include "phs_mma.cuh"
+// Shape-solve kernels instantiated for n=35, degree 2, d=3, 1 family (config C3).
+#include "phs_split.cuh"
 
 namespace mf {
 MF_INSTANTIATE_REG(35, 2, 3, 1)
 MF_INSTANTIATE_MMA(35, 2, 3, 1)
+MF_INSTANTIATE_SPLIT(35, 2, 3, 1)
 }  // namespace mf
