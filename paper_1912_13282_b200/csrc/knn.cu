@@ -27,7 +27,6 @@ namespace mf {
 
 constexpr double KNN_OCC = 2.0;   // mean pool points per grid cell
 constexpr int KNN_WARPS = 4;      // warps per block
-constexpr int KNN_MAXIT = 16;     // register candidate slots per lane (512 per warp)
 constexpr int KNN_SCAP = 256;     // survivor capacity per warp (shared memory)
 constexpr int KNN_RMAX = 255;     // cell-row ranges per cube held in shared memory
 constexpr int KNN_WIN = 16;       // bisection stops at <= K + WIN survivors
@@ -95,35 +94,43 @@ __device__ __forceinline__ bool key_lt2(double d1, int i1, double d2, int i2) {
     return (d1 < d2) | ((d1 == d2) & (i1 < i2));
 }
 
-// Bitonic sort of 64 keys (d2, index) held two per lane: element lane (d0, i0)
-// and element lane + 32 (d1, i1); ascending.  21 compare-exchange stages.
-__device__ __forceinline__ void bitonic64(double& d0, int& i0, double& d1, int& i1, int lane) {
+// Bitonic sort of 32*NS keys (d2, index), NS per lane: element e = lane + 32*s
+// in slot s; ascending.  Exchanges across lanes use shuffles, across slots
+// (distances 32, 64) stay in registers.
+template <int NS>
+__device__ __forceinline__ void bitonic_sort(double (&dk)[NS], int (&ik)[NS], int lane) {
+    constexpr int TOT = 32 * NS;
 #pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
+    for (int k = 2; k <= TOT; k <<= 1) {
 #pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {
-                if (key_lt2(d1, i1, d0, i0)) {
-                    double td = d0; d0 = d1; d1 = td;
-                    int ti = i0; i0 = i1; i1 = ti;
+            if (j >= 32) {
+                const int js = j >> 5;
+#pragma unroll
+                for (int sl = 0; sl < NS; ++sl) {
+                    if ((sl & js) == 0) {
+                        const int sp = sl | js;
+                        const bool asc = ((lane + 32 * sl) & k) == 0;
+                        const bool sw = asc ? key_lt2(dk[sp], ik[sp], dk[sl], ik[sl])
+                                            : key_lt2(dk[sl], ik[sl], dk[sp], ik[sp]);
+                        const double td = dk[sl];
+                        const int ti = ik[sl];
+                        dk[sl] = sw ? dk[sp] : dk[sl];
+                        ik[sl] = sw ? ik[sp] : ik[sl];
+                        dk[sp] = sw ? td : dk[sp];
+                        ik[sp] = sw ? ti : ik[sp];
+                    }
                 }
             } else {
                 const bool lower = (lane & j) == 0;
-                {
-                    const double dp = __shfl_xor_sync(FULL, d0, j);
-                    const int ip = __shfl_xor_sync(FULL, i0, j);
-                    const bool asc = k == 64 ? true : ((lane & k) == 0);
-                    const bool take = (lower == asc) ? key_lt2(dp, ip, d0, i0) : key_lt2(d0, i0, dp, ip);
-                    d0 = take ? dp : d0;
-                    i0 = take ? ip : i0;
-                }
-                {
-                    const double dp = __shfl_xor_sync(FULL, d1, j);
-                    const int ip = __shfl_xor_sync(FULL, i1, j);
-                    const bool asc = k == 64 ? true : (((lane + 32) & k) == 0);
-                    const bool take = (lower == asc) ? key_lt2(dp, ip, d1, i1) : key_lt2(d1, i1, dp, ip);
-                    d1 = take ? dp : d1;
-                    i1 = take ? ip : i1;
+#pragma unroll
+                for (int sl = 0; sl < NS; ++sl) {
+                    const double dp = __shfl_xor_sync(FULL, dk[sl], j);
+                    const int ip = __shfl_xor_sync(FULL, ik[sl], j);
+                    const bool asc = ((lane + 32 * sl) & k) == 0;
+                    const bool take = (lower == asc) ? key_lt2(dp, ip, dk[sl], ik[sl]) : key_lt2(dk[sl], ik[sl], dp, ip);
+                    dk[sl] = take ? dp : dk[sl];
+                    ik[sl] = take ? ip : ik[sl];
                 }
             }
         }
@@ -247,7 +254,7 @@ __device__ double extract_topk(const KnnArgs& a, const Box& b, const double* p, 
     return pd;
 }
 
-template <bool SEQ, int DD>
+template <bool SEQ, int DD, int MAXIT, int NS>
 __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const int32_t* __restrict__ order,
                                                             int64_t count, const unsigned long long* count_dev,
                                                             int K) {
@@ -309,13 +316,13 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
             if (M < K) continue;
 
             bool done = false;
-            if (small && M <= 32 * KNN_MAXIT) {
+            if (small && M <= 32 * MAXIT) {
                 // ---- register path: candidates c = it*32 + lane
-                double cd[KNN_MAXIT];
-                int ci[KNN_MAXIT];
+                double cd[MAXIT];
+                int ci[MAXIT];
                 int rc = 0;
 #pragma unroll
-                for (int it = 0; it < KNN_MAXIT; ++it) {
+                for (int it = 0; it < MAXIT; ++it) {
                     int c = it * 32 + lane;
                     cd[it] = INFINITY;
                     ci[it] = 0x7fffffff;
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                 auto count_le = [&](double t) {
                     int c = 0;
 #pragma unroll
-                    for (int it = 0; it < KNN_MAXIT; ++it)
+                    for (int it = 0; it < MAXIT; ++it)
                         if (it * 32 < M) c += __popc(__ballot_sync(FULL, cd[it] <= t));
                     return c;
                 };
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                 if (hi == INFINITY) {
                     double mx = 0.0;
 #pragma unroll
-                    for (int it = 0; it < KNN_MAXIT; ++it)
+                    for (int it = 0; it < MAXIT; ++it)
                         if (cd[it] != INFINITY) mx = fmax(mx, cd[it]);
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
@@ -385,11 +392,11 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                         lo = mid;
                     }
                 }
-                if (chi >= K && chi <= 64) {
-                    // compact the survivors, then a 64-key bitonic sort in registers
+                if (chi >= K && chi <= 32 * NS) {
+                    // compact the survivors, then a 32*NS-key bitonic sort in registers
                     int base = 0;
 #pragma unroll
-                    for (int it = 0; it < KNN_MAXIT; ++it) {
+                    for (int it = 0; it < MAXIT; ++it) {
                         if (it * 32 < M) {
                             bool keep = cd[it] <= hi;
                             unsigned bal = __ballot_sync(FULL, keep);
@@ -402,19 +409,23 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                         }
                     }
                     __syncwarp();
-                    double d0 = lane < base ? sm.sd2[lane] : INFINITY;
-                    int i0 = lane < base ? sm.sid[lane] : 0x7fffffff;
-                    double d1 = lane + 32 < base ? sm.sd2[lane + 32] : INFINITY;
-                    int i1 = lane + 32 < base ? sm.sid[lane + 32] : 0x7fffffff;
-                    __syncwarp();
-                    bitonic64(d0, i0, d1, i1, lane);
-                    if (lane < K) {
-                        sm.sel[lane] = i0;
-                        sm.seld2[lane] = d0;
+                    double dk[NS];
+                    int ik[NS];
+#pragma unroll
+                    for (int sl = 0; sl < NS; ++sl) {
+                        const int e = lane + 32 * sl;
+                        dk[sl] = e < base ? sm.sd2[e] : INFINITY;
+                        ik[sl] = e < base ? sm.sid[e] : 0x7fffffff;
                     }
-                    if (lane + 32 < K) {
-                        sm.sel[lane + 32] = i1;
-                        sm.seld2[lane + 32] = d1;
+                    __syncwarp();
+                    bitonic_sort<NS>(dk, ik, lane);
+#pragma unroll
+                    for (int sl = 0; sl < NS; ++sl) {
+                        const int e = lane + 32 * sl;
+                        if (e < K) {
+                            sm.sel[e] = ik[sl];
+                            sm.seld2[e] = dk[sl];
+                        }
                     }
                     __syncwarp();
                     dK = sm.seld2[K - 1];
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                     // compact survivors (d2 <= hi) into shared memory
                     int base = 0;
 #pragma unroll
-                    for (int it = 0; it < KNN_MAXIT; ++it) {
+                    for (int it = 0; it < MAXIT; ++it) {
                         if (it * 32 < M) {
                             bool keep = cd[it] <= hi;
                             unsigned bal = __ballot_sync(FULL, keep);
@@ -710,8 +721,12 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
 
     const int K = (int)(n + 8 < P ? n + 8 : P);
     KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
-    auto main_k = d == 1 ? knn_kernel<false, 1> : (d == 2 ? knn_kernel<false, 2> : knn_kernel<false, 3>);
-    auto strd_k = d == 1 ? knn_kernel<true, 1> : (d == 2 ? knn_kernel<true, 2> : knn_kernel<true, 3>);
+    // candidates per warp (32 * MAXIT) and sort width (32 * NS) sized by K
+    const bool big = K + KNN_WIN > 64;
+    auto main_k = big ? (d == 1 ? knn_kernel<false, 1, 32, 4> : (d == 2 ? knn_kernel<false, 2, 32, 4> : knn_kernel<false, 3, 32, 4>))
+                      : (d == 1 ? knn_kernel<false, 1, 16, 2> : (d == 2 ? knn_kernel<false, 2, 16, 2> : knn_kernel<false, 3, 16, 2>));
+    auto strd_k = big ? (d == 1 ? knn_kernel<true, 1, 32, 4> : (d == 2 ? knn_kernel<true, 2, 32, 4> : knn_kernel<true, 3, 32, 4>))
+                      : (d == 1 ? knn_kernel<true, 1, 16, 2> : (d == 2 ? knn_kernel<true, 2, 16, 2> : knn_kernel<true, 3, 16, 2>));
     main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, 0, st>>>(a, order, T, nullptr, K);
     MF_LAUNCH_CHECK();
     if (K > n) {

@@ -392,8 +392,10 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
     int rc = fill_phs_params(a.P, d, k, even, expos, l, base_bot, kinds, ax_a, ax_b, orders, nf, scale_code);
     if (rc != MF_OK) return rc;
 
+    const bool big = n + l > 48;  // CTA-per-stencil kernel for large systems
     if (mode == MF_PHS_REPLAY) {
         rc = launch_phs_replay_reg(a, nullptr, nullptr, m, st, sm_count());
+        if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_cta(a, true, nullptr, nullptr, m, st, sm_count());
         if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<true>(a, nullptr, nullptr, m, st);
         return rc;
     }
@@ -413,10 +415,12 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
         a.flag_count = flag_count;
     }
     rc = launch_phs_fast(a, st, sm_count());
+    if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_cta(a, false, nullptr, nullptr, m, st, sm_count());
     if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<false>(a, nullptr, nullptr, m, st);
     if (rc != MF_OK) return rc;
     if (mode == MF_PHS_HYBRID) {
         rc = launch_phs_replay_reg(a, flag_list, flag_count, m, st, sm_count());
+        if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_cta(a, true, flag_list, flag_count, m, st, sm_count());
         if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<true>(a, flag_list, flag_count, m, st);
         if (rc != MF_OK) return rc;
         if (n_replayed) MF_CUDA_CHECK(cudaMemcpyAsync(n_replayed, flag_count, sizeof(int64_t),

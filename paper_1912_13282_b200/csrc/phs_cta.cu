@@ -1,0 +1,353 @@
+// CTA-per-stencil shape solve for large or unusual stencil shapes (sm_100a).
+//
+// One thread block (W warps) per stencil; the augmented system [A | B] lives
+// in shared memory (s x (s + nrhs) doubles: 92 KB for C5's s = 105, so two
+// blocks per SM).  The W warps split every elimination step: the pivot search
+// is a block-wide argmax over (|a|, position) (warp REDUX-free reduction +
+// shared scratch), the row swap and rank-1 update are distributed rows-over-
+// warps / columns-over-lanes with the pivot row cached in registers.
+// REPLAY follows _solve_multi (_phs_batch.py:142-184) op for op; FAST uses FMA
+// and carries the +-1 probe right-hand side for the HYBRID criterion, exactly
+// as the warp kernels do.
+#include "common.cuh"
+#include "phs_params.cuh"
+
+namespace mf {
+
+constexpr int CTA_WARPS = 8;
+constexpr int CTA_THREADS = CTA_WARPS * 32;
+constexpr int CTA_MAXCOLS = 128;  // s + nrhs: pivot-row cache of 4 values per lane
+
+__host__ __device__ inline size_t cta_doubles(int n, int d, int s, int nrhs) {
+    size_t v = (size_t)n * d + (size_t)s * (s + nrhs) + (size_t)nrhs * s + 4 * CTA_WARPS + 8;
+    return (v + 1) & ~(size_t)1;
+}
+
+// block-wide argmax of (value, -pos), NaN never wins; returns via shared scratch
+__device__ __forceinline__ void block_argmax(double v, int pos, double* sv, int* sp, double& best, int& bpos) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(FULL, v, o);
+        int op = __shfl_xor_sync(FULL, pos, o);
+        if (ov > v || (ov == v && op < pos)) {
+            v = ov;
+            pos = op;
+        }
+    }
+    if (lane == 0) {
+        sv[w] = v;
+        sp[w] = pos;
+    }
+    __syncthreads();
+    best = sv[0];
+    bpos = sp[0];
+    for (int k = 1; k < CTA_WARPS; ++k) {
+        if (sv[k] > best || (sv[k] == best && sp[k] < bpos)) {
+            best = sv[k];
+            bpos = sp[k];
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double block_reduce_max(double v, double* sv) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+    if (lane == 0) sv[w] = v;
+    __syncthreads();
+    double r = sv[0];
+    for (int k = 1; k < CTA_WARPS; ++k) r = fmax(r, sv[k]);
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ double block_reduce_min(double v, double* sv) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+    if (lane == 0) sv[w] = v;
+    __syncthreads();
+    double r = sv[0];
+    for (int k = 1; k < CTA_WARPS; ++k) r = fmin(r, sv[k]);
+    __syncthreads();
+    return r;
+}
+
+template <bool REPLAY>
+__global__ void __launch_bounds__(CTA_THREADS) phs_cta(PhsArgs a, const int64_t* __restrict__ list,
+                                                       const int64_t* __restrict__ list_count) {
+    extern __shared__ double smem_c[];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n = a.n, d = a.P.d, l = a.P.l, nf = a.P.nf;
+    const int s = n + l;
+    constexpr bool PROBE = !REPLAY;
+    const int nrhs = nf + (PROBE ? 1 : 0);
+    const int lda = s + nrhs;
+    double* loc = smem_c;
+    double* A = loc + n * d;
+    double* scr = A + (size_t)s * lda;
+    double* red = scr + (size_t)nrhs * s;
+    int* redi = reinterpret_cast<int*>(red + 2 * CTA_WARPS);
+    const int64_t count = list ? *list_count : a.m;
+    const bool want_flag = PROBE && a.flag_list != nullptr;
+    const bool want_est = PROBE && (a.flag_list != nullptr || a.kappa != nullptr);
+    const PhsParams& P = a.P;
+
+    for (int64_t it = blockIdx.x; it < count; it += gridDim.x) {
+        const int64_t idx = list ? list[it] : it;
+        const int64_t row = a.rows[idx];
+        const int32_t* sti = a.stencils + idx * n;
+        // 1. local coordinates (_phs_batch.py:198-202)
+        for (int e = tid; e < n * d; e += CTA_THREADS) {
+            int j = e / d, ax = e - j * d;
+            loc[e] = __dsub_rn(a.pos[(int64_t)sti[j] * d + ax], a.pos[row * d + ax]);
+        }
+        __syncthreads();
+        // 2. scale (_phs_batch.py:204-221)
+        int stat = 0;
+        double sc = 1.0;
+        if (P.scale_code != MF_SCALE_NONE) {
+            const bool nearest = P.scale_code == MF_SCALE_NEAREST;
+            double best = nearest ? INFINITY : -1.0;
+            for (int j = tid; j < n; j += CTA_THREADS) {
+                double r2 = 0.0;
+                for (int ax = 0; ax < d; ++ax) r2 = __dadd_rn(r2, __dmul_rn(loc[j * d + ax], loc[j * d + ax]));
+                double r = __dsqrt_rn(r2);
+                if (nearest) {
+                    if (r > 0.0 && r < best) best = r;
+                } else if (r > best) {
+                    best = r;
+                }
+            }
+            best = nearest ? block_reduce_min(best, red) : block_reduce_max(best, red);
+            if (nearest ? (best == INFINITY) : !(best > 0.0)) stat = 2;
+            else sc = best;
+        }
+        double anorm = 0.0, r2min = INFINITY, rc2max = 0.0;
+        if (stat == 0) {
+            for (int e = tid; e < n * d; e += CTA_THREADS) loc[e] = __ddiv_rn(loc[e], sc);
+            __syncthreads();
+            // 3. system (_phs_batch.py:228-290); PHS block symmetric, one evaluation per pair
+            for (int e = tid; e < n * n; e += CTA_THREADS) {
+                int i = e / n, j = e - i * n;
+                if (j < i) continue;
+                double v = 0.0;
+                if (j > i) {
+                    double r2 = 0.0;
+                    for (int ax = 0; ax < d; ++ax) {
+                        double df = __dsub_rn(loc[i * d + ax], loc[j * d + ax]);
+                        r2 = __dadd_rn(r2, __dmul_rn(df, df));
+                    }
+                    r2min = fmin(r2min, r2);
+                    v = phs_phi(__dsqrt_rn(r2), P.k, P.even);
+                }
+                A[(size_t)i * lda + j] = v;
+                A[(size_t)j * lda + i] = v;
+            }
+            for (int e = tid; e < n * l; e += CTA_THREADS) {
+                int jm = e / n, i = e - jm * n;
+                double q = phs_monomial(loc + i * d, P.expos + jm * d, d);
+                A[(size_t)i * lda + n + jm] = q;
+                A[(size_t)(n + jm) * lda + i] = q;
+            }
+            for (int e = tid; e < l * l; e += CTA_THREADS) {
+                int i = e / l, j = e - i * l;
+                A[(size_t)(n + i) * lda + n + j] = 0.0;
+            }
+            for (int j = tid; j < n; j += CTA_THREADS) {
+                double top[MF_MAX_FAMILIES];
+                phs_rhs_top(loc + j * d, d, P, top);
+                for (int f = 0; f < nf; ++f) A[(size_t)j * lda + s + f] = __dmul_rn(top[f], pow_cr_int(sc, -P.orders[f]));
+                double rc2 = 0.0;
+                for (int ax = 0; ax < d; ++ax) rc2 = fma(loc[j * d + ax], loc[j * d + ax], rc2);
+                rc2max = fmax(rc2max, rc2);
+            }
+            for (int e = tid; e < l * nf; e += CTA_THREADS) {
+                int f = e / l, j = e - f * l;
+                A[(size_t)(n + j) * lda + s + f] = __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + j], pow_cr_int(sc, -P.orders[f]));
+            }
+            if (PROBE)
+                for (int r = tid; r < s; r += CTA_THREADS) A[(size_t)r * lda + s + nf] = probe_sign(idx, r);
+            __syncthreads();
+            if (want_est) {
+                double mx = 0.0;
+                for (int r = tid; r < s; r += CTA_THREADS) {
+                    double acc = 0.0;
+                    for (int c = 0; c < s; ++c) acc += fabs(A[(size_t)r * lda + c]);
+                    mx = fmax(mx, acc);
+                }
+                anorm = block_reduce_max(mx, red);
+            }
+            // 4. elimination with row partial pivoting (_phs_batch.py:150-176)
+            for (int col = 0; col < s; ++col) {
+                double best = -1.0;
+                int piv = 0x7fffffff;
+                for (int r = col + tid; r < s; r += CTA_THREADS) {
+                    double v = fabs(A[(size_t)r * lda + col]);
+                    if (v > best) {
+                        best = v;
+                        piv = r;
+                    }
+                }
+                const double a00 = fabs(A[(size_t)col * lda + col]);
+                block_argmax(best, piv, red, redi, best, piv);
+                if (isnan(a00) || best == 0.0 || !isfinite(best) || piv == 0x7fffffff) {
+                    stat = 1;
+                    break;
+                }
+                if (piv != col) {
+                    for (int cc = col + tid; cc < lda; cc += CTA_THREADS) {
+                        double t = A[(size_t)col * lda + cc];
+                        A[(size_t)col * lda + cc] = A[(size_t)piv * lda + cc];
+                        A[(size_t)piv * lda + cc] = t;
+                    }
+                    __syncthreads();
+                }
+                const double inv = __drcp_rn(A[(size_t)col * lda + col]);
+                const double* prow = A + (size_t)col * lda;
+                double pv[CTA_MAXCOLS / 32];
+#pragma unroll
+                for (int q = 0; q < CTA_MAXCOLS / 32; ++q) {
+                    const int cc = col + 1 + lane + 32 * q;
+                    pv[q] = cc < lda ? prow[cc] : 0.0;
+                }
+                for (int r = col + 1 + w; r < s; r += CTA_WARPS) {
+                    double* arow = A + (size_t)r * lda;
+                    const double fac = REPLAY ? __dmul_rn(arow[col], inv) : arow[col] * inv;
+                    if (fac != 0.0) {
+#pragma unroll
+                        for (int q = 0; q < CTA_MAXCOLS / 32; ++q) {
+                            const int cc = col + 1 + lane + 32 * q;
+                            if (cc < lda) {
+                                if (REPLAY) arow[cc] = __dsub_rn(arow[cc], __dmul_rn(fac, pv[q]));
+                                else arow[cc] = fma(-fac, pv[q], arow[cc]);
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (stat == 0) {
+            // 5. back-substitution (_phs_batch.py:177-183)
+            if (REPLAY) {
+                for (int col = s - 1; col >= 0; --col) {
+                    const int len = s - col - 1;
+                    for (int e = tid; e < len * nf; e += CTA_THREADS) {
+                        int f = e / len, r = col + 1 + (e - f * len);
+                        scr[f * s + r] = __dmul_rn(A[(size_t)col * lda + r], A[(size_t)r * lda + s + f]);
+                    }
+                    __syncthreads();
+                    if (tid < nf) {
+                        double acc = A[(size_t)col * lda + s + tid];
+                        for (int r = col + 1; r < s; ++r) acc = __dsub_rn(acc, scr[tid * s + r]);
+                        A[(size_t)col * lda + s + tid] = __dmul_rn(acc, __drcp_rn(A[(size_t)col * lda + col]));
+                    }
+                    __syncthreads();
+                }
+            } else {
+                for (int col = s - 1; col >= 0; --col) {
+                    if (tid < nrhs) A[(size_t)col * lda + s + tid] *= __drcp_rn(A[(size_t)col * lda + col]);
+                    __syncthreads();
+                    for (int e = tid; e < col * nrhs; e += CTA_THREADS) {
+                        int f = e / col, r = e - f * col;
+                        A[(size_t)r * lda + s + f] =
+                            fma(-A[(size_t)r * lda + col], A[(size_t)col * lda + s + f], A[(size_t)r * lda + s + f]);
+                    }
+                    __syncthreads();
+                }
+            }
+            // 6. outputs, non-finite check (_phs_batch.py:293-298)
+            double badv = 0.0;
+            for (int e = tid; e < n * nf; e += CTA_THREADS) {
+                int f = e / n, j = e - f * n;
+                double v = A[(size_t)j * lda + s + f];
+                if (!isfinite(v)) badv = 1.0;
+                a.out[((size_t)idx * nf + f) * n + j] = v;
+            }
+            if (block_reduce_max(badv, red) > 0.0) stat = 1;
+            if (want_est && stat == 0) {
+                double zw = 0.0, za = 0.0;
+                for (int r = tid; r < s; r += CTA_THREADS) {
+                    double v = fabs(A[(size_t)r * lda + s + nf]);
+                    za = fmax(za, v);
+                    if (r < n) zw = fmax(zw, v);
+                }
+                zw = block_reduce_max(zw, red);
+                za = block_reduce_max(za, red);
+                double ratio = 0.0;
+                for (int f = 0; f < nf; ++f) {
+                    double xa = 0.0, xw = 0.0;
+                    for (int r = tid; r < s; r += CTA_THREADS) {
+                        double v = fabs(A[(size_t)r * lda + s + f]);
+                        xa = fmax(xa, v);
+                        if (r < n) xw = fmax(xw, v);
+                    }
+                    xa = block_reduce_max(xa, red);
+                    xw = block_reduce_max(xw, red);
+                    ratio = fmax(ratio, xa / xw);
+                }
+                r2min = block_reduce_min(r2min, red);
+                rc2max = block_reduce_max(rc2max, red);
+                const double est = anorm * zw * ratio;
+                const bool close = r2min < a.min_sep2 * rc2max;
+                if (tid == 0 && a.kappa) {
+                    a.kappa[4 * idx + 0] = anorm;
+                    a.kappa[4 * idx + 1] = zw;
+                    a.kappa[4 * idx + 2] = za;
+                    a.kappa[4 * idx + 3] = ratio;
+                }
+                if (want_flag && tid == 0 && (close || !(est <= a.hybrid_thresh))) {
+                    unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+                    a.flag_list[slot] = idx;
+                }
+            }
+        }
+        if (want_flag && stat != 0) {
+            if (tid == 0) {
+                unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+                a.flag_list[slot] = idx;
+            }
+            stat = 0;
+        }
+        if (tid == 0) {
+            a.status[idx] = (int8_t)stat;
+            if (stat && a.first_fail) atomicMin((unsigned long long*)a.first_fail, (unsigned long long)idx);
+        }
+        __syncthreads();
+    }
+}
+
+template <bool REPLAY>
+int launch_cta_t(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count, cudaStream_t st,
+                 int sms) {
+    const int s = a.n + a.P.l;
+    const int nrhs = a.P.nf + (REPLAY ? 0 : 1);
+    if (s + nrhs > CTA_MAXCOLS) return MF_ERR_UNSUPPORTED;
+    const size_t bytes = cta_doubles(a.n, a.P.d, s, nrhs) * sizeof(double);
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (bytes > (size_t)max_smem) return MF_ERR_UNSUPPORTED;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(phs_cta<REPLAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int per_sm = 0;
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phs_cta<REPLAY>, CTA_THREADS, bytes));
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = max_count;
+    int64_t cap = (int64_t)sms * per_sm * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    phs_cta<REPLAY><<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a, list, list_count);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+int launch_phs_cta(const PhsArgs& a, bool replay, const int64_t* list, const int64_t* list_count,
+                   int64_t max_count, cudaStream_t st, int sms) {
+    return replay ? launch_cta_t<true>(a, list, list_count, max_count, st, sms)
+                  : launch_cta_t<false>(a, list, list_count, max_count, st, sms);
+}
+
+}  // namespace mf
