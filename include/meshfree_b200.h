@@ -162,7 +162,7 @@ int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatt
 
 /* ---- explicit Neumann closure ---------------------------------------------------
  * For listed node i with stencil row r = node_row[i] (stencils m x n int32,
- * stencil order): c_j = sum_a normals[i,a] * w_d1[a*mn + r*n + j]
+ * stencil order, listed as nodes[k]): c_j = sum_a normals[k,a] * w_d1[a*mn + r*n + j]
  * (storage.py:226-234), pivot guard |c_0| < 1e-12 ||c||_2 (storage.py:240-245),
  * value (gn[k] - sum_{j>=1} c_j u[st_j]) / c_0 (storage.py:246-250).
  * out (count, nullable) receives the values; u_scatter (N, nullable) gets
@@ -175,7 +175,7 @@ typedef struct {
     const double* w_d1; /* d planes of m*n weights (families d1_0..d1_{d-1}) */
     int64_t mn;
     int32_t d;
-    const double* normals; /* N x d */
+    const double* normals; /* count x d, row k = normal of nodes[k] */
     const int64_t* nodes;  /* count */
     const int64_t* node_row; /* N */
     const double* gn;      /* count */

@@ -133,6 +133,8 @@ def to_device(a, dtype) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:  # broadcast views: torch.from_numpy needs a writable buffer
+        arr = arr.copy()
     t = torch.from_numpy(arr)
     if t.dtype != dtype:
         t = t.to(dtype)

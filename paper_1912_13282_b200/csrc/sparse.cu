@@ -173,11 +173,11 @@ __global__ void __launch_bounds__(256) ell_apply_k(const int32_t* __restrict__ e
 // ---------------------------------------------------------------------------
 // Explicit Neumann closure (storage.py:226-250), one thread per listed node.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double neumann_coef(const mf_neumann_t& nm, int64_t i, int64_t base, int j) {
-    // c = n_0 w_0 + n_1 w_1 + ... accumulated per axis (storage.py:231-234)
-    double c = __dmul_rn(nm.normals[i * nm.d + 0], nm.w_d1[base + j]);
+__device__ __forceinline__ double neumann_coef(const mf_neumann_t& nm, int64_t k, int64_t base, int j) {
+    // c = n_0 w_0 + n_1 w_1 + ... accumulated per axis (storage.py:231-234); normals are per listed node
+    double c = __dmul_rn(nm.normals[k * nm.d + 0], nm.w_d1[base + j]);
     for (int a = 1; a < nm.d; ++a)
-        c = __dadd_rn(c, __dmul_rn(nm.normals[i * nm.d + a], nm.w_d1[(int64_t)a * nm.mn + base + j]));
+        c = __dadd_rn(c, __dmul_rn(nm.normals[k * nm.d + a], nm.w_d1[(int64_t)a * nm.mn + base + j]));
     return c;
 }
 
@@ -190,10 +190,10 @@ __global__ void neumann_k(mf_neumann_t nm, const double* __restrict__ u, double*
         const int64_t base = nm.node_row[i] * nm.n;
         double ss = 0.0;
         for (int j = 0; j < nm.n; ++j) {
-            double c = neumann_coef(nm, i, base, j);
+            double c = neumann_coef(nm, k, base, j);
             ss = fma(c, c, ss);
         }
-        const double pivot = neumann_coef(nm, i, base, 0);
+        const double pivot = neumann_coef(nm, k, base, 0);
         double val;
         if (fabs(pivot) < 1e-12 * sqrt(ss)) {
             if (bad) atomicMin((unsigned long long*)bad, (unsigned long long)k);
@@ -201,7 +201,7 @@ __global__ void neumann_k(mf_neumann_t nm, const double* __restrict__ u, double*
         } else {
             double acc = nm.gn[k];
             for (int j = 1; j < nm.n; ++j)
-                acc = __dsub_rn(acc, __dmul_rn(neumann_coef(nm, i, base, j), u[nm.stencils[base + j]]));
+                acc = __dsub_rn(acc, __dmul_rn(neumann_coef(nm, k, base, j), u[nm.stencils[base + j]]));
             val = __ddiv_rn(acc, pivot);
         }
         if (out) out[k] = val;
