@@ -62,6 +62,15 @@ struct Arena {
 // ---- device helpers -----------------------------------------------------------
 
 // Monotone map of a double onto uint64 (for atomic min/max over doubles).
+// A value the compiler cannot prove loop-invariant: conditions on kernel
+// parameters inside the big per-stencil loops would otherwise be unswitched,
+// duplicating the whole loop body in the instruction cache.
+__device__ __forceinline__ int opaque(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long ordered_bits(double x) {
     unsigned long long u = (unsigned long long)__double_as_longlong(x);
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);

@@ -15,8 +15,8 @@
 //   4. v solves K v = Z^T (f - Phi w_p), and w = w_p + Z v.
 // One warp per stencil; lane c owns reduced row c (n - l <= 32), so the
 // back-substitution runs on registers and shuffles.  The +-1 probe rides along
-// as one more right-hand side, and lambda (for the sensitivity estimate) comes
-// from Q1 lambda = (f - Phi w)_piv.  Rounding differs from the reference's LU;
+// as one more right-hand side, and the family multipliers lambda (for the
+// sensitivity estimate) come from Q1 lambda = (f - Phi w)_piv.  Rounding differs from the reference's LU;
 // HYBRID re-solves, in the reference's order, the rows the LU FAST kernel would
 // flag (near-coincident nodes, sensitivity estimate) plus any row whose reduced
 // pivots lose definiteness.
@@ -37,7 +37,7 @@ struct NsCfg {
     static constexpr int MP = ns_even(M);
     static constexpr int NR = NF + 1;        // families + probe
     static constexpr int RN = (NN + 31) / 32;
-    static constexpr int RW = 2 * LL * NR;   // per-lane products reduced for w_piv and lambda
+    static constexpr int RW = LL * NR + LL * NF;  // per-lane products reduced for w_piv and lambda
     static constexpr int WARPS = 4;
     // per-warp shared layout (doubles); E hosts Phi, then the LDL^T rows, then the reductions
     static constexpr int E_DBL = ns_even(ns_max(NN * NN, ns_max(M * MP + M * NR, M * RW + RW)));
@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
     double* V = F + Cfg::F_DBL;      // w1p[k][f] at k*NR+f, r_piv at LL*NR + k*NR + f
     double* loc = V + Cfg::V_DBL;
     int* IDX = reinterpret_cast<int*>(loc + Cfg::LOC_DBL);  // pivot nodes, then non-pivot nodes
-    const bool want_flag = a.flag_list != nullptr;
-    const bool want_est = want_flag || a.kappa != nullptr;
+    // HYBRID only (launch_ns): the flag list and the estimate are always wanted
+    constexpr bool want_flag = true, want_est = true;
     const PhsParams& P = a.P;
     const unsigned lt_mask = (1u << lane) - 1u;
     const bool act = lane < M;
@@ -89,12 +89,14 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
     for (int t = lane; t < NN; t += 32) IDX[t] = 0;  // every table entry is a valid node from here on
     __syncwarp();
 
+#pragma unroll 1
     for (int64_t idx = (int64_t)blockIdx.x * Cfg::WARPS + wib; idx < a.m; idx += (int64_t)gridDim.x * Cfg::WARPS) {
         const int64_t row = a.rows[idx];
         const int32_t* sti = a.stencils + idx * NN;
         int stat;
+        bool k3;
         double facs[NF], r2min, rc2max;
-        phs_stage<NN, DD, NF, false>(a, row, sti, lane, E, loc, stat, facs, r2min, rc2max);
+        phs_stage<NN, DD, NF, false>(a, row, sti, lane, E, loc, stat, facs, r2min, rc2max, k3);
 
         // ---- own nodes: Q rows (monomials) and node right-hand sides
         double q[RN][LL];
@@ -107,7 +109,8 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             monomials_reg<DD, DEG, 0, LL>(q[s], loc + ic * DD);
             if (live[s]) {
                 double top[MF_MAX_FAMILIES];
-                phs_rhs_top(loc + ic * DD, DD, P, top);
+                if (k3) phs_rhs_top_k3(loc + ic * DD, DD, P, top);
+                else phs_rhs_top(loc + ic * DD, DD, P, top);
 #pragma unroll
                 for (int f = 0; f < NF; ++f) F[ic * NR + f] = __dmul_rn(top[f], facs[f]);
                 F[ic * NR + NF] = probe_sign(idx, ic);
@@ -132,14 +135,20 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
                     anorm = fmax(anorm, acc);
                 }
             }
+            if (P.scale_code == MF_SCALE_SUPPORT) {
+                // constraint rows sum |Q_im| over the nodes: the constant column gives
+                // exactly n and every other monomial of |x| <= 1 is at most 1
+                anorm = fmax(anorm, (double)NN);
+            } else {
 #pragma unroll
-            for (int m = 0; m < LL; ++m) {
-                double cs = 0.0;
+                for (int m = 0; m < LL; ++m) {
+                    double cs = 0.0;
 #pragma unroll
-                for (int s = 0; s < RN; ++s) cs += fabs(q[s][m]);
+                    for (int s = 0; s < RN; ++s) cs += fabs(q[s][m]);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(FULL, cs, o);
-                anorm = fmax(anorm, cs);
+                    for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(FULL, cs, o);
+                    anorm = fmax(anorm, cs);
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) anorm = fmax(anorm, __shfl_xor_sync(FULL, anorm, o));
@@ -270,28 +279,39 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
         for (int k = 0; k < LL; ++k) {
             const double* Ek = E + pv[k] * NN;
             double y = phq[k];
-            double r[NR];
 #pragma unroll
-            for (int f = 0; f < NR; ++f) r[f] = F[pv[k] * NR + f];
+            for (int k2 = 0; k2 < LL; ++k2) y = fma(-Ek[pv[k2]], wr[k2], y);
+            if (act) Ym[lane * LLP + k] = y;
+        }
+        {
+            // r_piv[k] = f(p_k) - Phi[p_k][piv] w1p, one pivot per lane
+            const int kk = lane < LL ? lane : 0;
+            const int pk = IDX[kk];
+            double rr[NR];
+#pragma unroll
+            for (int f = 0; f < NR; ++f) rr[f] = F[pk * NR + f];
 #pragma unroll
             for (int k2 = 0; k2 < LL; ++k2) {
-                const double ph = Ek[pv[k2]];
-                y = fma(-ph, wr[k2], y);
+                const double ph = E[pk * NN + pv[k2]];
 #pragma unroll
-                for (int f = 0; f < NR; ++f) r[f] = fma(-ph, w1p[k2][f], r[f]);
+                for (int f = 0; f < NR; ++f) rr[f] = fma(-ph, w1p[k2][f], rr[f]);
             }
-            if (act) Ym[lane * LLP + k] = y;
+            if (lane < LL) {
 #pragma unroll
-            for (int f = 0; f < NR; ++f) bb[f] = fma(-wr[k], r[f], bb[f]);  // reduced rhs: r_c - W r_piv
-            if (lane == 0) {
-#pragma unroll
-                for (int f = 0; f < NR; ++f) {
-                    V[k * NR + f] = w1p[k][f];
-                    V[LL * NR + k * NR + f] = r[f];
-                }
+                for (int f = 0; f < NR; ++f) V[LL * NR + lane * NR + f] = rr[f];
             }
         }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < LL; ++k)
+#pragma unroll
+                for (int f = 0; f < NR; ++f) V[k * NR + f] = w1p[k][f];
+        }
         __syncwarp();
+#pragma unroll
+        for (int k = 0; k < LL; ++k)
+#pragma unroll
+            for (int f = 0; f < NR; ++f) bb[f] = fma(-wr[k], V[LL * NR + k * NR + f], bb[f]);  // r_c - W r_piv
 
         // ---- (4) reduced matrix row c: K[c][c'] = Phi[q_c][q_c'] - Phi[q_c][piv] W[c'] - W[c] Y[:, c']
         double K[M];
@@ -326,7 +346,6 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             const double dk = urow[k];
             const double rk = fast_rcp(dk);
             if (k == 0) d0 = dk;
-            definite = definite && dk * d0 > 0.0;
             dinv_own = lane == k ? rk : dinv_own;
             const double fac = lane > k ? K[k] * rk : 0.0;
 #pragma unroll
@@ -346,6 +365,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
         __syncwarp();
 
         // ---- (6) outputs: free weights v (lanes c < M), pivot weights w1p - W^T v
+        definite = __all_sync(FULL, !act || dinv_own * d0 > 0.0);
         bool bad = !ok || !definite;
         double* Red = E;
         if (act) {
@@ -360,7 +380,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
 #pragma unroll
                 for (int f = 0; f < NR; ++f) {
                     Red[lane * RW + k * NR + f] = wr[k] * bb[f];
-                    Red[lane * RW + LL * NR + k * NR + f] = y * bb[f];
+                    if (f < NF) Red[lane * RW + LL * NR + k * NF + f] = y * bb[f];
                 }
             }
         }
@@ -394,33 +414,33 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
         if (__any_sync(FULL, bad) && stat == 0) stat = 1;
 
         if (want_est) {
-            // lambda from Q1 lambda = r_piv - Y v (L1 then U1, uniform)
-            double lam[LL][NR];
+            // lambda (family columns) from Q1 lambda = r_piv - Y v (L1 then U1, uniform)
+            double lam[LL][NF];
 #pragma unroll
             for (int k = 0; k < LL; ++k) {
 #pragma unroll
-                for (int f = 0; f < NR; ++f) lam[k][f] = V[LL * NR + k * NR + f] - sums[LL * NR + k * NR + f];
+                for (int f = 0; f < NF; ++f) lam[k][f] = V[LL * NR + k * NR + f] - sums[LL * NR + k * NF + f];
 #pragma unroll
                 for (int j = 0; j < k; ++j) {
                     const double l = QL[k * LL + j];
 #pragma unroll
-                    for (int f = 0; f < NR; ++f) lam[k][f] = fma(-l, lam[j][f], lam[k][f]);
+                    for (int f = 0; f < NF; ++f) lam[k][f] = fma(-l, lam[j][f], lam[k][f]);
                 }
             }
-            double la[NR];
+            double la[NF];
 #pragma unroll
-            for (int f = 0; f < NR; ++f) la[f] = 0.0;
+            for (int f = 0; f < NF; ++f) la[f] = 0.0;
 #pragma unroll
             for (int k = LL - 1; k >= 0; --k) {
 #pragma unroll
                 for (int j = k + 1; j < LL; ++j) {
                     const double u = QU[k * LL + j];
 #pragma unroll
-                    for (int f = 0; f < NR; ++f) lam[k][f] = fma(-u, lam[j][f], lam[k][f]);
+                    for (int f = 0; f < NF; ++f) lam[k][f] = fma(-u, lam[j][f], lam[k][f]);
                 }
                 const double di = fast_rcp(QU[k * LL + k]);
 #pragma unroll
-                for (int f = 0; f < NR; ++f) {
+                for (int f = 0; f < NF; ++f) {
                     lam[k][f] *= di;
                     la[f] = fmax(la[f], fabs(lam[k][f]));
                 }
@@ -434,18 +454,11 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
 #pragma unroll
                 for (int f = 0; f < NF; ++f) xw[f] = fmax(xw[f], __shfl_xor_sync(FULL, xw[f], o));
             }
-            const double za = fmax(zw, la[NF]);
             double ratio = 0.0;
 #pragma unroll
             for (int f = 0; f < NF; ++f) ratio = fmax(ratio, fmax(xw[f], la[f]) / xw[f]);
             const double est = anorm * zw * ratio;
             const bool close = sep2 < a.min_sep2 * rc2max;
-            if (lane == 0 && a.kappa) {
-                a.kappa[4 * idx + 0] = anorm;
-                a.kappa[4 * idx + 1] = zw;
-                a.kappa[4 * idx + 2] = za;
-                a.kappa[4 * idx + 3] = ratio;
-            }
             if (want_flag && stat == 0 && lane == 0 && (close || !(est <= a.hybrid_thresh))) {
                 unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
                 a.flag_list[slot] = idx;
@@ -472,7 +485,8 @@ template <int NN, int DEG, int DD, int NF>
 int launch_ns(const PhsArgs& a, cudaStream_t st, int sms) {
     using Cfg = NsCfg<NN, DEG, DD, NF>;
     constexpr GradedLex<DD, DEG> g{};
-    if (!a.flag_list || a.P.l != Cfg::LL || a.P.nf != NF) return MF_ERR_UNSUPPORTED;
+    // (per-row kappa diagnostics come from the LU kernel)
+    if (!a.flag_list || a.kappa || a.P.l != Cfg::LL || a.P.nf != NF) return MF_ERR_UNSUPPORTED;
     for (int m = 0; m < Cfg::LL; ++m)
         for (int ax = 0; ax < DD; ++ax)
             if (a.P.expos[m * DD + ax] != g.e[m][ax]) return MF_ERR_UNSUPPORTED;

@@ -116,6 +116,31 @@ __device__ __forceinline__ void phs_rhs_top(const double* loc, int d, const PhsP
     }
 }
 
+// FAST k = 3 (odd) right-hand side: r^3, 3 r, 6 r with FMA-contracted arithmetic
+__device__ __forceinline__ void phs_rhs_top_k3(const double* loc, int d, const PhsParams& P, double* top) {
+    double r2 = loc[0] * loc[0];
+    for (int ax = 1; ax < d; ++ax) r2 = fma(loc[ax], loc[ax], r2);
+    const double r = sqrt(r2);
+    const double val = r2 * r, d1r = 3.0 * r, d2v = 6.0 * r;
+    const double ir2 = r > 0.0 ? 1.0 / r2 : 0.0;
+    for (int f = 0; f < P.nf; ++f) {
+        const int kind = P.kinds[f];
+        double t;
+        if (kind == MF_KIND_IDENTITY) {
+            t = val;
+        } else if (kind == MF_KIND_D1) {
+            t = -d1r * loc[P.ax_a[f]];
+        } else if (kind == MF_KIND_D2) {
+            const double ee = loc[P.ax_a[f]] * loc[P.ax_b[f]] * ir2;
+            const double delta = P.ax_a[f] == P.ax_b[f] ? 1.0 : 0.0;
+            t = fma(d2v, ee, d1r * (delta - ee));
+        } else {
+            t = fma((double)(d - 1), d1r, d2v);
+        }
+        top[f] = t;
+    }
+}
+
 // deterministic +-1 probe vector for the conditioning estimate
 __device__ __forceinline__ double probe_sign(int64_t idx, int r) {
     unsigned long long h = (unsigned long long)idx * 0x9E3779B97F4A7C15ull + (unsigned long long)r * 0xBF58476D1CE4E5B9ull;
