@@ -46,7 +46,7 @@ struct NsCfg {
     static constexpr int W_DBL = M * LLP;
     static constexpr int Y_DBL = M * LLP;
     static constexpr int F_DBL = ns_even(NN * NR);
-    static constexpr int V_DBL = ns_even(2 * LL * NR);
+    static constexpr int V_DBL = ns_even(2 * LL * NR + LL);  // + 1/U1[k][k]
     static constexpr int LOC_DBL = ns_even(NN * DD);
     static constexpr int IDX_DBL = ns_even((NN + 1) / 2);
     static constexpr int WARP_DBL = E_DBL + QU_DBL + QL_DBL + W_DBL + Y_DBL + F_DBL + V_DBL + LOC_DBL + IDX_DBL;
@@ -54,6 +54,14 @@ struct NsCfg {
     static_assert(M >= 1 && M <= 32, "the reduced system must fit one warp");
     static_assert(RN <= 2, "at most 64 stencil nodes");
 };
+
+// D = a x b + D on the fp64 tensor core (m8n8k4, row.col): lane holds A[g][t4],
+// B[t4][g] and D[g][2 t4 .. 2 t4 + 1] with g = lane / 4, t4 = lane % 4
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
 
 template <int DD, int DEG, int MM, int LL>
 __device__ __forceinline__ void monomials_reg(double (&q)[LL], const double* x) {
@@ -78,6 +86,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
     double* Ym = Wm + Cfg::W_DBL;    // Y column c at c*LLP: Y[k][c] = (Phi Z)[p_k][c]
     double* F = Ym + Cfg::Y_DBL;     // node rhs: F[i*NR + f]
     double* V = F + Cfg::F_DBL;      // w1p[k][f] at k*NR+f, r_piv at LL*NR + k*NR + f
+    double* QD = V + 2 * LL * NR;    // 1/U1[k][k]
     double* loc = V + Cfg::V_DBL;
     int* IDX = reinterpret_cast<int*>(loc + Cfg::LOC_DBL);  // pivot nodes, then non-pivot nodes
     // HYBRID only (launch_ns): the flag list and the estimate are always wanted
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
         int stat;
         bool k3;
         double facs[NF], r2min, rc2max;
-        phs_stage<NN, DD, NF, false>(a, row, sti, lane, E, loc, stat, facs, r2min, rc2max, k3);
+        phs_stage<NN, DD, NF, false, true>(a, row, sti, lane, E, loc, stat, facs, r2min, rc2max, k3);
 
         // ---- own nodes: Q rows (monomials) and node right-hand sides
         double q[RN][LL];
@@ -109,8 +118,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             monomials_reg<DD, DEG, 0, LL>(q[s], loc + ic * DD);
             if (live[s]) {
                 double top[MF_MAX_FAMILIES];
-                if (k3) phs_rhs_top_k3(loc + ic * DD, DD, P, top);
-                else phs_rhs_top(loc + ic * DD, DD, P, top);
+                phs_rhs_top_k3(loc + ic * DD, DD, P, top);
 #pragma unroll
                 for (int f = 0; f < NF; ++f) F[ic * NR + f] = __dmul_rn(top[f], facs[f]);
                 F[ic * NR + NF] = probe_sign(idx, ic);
@@ -174,6 +182,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             ok = ok && ball != 0u && mh != 0u;
             const int wl = (__ffs(ball) - 1) & 31;
             const double inv = __shfl_sync(FULL, fast_rcp(cval), wl);
+            QD[k] = inv;  // every lane stores the same value
             const int ps = __shfl_sync(FULL, bslot, wl);
             if (lane == wl) {
 #pragma unroll
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
 #pragma unroll
                 for (int f = 0; f < NR; ++f) w1p[k][f] = fma(-u, w1p[j][f], w1p[k][f]);
             }
-            const double di = fast_rcp(QU[k * LL + k]);
+            const double di = QD[k];
 #pragma unroll
             for (int f = 0; f < NR; ++f) w1p[k][f] *= di;
         }
@@ -275,13 +284,62 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             for (int k = 0; k < LL; ++k) r = fma(-phq[k], w1p[k][f], r);
             bb[f] = r;  // r at the non-pivot node q_c
         }
+        __syncwarp();  // W rows visible
+        // Y = Phi12 - Phi11 W^T (l x m) on the fp64 tensor core; fragments straight
+        // from Phi (through the pivot / free node table) and the W rows
+        {
+            constexpr int LT = (LL + 7) / 8, MT = (M + 7) / 8, KS = (LL + 3) / 4;
+            const int g = lane >> 2, t4 = lane & 3;
+            int pr[LT];
 #pragma unroll
-        for (int k = 0; k < LL; ++k) {
-            const double* Ek = E + pv[k] * NN;
-            double y = phq[k];
+            for (int lt = 0; lt < LT; ++lt) pr[lt] = IDX[min(lt * 8 + g, LL - 1)];
+            double acc[LT][MT][2];
 #pragma unroll
-            for (int k2 = 0; k2 < LL; ++k2) y = fma(-Ek[pv[k2]], wr[k2], y);
-            if (act) Ym[lane * LLP + k] = y;
+            for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = mt * 8 + 2 * t4 + h;
+                    const int qc = IDX[LL + min(c, M - 1)];
+#pragma unroll
+                    for (int lt = 0; lt < LT; ++lt) {
+                        const double v = E[pr[lt] * NN + qc];
+                        acc[lt][mt][h] = (lt * 8 + g < LL && c < M) ? v : 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int k2 = ks * 4 + t4;
+                const bool k2v = k2 < LL;
+                const int pk2 = IDX[min(k2, LL - 1)];
+                double af[LT], bf[MT];
+#pragma unroll
+                for (int lt = 0; lt < LT; ++lt) {
+                    const double v = E[pr[lt] * NN + pk2];
+                    af[lt] = (k2v && lt * 8 + g < LL) ? -v : 0.0;
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int c = mt * 8 + g;
+                    const double v = Wm[min(c, M - 1) * LLP + min(k2, LL - 1)];
+                    bf[mt] = (k2v && c < M) ? v : 0.0;
+                }
+#pragma unroll
+                for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) dmma_f64(acc[lt][mt][0], acc[lt][mt][1], af[lt], bf[mt]);
+            }
+#pragma unroll
+            for (int lt = 0; lt < LT; ++lt) {
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int k = lt * 8 + g, c = mt * 8 + 2 * t4 + h;
+                        if (k < LL && c < M) Ym[c * LLP + k] = acc[lt][mt][h];
+                    }
+                }
+            }
         }
         {
             // r_piv[k] = f(p_k) - Phi[p_k][piv] w1p, one pivot per lane
@@ -313,19 +371,75 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
 #pragma unroll
             for (int f = 0; f < NR; ++f) bb[f] = fma(-wr[k], V[LL * NR + k * NR + f], bb[f]);  // r_c - W r_piv
 
-        // ---- (4) reduced matrix row c: K[c][c'] = Phi[q_c][q_c'] - Phi[q_c][piv] W[c'] - W[c] Y[:, c']
+        // ---- (4) reduced matrix K = Phi22 - [H W] [W^T; Y] (H = Phi21) on the fp64
+        //      tensor core, then one row per lane through shared memory
+        __syncwarp();  // Y columns visible
         double K[M];
+        {
+            constexpr int MT = (M + 7) / 8, KS = (2 * LL + 3) / 4, KP = MP;
+            const int g = lane >> 2, t4 = lane & 3;
+            int qr[MT];
 #pragma unroll
-        for (int c2 = 0; c2 < M; ++c2) {
-            double v = E[qn * NN + IDX[LL + c2]];
-            const double* w2 = Wm + c2 * LLP;
-            const double* y2 = Ym + c2 * LLP;
+            for (int rt = 0; rt < MT; ++rt) qr[rt] = IDX[LL + min(rt * 8 + g, M - 1)];
+            double acc[MT][MT][2];
 #pragma unroll
-            for (int k = 0; k < LL; ++k) {
-                v = fma(-phq[k], w2[k], v);
-                v = fma(-wr[k], y2[k], v);
+            for (int ct = 0; ct < MT; ++ct) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c2 = ct * 8 + 2 * t4 + h;
+                    const int qc = IDX[LL + min(c2, M - 1)];
+#pragma unroll
+                    for (int rt = 0; rt < MT; ++rt) {
+                        const double v = E[qr[rt] * NN + qc];
+                        acc[rt][ct][h] = (rt * 8 + g < M && c2 < M) ? v : 0.0;
+                    }
+                }
             }
-            K[c2] = v;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int kk = ks * 4 + t4;  // < LL: H column kk, else W / Y row kk - LL
+                const bool hp = kk < LL, kv = kk < 2 * LL;
+                const int kh = min(kk, LL - 1), kw = min(max(kk - LL, 0), LL - 1);
+                const int pk = IDX[kh];
+                double af[MT], bf[MT];
+#pragma unroll
+                for (int rt = 0; rt < MT; ++rt) {
+                    const int c = rt * 8 + g;
+                    const double vh = E[qr[rt] * NN + pk];
+                    const double vw = Wm[min(c, M - 1) * LLP + kw];
+                    af[rt] = (c < M && kv) ? -(hp ? vh : vw) : 0.0;
+                }
+#pragma unroll
+                for (int ct = 0; ct < MT; ++ct) {
+                    const int c2 = min(ct * 8 + g, M - 1);
+                    const double vw = Wm[c2 * LLP + kh];
+                    const double vy = Ym[c2 * LLP + kw];
+                    bf[ct] = (ct * 8 + g < M && kv) ? (hp ? vw : vy) : 0.0;
+                }
+#pragma unroll
+                for (int rt = 0; rt < MT; ++rt)
+#pragma unroll
+                    for (int ct = 0; ct < MT; ++ct) dmma_f64(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
+            }
+            __syncwarp();  // every read of Phi is done: K takes its place
+            double* Ks = E;
+#pragma unroll
+            for (int rt = 0; rt < MT; ++rt) {
+#pragma unroll
+                for (int ct = 0; ct < MT; ++ct) {
+                    const int c = rt * 8 + g, c2 = ct * 8 + 2 * t4;
+                    if (c < M && c2 < M) {
+                        if (c2 + 1 < KP) {
+                            *reinterpret_cast<double2*>(Ks + c * KP + c2) = make_double2(acc[rt][ct][0], acc[rt][ct][1]);
+                        } else {
+                            Ks[c * KP + c2] = acc[rt][ct][0];
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < M; ++j) K[j] = Ks[cc * KP + j];
         }
         __syncwarp();  // E (Phi) is dead from here on
 
@@ -438,7 +552,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
 #pragma unroll
                     for (int f = 0; f < NF; ++f) lam[k][f] = fma(-u, lam[j][f], lam[k][f]);
                 }
-                const double di = fast_rcp(QU[k * LL + k]);
+                const double di = QD[k];
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
                     lam[k][f] *= di;
@@ -490,8 +604,9 @@ int launch_ns(const PhsArgs& a, cudaStream_t st, int sms) {
     for (int m = 0; m < Cfg::LL; ++m)
         for (int ax = 0; ax < DD; ++ax)
             if (a.P.expos[m * DD + ax] != g.e[m][ax]) return MF_ERR_UNSUPPORTED;
-    const int order = a.P.even ? a.P.k / 2 + 1 : (a.P.k + 1) / 2;
-    if (a.P.k < 1 || order > DEG + 1) return MF_ERR_UNSUPPORTED;
+    // r^3 (conditionally positive definite of order 2: the reduced matrix is
+    // definite for degree >= 1); other kernels take the LU path
+    if (a.P.k != 3 || a.P.even || DEG < 1) return MF_ERR_UNSUPPORTED;
     auto kern = phs_ns<NN, DEG, DD, NF>;
     MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
     int per_sm = 0;
