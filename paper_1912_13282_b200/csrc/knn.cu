@@ -13,9 +13,9 @@
 //      gathers the points of a cube of cells around the target, whose inner
 //      radius bounds every point left outside;
 //   3. the K smallest keys are found exactly: bisection on d2 shrinks the
-//      candidate set to a window just above K, and the survivors are ranked
-//      by (d2, index) in shared memory; the cube grows until the K-th key is
-//      provably inside it;
+//      candidate set to a window just above K, and every survivor's rank by
+//      (d2, index) is counted against the packed survivor keys in shared
+//      memory; the cube grows until the K-th key is provably inside it;
 //   4. straddle rows are re-run with the sequential-sum metric (K = n);
 //   5. the self-first rule is applied before the row is written.
 #include <cub/device/device_radix_sort.cuh>
@@ -94,49 +94,6 @@ __device__ __forceinline__ bool key_lt2(double d1, int i1, double d2, int i2) {
     return (d1 < d2) | ((d1 == d2) & (i1 < i2));
 }
 
-// Bitonic sort of 32*NS keys (d2, index), NS per lane: element e = lane + 32*s
-// in slot s; ascending.  Exchanges across lanes use shuffles, across slots
-// (distances 32, 64) stay in registers.
-template <int NS>
-__device__ __forceinline__ void bitonic_sort(double (&dk)[NS], int (&ik)[NS], int lane) {
-    constexpr int TOT = 32 * NS;
-#pragma unroll
-    for (int k = 2; k <= TOT; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const int js = j >> 5;
-#pragma unroll
-                for (int sl = 0; sl < NS; ++sl) {
-                    if ((sl & js) == 0) {
-                        const int sp = sl | js;
-                        const bool asc = ((lane + 32 * sl) & k) == 0;
-                        const bool sw = asc ? key_lt2(dk[sp], ik[sp], dk[sl], ik[sl])
-                                            : key_lt2(dk[sl], ik[sl], dk[sp], ik[sp]);
-                        const double td = dk[sl];
-                        const int ti = ik[sl];
-                        dk[sl] = sw ? dk[sp] : dk[sl];
-                        ik[sl] = sw ? ik[sp] : ik[sl];
-                        dk[sp] = sw ? td : dk[sp];
-                        ik[sp] = sw ? ti : ik[sp];
-                    }
-                }
-            } else {
-                const bool lower = (lane & j) == 0;
-#pragma unroll
-                for (int sl = 0; sl < NS; ++sl) {
-                    const double dp = __shfl_xor_sync(FULL, dk[sl], j);
-                    const int ip = __shfl_xor_sync(FULL, ik[sl], j);
-                    const bool asc = ((lane + 32 * sl) & k) == 0;
-                    const bool take = (lower == asc) ? key_lt2(dp, ip, dk[sl], ik[sl]) : key_lt2(dk[sl], ik[sl], dp, ip);
-                    dk[sl] = take ? dp : dk[sl];
-                    ik[sl] = take ? ip : ik[sl];
-                }
-            }
-        }
-    }
-}
-
 struct Box {
     int clo[3], chi[3];
     double limit;  // K-th key must be <= limit to be provably inside
@@ -193,12 +150,20 @@ __device__ __forceinline__ int box_ranges(const Box& b, int d) {
     return R;
 }
 
+constexpr int KNN_CQ = 32 * 32;  // candidate table capacity (32 * the largest MAXIT)
+
+// survivor key, 16 bytes: one shared load per comparison
+struct __align__(16) KnnKey {
+    double d2;
+    unsigned long long ic;  // (node index << 32) | candidate id
+};
+
 struct WarpSmem {
     int32_t roff[KNN_RMAX + 1];  // candidate offset of each range (prefix)
     int32_t rlo[KNN_RMAX];       // first item of each range
-    double sd2[KNN_SCAP];
-    int32_t sid[KNN_SCAP];
-    int32_t scid[KNN_SCAP];
+    int32_t cq[KNN_CQ];          // sorted-pool position of each candidate
+    KnnKey skey[KNN_SCAP];
+    double sd2[KNN_SCAP + 2];    // survivor d2 alone, padded to an even count
     int32_t sel[KNN_SCAP];
     double seld2[KNN_SCAP];
 };
@@ -254,11 +219,12 @@ __device__ double extract_topk(const KnnArgs& a, const Box& b, const double* p, 
     return pd;
 }
 
-template <bool SEQ, int DD, int MAXIT, int NS>
+template <bool SEQ, int DD, int MAXIT>
 __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const int32_t* __restrict__ order,
                                                             int64_t count, const unsigned long long* count_dev,
                                                             int K) {
-    __shared__ WarpSmem smem[KNN_WARPS];
+    extern __shared__ __align__(16) unsigned char knn_smem[];  // KNN_WARPS x WarpSmem
+    WarpSmem* smem = reinterpret_cast<WarpSmem*>(knn_smem);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     WarpSmem& sm = smem[wib];
@@ -266,8 +232,10 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
     constexpr int d = DD;
     const int n = a.n;
     if (count_dev) count = (int64_t)*count_dev;
-    // cube half-width giving ~1.5 K candidates
-    int rho0 = (int)ceil((pow(1.5 * K / KNN_OCC, 1.0 / d) - 1.0) * 0.5);
+    // first cube: half-width ~ the K-th neighbour radius at the grid density
+    // (in cells), so the inner-radius proof usually succeeds on the first pass
+    const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
+    int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
 
     for (int64_t w = (int64_t)blockIdx.x * KNN_WARPS + wib; w < count; w += (int64_t)gridDim.x * KNN_WARPS) {
@@ -298,8 +266,11 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                         if (lane >= o) incl += v;
                     }
                     if (r < R) {
-                        sm.roff[r] = M + incl - len;
+                        const int off = M + incl - len;
+                        sm.roff[r] = off;
                         sm.rlo[r] = lo;
+                        const int lim = min(len, KNN_CQ - off);
+                        for (int t = 0; t < lim; ++t) sm.cq[off + t] = lo + t;
                     }
                     M += __shfl_sync(FULL, incl, 31);
                 }
@@ -320,15 +291,13 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                 // ---- register path: candidates c = it*32 + lane
                 double cd[MAXIT];
                 int ci[MAXIT];
-                int rc = 0;
 #pragma unroll
                 for (int it = 0; it < MAXIT; ++it) {
                     int c = it * 32 + lane;
                     cd[it] = INFINITY;
                     ci[it] = 0x7fffffff;
                     if (it * 32 < M && c < M) {
-                        while (sm.roff[rc + 1] <= c) ++rc;
-                        int q = sm.rlo[rc] + (c - sm.roff[rc]);
+                        const int q = sm.cq[c];
                         cd[it] = metric<SEQ>(a.spos + (size_t)q * d, p, d);
                         ci[it] = a.sidx[q];
                     }
@@ -392,8 +361,8 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                         lo = mid;
                     }
                 }
-                if (chi >= K && chi <= 32 * NS) {
-                    // compact the survivors, then a 32*NS-key bitonic sort in registers
+                if (chi >= K && chi <= KNN_SCAP) {
+                    // compact the survivors (d2 <= hi) as packed keys, in candidate order
                     int base = 0;
 #pragma unroll
                     for (int it = 0; it < MAXIT; ++it) {
@@ -402,62 +371,53 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                             unsigned bal = __ballot_sync(FULL, keep);
                             if (keep) {
                                 int at = base + __popc(bal & ((1u << lane) - 1u));
+                                KnnKey kk;
+                                kk.d2 = cd[it];
+                                kk.ic = ((unsigned long long)(unsigned)ci[it] << 32) | (unsigned)(it * 32 + lane);
+                                sm.skey[at] = kk;
                                 sm.sd2[at] = cd[it];
-                                sm.sid[at] = ci[it];
                             }
                             base += __popc(bal);
                         }
                     }
                     __syncwarp();
-                    double dk[NS];
-                    int ik[NS];
-#pragma unroll
-                    for (int sl = 0; sl < NS; ++sl) {
-                        const int e = lane + 32 * sl;
-                        dk[sl] = e < base ? sm.sd2[e] : INFINITY;
-                        ik[sl] = e < base ? sm.sid[e] : 0x7fffffff;
-                    }
-                    __syncwarp();
-                    bitonic_sort<NS>(dk, ik, lane);
-#pragma unroll
-                    for (int sl = 0; sl < NS; ++sl) {
-                        const int e = lane + 32 * sl;
-                        if (e < K) {
-                            sm.sel[e] = ik[sl];
-                            sm.seld2[e] = dk[sl];
-                        }
-                    }
-                    __syncwarp();
-                    dK = sm.seld2[K - 1];
-                    done = true;
-                }
-                if (!done && chi >= K && chi <= KNN_SCAP) {
-                    // compact survivors (d2 <= hi) into shared memory
-                    int base = 0;
-#pragma unroll
-                    for (int it = 0; it < MAXIT; ++it) {
-                        if (it * 32 < M) {
-                            bool keep = cd[it] <= hi;
-                            unsigned bal = __ballot_sync(FULL, keep);
-                            if (keep) {
-                                int at = base + __popc(bal & ((1u << lane) - 1u));
-                                sm.sd2[at] = cd[it];
-                                sm.sid[at] = ci[it];
-                                sm.scid[at] = it * 32 + lane;
-                            }
-                            base += __popc(bal);
-                        }
-                    }
-                    __syncwarp();
+                    // rank of each survivor = number of survivors with a smaller
+                    // (d2, node index, candidate id).  Count on d2 alone, two keys per
+                    // 16-byte load; a d2 shared with another survivor (rare) re-counts
+                    // that pass on the full key.  Two survivors per lane per pass.
                     const int S = base;
-                    for (int e = lane; e < S; e += 32) {
-                        double de = sm.sd2[e];
-                        int ie = sm.sid[e], ce = sm.scid[e];
-                        int rank = 0;
-                        for (int f = 0; f < S; ++f) rank += key_lt(sm.sd2[f], sm.sid[f], sm.scid[f], de, ie, ce);
-                        if (rank < K) {
-                            sm.sel[rank] = ie;
-                            sm.seld2[rank] = de;
+                    if (lane == 0) sm.sd2[S] = INFINITY;  // pad to an even count
+                    __syncwarp();
+                    for (int e0 = 0; e0 < S; e0 += 64) {
+                        const int ea = e0 + lane, eb = ea + 32;
+                        const KnnKey none{INFINITY, ~0ull};
+                        const KnnKey ka = ea < S ? sm.skey[ea] : none;
+                        const KnnKey kb = eb < S ? sm.skey[eb] : none;
+                        int ra = 0, rb = 0, qa = 0, qb = 0;
+#pragma unroll 4
+                        for (int f = 0; f < S; f += 2) {
+                            const double2 v = *reinterpret_cast<const double2*>(sm.sd2 + f);
+                            ra += (v.x < ka.d2) + (v.y < ka.d2);
+                            qa += (v.x == ka.d2) + (v.y == ka.d2);
+                            rb += (v.x < kb.d2) + (v.y < kb.d2);
+                            qb += (v.x == kb.d2) + (v.y == kb.d2);
+                        }
+                        if (__any_sync(FULL, (ea < S && qa > 1) || (eb < S && qb > 1))) {
+                            ra = 0;
+                            rb = 0;
+                            for (int f = 0; f < S; ++f) {
+                                const KnnKey kf = sm.skey[f];
+                                ra += (kf.d2 < ka.d2) | ((kf.d2 == ka.d2) & (kf.ic < ka.ic));
+                                rb += (kf.d2 < kb.d2) | ((kf.d2 == kb.d2) & (kf.ic < kb.ic));
+                            }
+                        }
+                        if (ea < S && ra < K) {
+                            sm.sel[ra] = (int)(ka.ic >> 32);
+                            sm.seld2[ra] = ka.d2;
+                        }
+                        if (eb < S && rb < K) {
+                            sm.sel[rb] = (int)(kb.ic >> 32);
+                            sm.seld2[rb] = kb.d2;
                         }
                     }
                     __syncwarp();
@@ -721,17 +681,21 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
 
     const int K = (int)(n + 8 < P ? n + 8 : P);
     KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
-    // candidates per warp (32 * MAXIT) and sort width (32 * NS) sized by K
+    // candidates per warp (32 * MAXIT) sized by K
     const bool big = K + KNN_WIN > 64;
-    auto main_k = big ? (d == 1 ? knn_kernel<false, 1, 32, 4> : (d == 2 ? knn_kernel<false, 2, 32, 4> : knn_kernel<false, 3, 32, 4>))
-                      : (d == 1 ? knn_kernel<false, 1, 16, 2> : (d == 2 ? knn_kernel<false, 2, 16, 2> : knn_kernel<false, 3, 16, 2>));
-    auto strd_k = big ? (d == 1 ? knn_kernel<true, 1, 32, 4> : (d == 2 ? knn_kernel<true, 2, 32, 4> : knn_kernel<true, 3, 32, 4>))
-                      : (d == 1 ? knn_kernel<true, 1, 16, 2> : (d == 2 ? knn_kernel<true, 2, 16, 2> : knn_kernel<true, 3, 16, 2>));
-    main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, 0, st>>>(a, order, T, nullptr, K);
+    auto main_k = big ? (d == 1 ? knn_kernel<false, 1, 32> : (d == 2 ? knn_kernel<false, 2, 32> : knn_kernel<false, 3, 32>))
+                      : (d == 1 ? knn_kernel<false, 1, 16> : (d == 2 ? knn_kernel<false, 2, 16> : knn_kernel<false, 3, 16>));
+    auto strd_k = big ? (d == 1 ? knn_kernel<true, 1, 32> : (d == 2 ? knn_kernel<true, 2, 32> : knn_kernel<true, 3, 32>))
+                      : (d == 1 ? knn_kernel<true, 1, 16> : (d == 2 ? knn_kernel<true, 2, 16> : knn_kernel<true, 3, 16>));
+    constexpr int smem_bytes = KNN_WARPS * (int)sizeof(WarpSmem);
+    MF_CUDA_CHECK(cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    MF_CUDA_CHECK(cudaFuncSetAttribute(strd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, smem_bytes, st>>>(a, order, T, nullptr, K);
     MF_LAUNCH_CHECK();
     if (K > n) {
         // straddle rows: top-n by the sequential-sum metric (stencils.py:67-75)
-        strd_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, 0, st>>>(a, L.straddle_list, T, L.straddle_count, n);
+        strd_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.straddle_list, T, L.straddle_count,
+                                                                            n);
         MF_LAUNCH_CHECK();
     }
     if (n_straddle)
