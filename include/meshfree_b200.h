@@ -94,7 +94,9 @@ int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* targets, int6
  * failing row index, or INT64 0x7f7f7f7f7f7f7f7f when every row succeeded.
  * n_replayed (device int64, nullable) counts rows re-solved in REPLAY order
  * (HYBRID mode).  opts (host struct, nullable) sets the HYBRID threshold and
- * an optional per-row conditioning-estimate output. */
+ * an optional per-row conditioning-estimate output.  HYBRID's first pass is
+ * the nullspace solve for r^3 with degree >= 1 on the compiled hot shapes,
+ * else the FAST LU; requesting kappa selects the FAST LU first pass. */
 typedef struct {
     double hybrid_threshold; /* HYBRID re-solve threshold on the sensitivity estimate
                                 ||A||_inf ||(A^-1 z)_w||_inf max_f ||x_f||_inf/||w_f||_inf; <= 0: default */
