@@ -109,6 +109,21 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_ARANGE = {}
+
+
+def device_arange(n: int) -> torch.Tensor:
+    """Cached int64 0..n-1 on the current device (full selections need no H2D copy)."""
+    dev = device()  # raises LibraryError without a CUDA device
+    key = (dev.index, int(n))
+    t = _ARANGE.get(key)
+    if t is None:
+        t = torch.arange(int(n), dtype=torch.int64, device=dev)
+        _ARANGE.clear() if len(_ARANGE) > 8 else None
+        _ARANGE[key] = t
+    return t
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 

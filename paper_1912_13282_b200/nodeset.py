@@ -34,13 +34,24 @@ class _DevicePositions:
 
 
 class _Block:
-    """Stencils of `nodes` (host int64), either a device (T, n) int32 matrix or host rows."""
+    """Stencils of `nodes` (host int64), either a device (T, n) int32 matrix or host rows.
 
-    def __init__(self, nodes, mat=None, rows=None):
-        self.nodes = np.asarray(nodes, dtype=np.int64)
+    ``nodes=None`` with ``full=N`` is the block of every node in index order
+    (the common find_closest_stencils() case): no index array is materialised.
+    """
+
+    def __init__(self, nodes, mat=None, rows=None, full=None):
+        self.full = full
+        self._nodes = None if full is not None else np.asarray(nodes, dtype=np.int64)
         self.mat = mat
         self._rows = rows
         self._host = None
+
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            self._nodes = np.arange(self.full, dtype=np.int64)
+        return self._nodes
 
     @property
     def size(self):
@@ -77,15 +88,16 @@ class NodeSet:
         self.types = np.asarray(types, dtype=np.int64)
         if self.types.shape != (n,):
             raise GeometryError("types must be a length-N vector")
-        if normals is None:
-            normals = np.full((n, d), np.nan)
-        self.normals = np.asarray(normals, dtype=float)
-        if self.normals.shape != (n, d):
-            raise GeometryError("normals must be an (N, d) array")
+        if normals is not None:
+            normals = np.asarray(normals, dtype=float)
+            if normals.shape != (n, d):
+                raise GeometryError("normals must be an (N, d) array")
+        self._normals = normals  # None: all NaN, materialised on first access
         self._pos = _DevicePositions(self.positions)
         self._blocks: list[_Block] = []
         self._blk = np.full(n, -1, dtype=np.int32)
         self._row = np.zeros(n, dtype=np.int64)
+        self._full = -1  # index of a block covering every node in order, else -1
         self._list_cache = None
         if stencils is not None:
             stencils = list(stencils)
@@ -96,31 +108,58 @@ class NodeSet:
                 rows = [np.asarray(stencils[i], dtype=np.int64) for i in have]
                 self._add_block(_Block(np.array(have, dtype=np.int64), rows=rows))
 
+    @property
+    def normals(self) -> np.ndarray:
+        if self._normals is None:
+            self._normals = np.full(self.positions.shape, np.nan)
+        return self._normals
+
+    @normals.setter
+    def normals(self, value):
+        self._normals = value
+
     # -- internal stencil bookkeeping ------------------------------------
 
     def _add_block(self, block: _Block):
         b = len(self._blocks)
         self._blocks.append(block)
-        self._blk[block.nodes] = b
-        self._row[block.nodes] = np.arange(block.nodes.shape[0])
+        if block.full is not None:
+            self._blk = np.full(len(self), b, dtype=np.int32)
+            self._row = np.arange(len(self), dtype=np.int64)
+            self._full = b
+        else:
+            self._blk[block.nodes] = b
+            self._row[block.nodes] = np.arange(block.nodes.shape[0])
+            self._full = -1
         self._list_cache = None
 
-    def _derive(self) -> "NodeSet":
+    def _derive(self, copy_maps: bool = True) -> "NodeSet":
         new = NodeSet.__new__(NodeSet)
         new.positions = self.positions
         new.types = self.types
-        new.normals = self.normals
+        new._normals = self._normals
         new._pos = self._pos
         new._blocks = list(self._blocks)
-        new._blk = self._blk.copy()
-        new._row = self._row.copy()
+        new._blk = self._blk.copy() if copy_maps else self._blk
+        new._row = self._row.copy() if copy_maps else self._row
+        new._full = self._full
         new._list_cache = None
         return new
 
     def _with_device_stencils(self, targets, mat: torch.Tensor) -> "NodeSet":
+        if targets is None:  # every node, in index order: the maps are rebuilt, not copied
+            new = self._derive(copy_maps=False)
+            new._add_block(_Block(None, mat=mat, full=len(self)))
+            return new
         new = self._derive()
         new._add_block(_Block(np.asarray(targets, dtype=np.int64), mat=mat))
         return new
+
+    def full_block_matrix(self):
+        """The (N, n) device stencil matrix when one block covers every node in order, else None."""
+        if self._full < 0:
+            return None
+        return self._blocks[self._full].device_matrix()
 
     def positions_device(self) -> torch.Tensor:
         return self._pos.get()
@@ -130,6 +169,9 @@ class NodeSet:
         idx = np.asarray(idx, dtype=np.int64)
         if idx.size == 0:
             return torch.empty((0, 0), dtype=torch.int32, device=_lib.device())
+        if self._full >= 0 and idx.shape[0] == len(self) and idx[0] == 0 and idx[-1] == len(self) - 1 \
+                and np.array_equal(idx, np.arange(len(self))):
+            return self._blocks[self._full].device_matrix()
         blk = self._blk[idx]
         missing = np.flatnonzero(blk < 0)
         if missing.size:
@@ -259,6 +301,7 @@ class NodeSet:
         n_old = len(self)
         new._blk[:n_old] = self._blk
         new._row[:n_old] = self._row
+        new._full = -1
         return new
 
     def with_stencils(self, indices, stencils):

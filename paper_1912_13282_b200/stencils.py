@@ -42,6 +42,10 @@ def knn_device(nodes: NodeSet, n: int, targets: np.ndarray, pool: np.ndarray):
     return out, nstr
 
 
+def _is_all(which) -> bool:
+    return which is None or (isinstance(which, str) and which == "all")
+
+
 def find_closest_stencils(nodes: NodeSet, n: int, for_which=None, search_among=None) -> NodeSet:
     """Attach n-nearest-neighbour stencils to the selected nodes.
 
@@ -49,15 +53,22 @@ def find_closest_stencils(nodes: NodeSet, n: int, for_which=None, search_among=N
     the pool stencil members are drawn from (selector syntax as in NodeSet).
     Returns a new NodeSet.
     """
-    targets = nodes.select(for_which)
-    pool = nodes.select(search_among)
+    N = len(nodes)
+    all_t, all_p = _is_all(for_which), _is_all(search_among)
+    targets = None if all_t else nodes.select(for_which)
+    pool = None if all_p else nodes.select(search_among)
+    P = N if all_p else pool.shape[0]
+    T = N if all_t else targets.shape[0]
     if n < 1:
         raise StencilError(f"stencil size must be at least 1, got {n}")
-    if n > pool.shape[0]:
+    if n > P:
         raise StencilError(
-            f"stencil size {n} exceeds search pool of {pool.shape[0]} nodes"
+            f"stencil size {n} exceeds search pool of {P} nodes"
         )
-    if targets.shape[0] == 0:
+    if T == 0:
         return nodes
-    mat, _ = knn_device(nodes, int(n), targets, pool)
-    return nodes._with_device_stencils(targets, mat)
+    # full selections go to the device as a cached arange (no host array, no H2D)
+    t_arg = _lib.device_arange(N) if all_t else targets
+    p_arg = _lib.device_arange(N) if all_p else pool
+    mat, _ = knn_device(nodes, int(n), t_arg, p_arg)
+    return nodes._with_device_stencils(None if all_t else targets, mat)

@@ -565,6 +565,21 @@ class WeightStore:
 # compute_weights
 # ---------------------------------------------------------------------------
 
+_HOST_ARANGE = {}
+
+
+def _host_arange(n: int) -> np.ndarray:
+    """Cached read-only int64 0..n-1 (row lists of full node sets)."""
+    a = _HOST_ARANGE.get(n)
+    if a is None:
+        a = np.arange(n, dtype=np.int64)
+        a.flags.writeable = False
+        if len(_HOST_ARANGE) > 8:
+            _HOST_ARANGE.clear()
+        _HOST_ARANGE[n] = a
+    return a
+
+
 def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
     """Evaluate ``engine`` on every selected node for all families (storage.py:258-307).
 
@@ -572,7 +587,11 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
     ``for_which=None`` means every node that has a stencil; nodes selected
     explicitly must all have stencils.
     """
-    if for_which is None:
+    full = nodes.full_block_matrix() if for_which is None else None
+    if full is not None:
+        # every node has a stencil, in index order: no host index bookkeeping
+        rows = _host_arange(len(nodes))
+    elif for_which is None:
         rows = np.flatnonzero(nodes._blk >= 0).astype(np.int64)
         if rows.size == 0:
             raise StencilError("no node has a stencil; run find_closest_stencils first")
@@ -603,12 +622,16 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
         groups = [(engine, fams)]
     for eng, _ in groups:
         _check_batchable(eng)
-    missing = np.flatnonzero(nodes._blk[rows] < 0)
-    if missing.size:
-        raise StencilError(f"node {int(rows[missing[0]])} has no stencil")
-    stencils_d = nodes.stencil_matrix_device(rows)
+    if full is not None:
+        stencils_d = full
+        rows_d = _lib.device_arange(len(nodes))
+    else:
+        missing = np.flatnonzero(nodes._blk[rows] < 0)
+        if missing.size:
+            raise StencilError(f"node {int(rows[missing[0]])} has no stencil")
+        stencils_d = nodes.stencil_matrix_device(rows)
+        rows_d = _lib.to_device(rows, torch.int64)
     n = int(stencils_d.shape[1]) if rows.size else 0
-    rows_d = _lib.to_device(rows, torch.int64)
     values = {}
     for eng, sub in groups:
         values.update(_run_batch(nodes, eng, sub, rows, rows_d, stencils_d, n))
