@@ -76,29 +76,62 @@ def measured_peaks():
         return {}
 
 
+_NVML_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("ready %d" % pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print("%d,%d" % (mhz, rs), flush=True)
+    time.sleep(0.005)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region by a
+    separate NVML process (5 ms; a thread would contend for the GIL with the
+    launching thread), else an nvidia-smi -lms subprocess."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                 "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
+        self.kind = None
+        self.max_mhz = None
+        self.lines = []
 
     def __enter__(self):
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline()
+            if first.startswith("ready"):
+                self.max_mhz = float(first.split()[1])
+                self.kind = "nvml"
+                return self
+            self.proc.kill()
+            self.proc.wait()
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.kind = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -109,22 +142,23 @@ class ClockSampler:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons = [], self.max_mhz, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in getattr(self, "lines", []):
+        for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
-                continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                if self.kind == "nvml" and len(parts) == 2:
+                    sm.append(float(parts[0]))
+                    rs = int(parts[1])
+                    reasons |= {nm for nm, bit in self.NVML_BITS.items() if rs & bit}
+                elif len(parts) >= 6:
+                    sm.append(float(parts[0]))
+                    mx = float(parts[1])
+                    reasons |= {nm for nm, flag in zip(names, parts[2:6]) if flag.lower() == "active"}
             except ValueError:
                 continue
-            for name, flag in zip(names, parts[2:6]):
-                if flag.lower() == "active":
-                    reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.kind}
 
 
 # ---------------------------------------------------------------------------
@@ -334,8 +368,8 @@ def main():
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e = {"value": world * N / float(e2e_t.item()), "unit": UNIT,
-               # positions, field, and the int64 target/pool/row index arrays
-               "h2d_bytes_per_step": int(pts.nbytes + u_host.nbytes + 3 * N * 8),
+               # positions and field (whole-set selections send no index arrays)
+               "h2d_bytes_per_step": int(pts.nbytes + u_host.nbytes),
                "d2h_bytes_per_step": int(y_h.nbytes)}
 
     cpu = None
