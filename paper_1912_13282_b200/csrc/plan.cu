@@ -15,22 +15,23 @@
 
 namespace mf {
 
-__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {  // 21 bits -> every 3rd bit
-    x &= 0x1fffffull;
-    x = (x | (x << 32)) & 0x1f00000000ffffull;
-    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
-    x = (x | (x << 8)) & 0x100f00f00f00f00full;
-    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
-    x = (x | (x << 2)) & 0x1249249249249249ull;
+// 32-bit Morton keys (10 bits per axis in 3D, 16 in 2D, 32 in 1D): a 1024^3
+// lattice is far finer than any node spacing the plan is built for, and the
+// radix sort needs 4 digit passes instead of 8 for 64-bit keys
+__device__ __forceinline__ unsigned spread3(unsigned x) {  // 10 bits -> every 3rd bit
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
     return x;
 }
-__device__ __forceinline__ unsigned long long spread2(unsigned long long x) {  // 32 bits -> every 2nd bit
-    x &= 0xffffffffull;
-    x = (x | (x << 16)) & 0x0000ffff0000ffffull;
-    x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
-    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
-    x = (x | (x << 2)) & 0x3333333333333333ull;
-    x = (x | (x << 1)) & 0x5555555555555555ull;
+__device__ __forceinline__ unsigned spread2(unsigned x) {  // 16 bits -> every 2nd bit
+    x &= 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
     return x;
 }
 
@@ -56,23 +57,23 @@ __global__ void plan_bbox(const double* __restrict__ pos, int64_t N, int d, unsi
 }
 
 __global__ void plan_keys(const double* __restrict__ pos, int64_t N, int d, const unsigned long long* __restrict__ bb,
-                          unsigned long long* __restrict__ key, int32_t* __restrict__ val) {
+                          unsigned* __restrict__ key, int32_t* __restrict__ val) {
     double lo[3], sc[3];
-    const int bits = d == 1 ? 63 : (d == 2 ? 32 : 21);
-    const double span = (double)((1ull << (bits > 62 ? 62 : bits)) - 1);
+    const int bits = d == 1 ? 32 : (d == 2 ? 16 : 10);
+    const double span = (double)((1ull << bits) - 1);
     for (int a = 0; a < d; ++a) {
         lo[a] = from_ordered_bits(bb[a]);
         double ext = from_ordered_bits(bb[3 + a]) - lo[a];
         sc[a] = ext > 0.0 ? span / ext : 0.0;
     }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long q[3] = {0, 0, 0};
+        unsigned q[3] = {0, 0, 0};
         for (int a = 0; a < d; ++a) {
             double t = (pos[i * d + a] - lo[a]) * sc[a];
             t = t > 0.0 ? (t < span ? t : span) : 0.0;
-            q[a] = (unsigned long long)t;
+            q[a] = (unsigned)t;
         }
-        unsigned long long k;
+        unsigned k;
         if (d == 1) k = q[0];
         else if (d == 2) k = spread2(q[0]) | (spread2(q[1]) << 1);
         else k = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
@@ -166,13 +167,13 @@ extern "C" int mf_order_workspace_size(int64_t N, size_t* bytes) {
         return MF_ERR_ARG;
     }
     size_t sort_bytes = 0;
-    cub::DoubleBuffer<unsigned long long> k(nullptr, nullptr);
+    cub::DoubleBuffer<unsigned> k(nullptr, nullptr);
     cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k, v, (int)(N > 0 ? N : 1));
     Arena ar{nullptr, 0, 0, true};
     ar.take<unsigned long long>(6);
-    ar.take<unsigned long long>(N);
-    ar.take<unsigned long long>(N);
+    ar.take<unsigned>(N);
+    ar.take<unsigned>(N);
     ar.take<int32_t>(N);
     ar.take<char>(sort_bytes);
     *bytes = ar.off;
@@ -185,13 +186,13 @@ extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_
     if (N == 0) return MF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     size_t sort_bytes = 0;
-    cub::DoubleBuffer<unsigned long long> probe_k(nullptr, nullptr);
+    cub::DoubleBuffer<unsigned> probe_k(nullptr, nullptr);
     cub::DoubleBuffer<int32_t> probe_v(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, probe_k, probe_v, (int)N);
     Arena ar{(char*)ws, ws_bytes, 0, false};
     unsigned long long* bb = ar.take<unsigned long long>(6);
-    unsigned long long* k0 = ar.take<unsigned long long>(N);
-    unsigned long long* k1 = ar.take<unsigned long long>(N);
+    unsigned* k0 = ar.take<unsigned>(N);
+    unsigned* k1 = ar.take<unsigned>(N);
     int32_t* v0 = ar.take<int32_t>(N);
     char* tmp = ar.take<char>(sort_bytes);
     if (!ws || !ar.ok()) {
@@ -204,9 +205,9 @@ extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_
     MF_LAUNCH_CHECK();
     plan_keys<<<grid_of(N, 256), 256, 0, st>>>(pos, N, d, bb, k0, v0);
     MF_LAUNCH_CHECK();
-    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+    cub::DoubleBuffer<unsigned> kb(k0, k1);
     cub::DoubleBuffer<int32_t> vb(v0, order);
-    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, kb, vb, (int)N, 0, 64, st));
+    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, kb, vb, (int)N, 0, d == 3 ? 30 : 32, st));
     if (vb.Current() != order)
         MF_CUDA_CHECK(cudaMemcpyAsync(order, vb.Current(), sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
     if (inv) {

@@ -64,6 +64,42 @@ __global__ void csr_fill(const int64_t* __restrict__ rows, const int32_t* __rest
     }
 }
 
+// Same ranks, rows staged in shared memory as unique 32-bit keys column*64 + slot
+// (N < 2^25, n <= 64), each row padded to a multiple of 4 with INT_MAX so a
+// 16-byte load serves four comparisons.  A block takes CSR_ROWS rows at a time.
+constexpr int CSR_ROWS = 32;
+
+__global__ void __launch_bounds__(256) csr_fill_smem(const int64_t* __restrict__ rows, const int32_t* __restrict__ st,
+                                                     int64_t m, int n, const int32_t* __restrict__ indptr,
+                                                     int32_t* __restrict__ indices, int32_t* __restrict__ perm) {
+    extern __shared__ __align__(16) int32_t sk[];  // CSR_ROWS x n4 keys
+    const int n4 = (n + 3) & ~3;
+    for (int64_t r0 = (int64_t)blockIdx.x * CSR_ROWS; r0 < m; r0 += (int64_t)gridDim.x * CSR_ROWS) {
+        const int nr = (int)(m - r0 < CSR_ROWS ? m - r0 : CSR_ROWS);
+        const int tot = nr * n;
+        __syncthreads();
+        for (int t = threadIdx.x; t < nr * n4; t += blockDim.x) {
+            const int rr = t / n4, j = t - rr * n4;
+            sk[t] = j < n ? (st[(r0 + rr) * n + j] << 6) | j : 0x7fffffff;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+            const int rr = t / n, j = t - rr * n;
+            const int4* row = reinterpret_cast<const int4*>(sk + rr * n4);
+            const int32_t ke = sk[rr * n4 + j];
+            int rank = 0;
+            for (int q = 0; q < (n4 >> 2); ++q) {
+                const int4 v = row[q];
+                rank += (v.x < ke) + (v.y < ke) + (v.z < ke) + (v.w < ke);
+            }
+            const int64_t r = r0 + rr;
+            const int64_t base = indptr[rows[r]];
+            indices[base + rank] = ke >> 6;
+            perm[base + rank] = (int32_t)(r * n + j);
+        }
+    }
+}
+
 __global__ void csr_gather_k(const int32_t* __restrict__ perm, const double* __restrict__ w, int64_t nnz,
                              double* __restrict__ data) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
@@ -267,7 +303,13 @@ extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_
     MF_LAUNCH_CHECK();
     MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, indptr, (int)(N + 1), st));
     if (m > 0) {
-        csr_fill<<<grid_for(m * (int64_t)n, 256, 16), 256, 0, st>>>(rows, stencils, m, n, indptr, indices, perm);
+        if (N < (1 << 25) && n <= 64) {
+            const int smem = CSR_ROWS * ((n + 3) & ~3) * (int)sizeof(int32_t);
+            csr_fill_smem<<<grid_for((m + CSR_ROWS - 1) / CSR_ROWS, 1, 8), 256, smem, st>>>(rows, stencils, m, n,
+                                                                                         indptr, indices, perm);
+        } else {
+            csr_fill<<<grid_for(m * (int64_t)n, 256, 16), 256, 0, st>>>(rows, stencils, m, n, indptr, indices, perm);
+        }
         MF_LAUNCH_CHECK();
     }
     return MF_OK;

@@ -160,23 +160,32 @@ class _CsrStructure:
                 raise StorageError("stored rows must be distinct node indices")
             self._checked = True
 
+    def _order(self, ordered: bool):
+        """(order, inv) of the Morton renumbering, or (None, None)."""
+        if not ordered:
+            return None, None
+        if getattr(self, "_morton", None) is None:
+            lib = _lib.load()
+            dev = self.indptr.device
+            order = torch.empty(self.N, dtype=torch.int32, device=dev)
+            inv = torch.empty(self.N, dtype=torch.int32, device=dev)
+            size = ctypes.c_size_t(0)
+            _lib.check(lib.mf_order_workspace_size(self.N, ctypes.byref(size)), "mf_order_workspace_size")
+            ws = _lib.workspace(size.value)
+            pos = self.positions_d
+            _lib.check(lib.mf_locality_order(pos.data_ptr(), self.N, int(pos.shape[1]), order.data_ptr(),
+                                             inv.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+                       "mf_locality_order")
+            self._morton = (order, inv)
+        return self._morton
+
     def plan(self, ordered: bool):
         """Apply-plan structure: (order, inv, ell_idx, ell_len); order/inv None when unordered."""
         ordered = ordered and self.positions_d is not None
         if ordered not in self._plans:
             lib = _lib.load()
             dev = self.indptr.device
-            order = inv = None
-            if ordered:
-                order = torch.empty(self.N, dtype=torch.int32, device=dev)
-                inv = torch.empty(self.N, dtype=torch.int32, device=dev)
-                size = ctypes.c_size_t(0)
-                _lib.check(lib.mf_order_workspace_size(self.N, ctypes.byref(size)), "mf_order_workspace_size")
-                ws = _lib.workspace(size.value)
-                pos = self.positions_d
-                _lib.check(lib.mf_locality_order(pos.data_ptr(), self.N, int(pos.shape[1]), order.data_ptr(),
-                                                 inv.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
-                           "mf_locality_order")
+            order, inv = self._order(ordered)
             total = ((self.N + 31) // 32) * 32 * self.n
             ell_idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
             ell_len = torch.empty(max(self.N, 1), dtype=torch.int32, device=dev)
@@ -187,12 +196,25 @@ class _CsrStructure:
         return self._plans[ordered]
 
     def plan_values(self, data, ordered: bool):
-        order, inv, _, _ = self.plan(ordered)
+        """ELL values of `data` in the plan's layout (the first call also builds the
+        structure arrays in the same pass over the CSR)."""
+        ordered = ordered and self.positions_d is not None
         total = ((self.N + 31) // 32) * 32 * self.n
         val = torch.empty(max(total, 1), dtype=torch.float64, device=data.device)
+        fresh = ordered not in self._plans
+        if fresh:
+            order, inv = self._order(ordered)
+            ell_idx = torch.empty(max(total, 1), dtype=torch.int32, device=data.device)
+            ell_len = torch.empty(max(self.N, 1), dtype=torch.int32, device=data.device)
+        else:
+            order, inv, ell_idx, ell_len = self._plans[ordered]
         _lib.check(_lib.load().mf_plan_build(self.indptr.data_ptr(), self.indices.data_ptr(), data.data_ptr(),
-                                             self.N, self.n, _lib.ptr(order), _lib.ptr(inv), None,
-                                             val.data_ptr(), None, _lib.stream_ptr()), "mf_plan_build")
+                                             self.N, self.n, _lib.ptr(order), _lib.ptr(inv),
+                                             ell_idx.data_ptr() if fresh else None, val.data_ptr(),
+                                             ell_len.data_ptr() if fresh else None, _lib.stream_ptr()),
+                   "mf_plan_build")
+        if fresh:
+            self._plans[ordered] = (order, inv, ell_idx, ell_len)
         return val
 
 
@@ -259,8 +281,8 @@ class DeviceCSR:
     def plan(self, ordered: bool = True) -> ApplyPlan:
         """The apply plan of this matrix (built once per ordering)."""
         if ordered not in self._plan:
+            val = self._s.plan_values(self.data_device, ordered)
             order, inv, idx, ln = self._s.plan(ordered)
-            val = self._s.plan_values(self.data_device, order is not None)
             self._plan[ordered] = ApplyPlan(order, inv, idx, val, ln, self._s.N, self._s.n)
         return self._plan[ordered]
 
