@@ -68,6 +68,15 @@ def apply_bytes(N, nnz, r=1):
     return nnz * (8 * r + 4) + N * 8 + r * N * 8 + (N + 1) * 4
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture summary, else None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            return int(json.load(f)[kernel]["bytes"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -415,12 +424,12 @@ def main():
             "apply_gbs": apply_gbs,
             "roofline": {"bound": "fp64", "kernel": "mf_phs_weights (shape solve)",
                          "achieved": phs_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": phs_tflops / fp64_peak, "traffic": None,
+                         "frac": phs_tflops / fp64_peak, "traffic": ncu_traffic("phs_ns"),
                          "note": "F=(2/3)s^3+2rs^2 per stencil (s=45, r=1); peak = DFMA probe measured "
                                  "in this run (MEASURED_PEAKS.json has no fp64 entry)"},
             "apply_roofline": {"bound": "hbm", "kernel": "mf_plan_apply (Morton-ordered ELL-32 + u/y permutes)", "achieved": apply_gbs,
                                "peak": hbm_peak, "unit": "GB/s", "frac": apply_gbs / hbm_peak,
-                               "traffic": None, "bytes_per_launch": b_apply,
+                               "traffic": ncu_traffic("plan_apply_k"), "bytes_per_launch": b_apply,
                                "note": "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"},
             "replayed_stencils": n_replayed,
             "gpu_launches": int(launches),
