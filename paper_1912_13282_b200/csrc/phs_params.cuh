@@ -143,11 +143,11 @@ __device__ __forceinline__ void phs_rhs_top_k3(const double* loc, int d, const P
 
 // deterministic +-1 probe vector for the conditioning estimate
 __device__ __forceinline__ double probe_sign(int64_t idx, int r) {
-    unsigned long long h = (unsigned long long)idx * 0x9E3779B97F4A7C15ull + (unsigned long long)r * 0xBF58476D1CE4E5B9ull;
-    h ^= h >> 31;
-    h *= 0x94D049BB133111EBull;
-    h ^= h >> 29;
-    return (h & 1) ? 1.0 : -1.0;
+    unsigned h = (unsigned)idx * 0x9E3779B1u ^ ((unsigned)r + 0x7F4A7C15u) * 0x85EBCA77u;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return (h & 0x80000000u) ? 1.0 : -1.0;
 }
 
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms);
