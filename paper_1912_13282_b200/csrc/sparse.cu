@@ -246,6 +246,60 @@ __global__ void neumann_k(mf_neumann_t nm, const double* __restrict__ u, double*
     }
 }
 
+// Heat step for rows of at most MAXW entries: a thread issues its row's whole
+// index / value stream, then every u gather, then sums in storage order
+// (bitwise the same as the batched loop above) -- more loads in flight per
+// thread than the unroll-by-5 loop, whose gathers wait on each batch.
+template <int MAXW, int CHUNK>
+__global__ void __launch_bounds__(256) ell_heat_wide_k(const int32_t* __restrict__ ell_len,
+                                                       const int32_t* __restrict__ ell_idx,
+                                                       const double* __restrict__ ell_val, int64_t N, int W,
+                                                       const double* __restrict__ u, double* __restrict__ y,
+                                                       HeatStep hs) {
+    if (step_blew_up(hs.peak_prev)) return;
+    unsigned long long peak = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ((N + 31) & ~31ll); r += stride) {
+        if (r >= N) continue;
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double v = u[r];
+        if (hs.interior[r]) {
+            const int len = ell_len[r];
+            double acc = 0.0;
+#pragma unroll
+            for (int j0 = 0; j0 < MAXW; j0 += CHUNK) {
+                double a[CHUNK], g[CHUNK];
+                int32_t c[CHUNK];
+#pragma unroll
+                for (int j = 0; j < CHUNK; ++j) {
+                    a[j] = j0 + j < len ? __ldcs(ell_val + base + 32 * (j0 + j)) : 0.0;
+                    c[j] = j0 + j < len ? __ldcs(ell_idx + base + 32 * (j0 + j)) : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < CHUNK; ++j) g[j] = j0 + j < len ? __ldg(u + c[j]) : 0.0;
+#pragma unroll
+                for (int j = 0; j < CHUNK; ++j)
+                    if (j0 + j < len) acc = __dadd_rn(acc, __dmul_rn(a[j], g[j]));
+            }
+            double f = hs.source ? hs.source[r] : 0.0;
+            // u + dt * (D * lap_u + f)   (drivers.py:93-96)
+            v = __dadd_rn(v, __dmul_rn(hs.dt, __dadd_rn(__dmul_rn(hs.D, acc), f)));
+        }
+        if (hs.dirichlet[r]) v = hs.g_dir[r];
+        y[r] = v;
+        if (!(hs.peak_skip && hs.peak_skip[r])) {
+            unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+            peak = b > peak ? b : peak;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long ob = __shfl_xor_sync(FULL, peak, o);
+        peak = ob > peak ? ob : peak;
+    }
+    if ((threadIdx.x & 31) == 0 && peak) atomicMax(hs.peak_out, peak);
+}
+
 inline int grid_for(int64_t work, int threads, int per_sm = 16) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -373,7 +427,10 @@ extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, con
         HeatStep hs{interior, dirichlet, g_dir, source, has_nm ? nm->mask : nullptr, dt, diffusivity, cur, prev};
         double* u_old = buf[s & 1];
         double* u_new = buf[(s + 1) & 1];
-        ell_apply_k<true><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
+        if (W <= 16)
+            ell_heat_wide_k<16, 8><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
+        else
+            ell_apply_k<true><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
         MF_LAUNCH_CHECK();
         if (has_nm) {
             neumann_k<<<grid_for(nm->count, 128), 128, 0, st>>>(*nm, u_old, nullptr, u_new, cur, nullptr, prev);
