@@ -383,41 +383,52 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                     __syncwarp();
                     // rank of each survivor = number of survivors with a smaller
                     // (d2, node index, candidate id).  Count on d2 alone, two keys per
-                    // 16-byte load; a d2 shared with another survivor (rare) re-counts
-                    // that pass on the full key.  Two survivors per lane per pass.
+                    // 16-byte load, two survivors per lane per pass; a d2 shared by two
+                    // survivors (rare) shows up as a rank collision and re-counts every
+                    // rank on the full key.
                     const int S = base;
                     if (lane == 0) sm.sd2[S] = INFINITY;  // pad to an even count
                     __syncwarp();
+                    int32_t* slot = sm.cq;              // the candidate table is free by now
+                    int32_t* srank = sm.cq + KNN_SCAP;
                     for (int e0 = 0; e0 < S; e0 += 64) {
                         const int ea = e0 + lane, eb = ea + 32;
-                        const KnnKey none{INFINITY, ~0ull};
-                        const KnnKey ka = ea < S ? sm.skey[ea] : none;
-                        const KnnKey kb = eb < S ? sm.skey[eb] : none;
-                        int ra = 0, rb = 0, qa = 0, qb = 0;
+                        const double da = ea < S ? sm.sd2[ea] : INFINITY;
+                        const double db = eb < S ? sm.sd2[eb] : INFINITY;
+                        int ra = 0, rb = 0;
 #pragma unroll 4
                         for (int f = 0; f < S; f += 2) {
                             const double2 v = *reinterpret_cast<const double2*>(sm.sd2 + f);
-                            ra += (v.x < ka.d2) + (v.y < ka.d2);
-                            qa += (v.x == ka.d2) + (v.y == ka.d2);
-                            rb += (v.x < kb.d2) + (v.y < kb.d2);
-                            qb += (v.x == kb.d2) + (v.y == kb.d2);
+                            ra += (v.x < da) + (v.y < da);
+                            rb += (v.x < db) + (v.y < db);
                         }
-                        if (__any_sync(FULL, (ea < S && qa > 1) || (eb < S && qb > 1))) {
-                            ra = 0;
-                            rb = 0;
+                        if (ea < S) srank[ea] = ra;
+                        if (eb < S) srank[eb] = rb;
+                    }
+                    __syncwarp();
+                    // survivors sharing a d2 get the same count: claim slot[rank], read it back
+                    for (int e = lane; e < S; e += 32) slot[srank[e]] = e;
+                    __syncwarp();
+                    bool clash = false;
+                    for (int e = lane; e < S; e += 32) clash |= slot[srank[e]] != e;
+                    __syncwarp();
+                    if (__any_sync(FULL, clash)) {
+                        for (int e = lane; e < S; e += 32) {
+                            const KnnKey ke = sm.skey[e];
+                            int r = 0;
                             for (int f = 0; f < S; ++f) {
                                 const KnnKey kf = sm.skey[f];
-                                ra += (kf.d2 < ka.d2) | ((kf.d2 == ka.d2) & (kf.ic < ka.ic));
-                                rb += (kf.d2 < kb.d2) | ((kf.d2 == kb.d2) & (kf.ic < kb.ic));
+                                r += (kf.d2 < ke.d2) | ((kf.d2 == ke.d2) & (kf.ic < ke.ic));
                             }
+                            srank[e] = r;
                         }
-                        if (ea < S && ra < K) {
-                            sm.sel[ra] = (int)(ka.ic >> 32);
-                            sm.seld2[ra] = ka.d2;
-                        }
-                        if (eb < S && rb < K) {
-                            sm.sel[rb] = (int)(kb.ic >> 32);
-                            sm.seld2[rb] = kb.d2;
+                        __syncwarp();
+                    }
+                    for (int e = lane; e < S; e += 32) {
+                        const int r = srank[e];
+                        if (r < K) {
+                            sm.sel[r] = (int)(sm.skey[e].ic >> 32);
+                            sm.seld2[r] = sm.skey[e].d2;
                         }
                     }
                     __syncwarp();
