@@ -40,14 +40,20 @@ __device__ __forceinline__ void block_argmax(double v, int pos, double* sv, int*
         sp[w] = pos;
     }
     __syncthreads();
-    best = sv[0];
-    bpos = sp[0];
-    for (int k = 1; k < CTA_WARPS; ++k) {
-        if (sv[k] > best || (sv[k] == best && sp[k] < bpos)) {
-            best = sv[k];
-            bpos = sp[k];
+    // every warp reduces the CTA_WARPS candidates in its first lanes (3 shuffle steps)
+    v = lane < CTA_WARPS ? sv[lane] : -INFINITY;
+    pos = lane < CTA_WARPS ? sp[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = CTA_WARPS / 2; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(FULL, v, o);
+        int op = __shfl_xor_sync(FULL, pos, o);
+        if (ov > v || (ov == v && op < pos)) {
+            v = ov;
+            pos = op;
         }
     }
+    best = __shfl_sync(FULL, v, 0);
+    bpos = __shfl_sync(FULL, pos, 0);
     __syncthreads();
 }
 
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_cta(PhsArgs a, const int64_t*
                 for (int r = col + 1 + w; r < s; r += CTA_WARPS) {
                     double* arow = A + (size_t)r * lda;
                     const double fac = REPLAY ? __dmul_rn(arow[col], inv) : arow[col] * inv;
-                    if (fac != 0.0) {
+                    if (!REPLAY || fac != 0.0) {  // the reference skips zero multipliers
 #pragma unroll
                         for (int q = 0; q < CTA_MAXCOLS / 32; ++q) {
                             const int cc = col + 1 + lane + 32 * q;
@@ -251,10 +257,10 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_cta(PhsArgs a, const int64_t*
                 for (int col = s - 1; col >= 0; --col) {
                     if (tid < nrhs) A[(size_t)col * lda + s + tid] *= __drcp_rn(A[(size_t)col * lda + col]);
                     __syncthreads();
-                    for (int e = tid; e < col * nrhs; e += CTA_THREADS) {
-                        int f = e / col, r = e - f * col;
-                        A[(size_t)r * lda + s + f] =
-                            fma(-A[(size_t)r * lda + col], A[(size_t)col * lda + s + f], A[(size_t)r * lda + s + f]);
+                    for (int r = tid; r < col; r += CTA_THREADS) {
+                        double* arow = A + (size_t)r * lda;
+                        const double u = arow[col];
+                        for (int f = 0; f < nrhs; ++f) arow[s + f] = fma(-u, A[(size_t)col * lda + s + f], arow[s + f]);
                     }
                     __syncthreads();
                 }
