@@ -20,6 +20,7 @@ import torch
 
 from . import _lib
 from .errors import ConfigError, InstabilityError, NumericalError
+from .storage import _to_host
 
 BLOWUP_LIMIT = 1e12
 
@@ -189,7 +190,7 @@ def run_heat_explicit(
         _lib.check(lib.mf_permute(u_d.data_ptr(), plan.order.data_ptr(), n, 1, u_node.data_ptr(),
                                   _lib.stream_ptr()), "mf_permute")
         u_d = u_node
-    return u_d if return_device else u_d.cpu().numpy()
+    return u_d if return_device else _to_host(u_d)
 
 
 def _first_bad(peaks: torch.Tensor):

@@ -95,9 +95,11 @@ class NodeSet:
         self._normals = normals  # None: all NaN, materialised on first access
         self._pos = _DevicePositions(self.positions)
         self._blocks: list[_Block] = []
-        self._blk = np.full(n, -1, dtype=np.int32)
-        self._row = np.zeros(n, dtype=np.int64)
-        self._full = -1  # index of a block covering every node in order, else -1
+        # node -> block / row-in-block maps, materialised on demand (None: derived
+        # from _full, the block covering every node in order, or "no stencil")
+        self._blk_arr = None
+        self._row_arr = None
+        self._full = -1
         self._list_cache = None
         if stencils is not None:
             stencils = list(stencils)
@@ -107,6 +109,19 @@ class NodeSet:
             if have:
                 rows = [np.asarray(stencils[i], dtype=np.int64) for i in have]
                 self._add_block(_Block(np.array(have, dtype=np.int64), rows=rows))
+
+    @property
+    def _blk(self) -> np.ndarray:
+        if self._blk_arr is None:
+            self._blk_arr = np.full(len(self), self._full, dtype=np.int32)
+        return self._blk_arr
+
+    @property
+    def _row(self) -> np.ndarray:
+        if self._row_arr is None:
+            self._row_arr = (np.arange(len(self), dtype=np.int64) if self._full >= 0
+                             else np.zeros(len(self), dtype=np.int64))
+        return self._row_arr
 
     @property
     def normals(self) -> np.ndarray:
@@ -124,12 +139,13 @@ class NodeSet:
         b = len(self._blocks)
         self._blocks.append(block)
         if block.full is not None:
-            self._blk = np.full(len(self), b, dtype=np.int32)
-            self._row = np.arange(len(self), dtype=np.int64)
+            self._blk_arr = None  # implied: every node -> block b, row = node
+            self._row_arr = None
             self._full = b
         else:
-            self._blk[block.nodes] = b
-            self._row[block.nodes] = np.arange(block.nodes.shape[0])
+            blk, row = self._blk, self._row  # materialise before the maps change meaning
+            blk[block.nodes] = b
+            row[block.nodes] = np.arange(block.nodes.shape[0])
             self._full = -1
         self._list_cache = None
 
@@ -140,8 +156,8 @@ class NodeSet:
         new._normals = self._normals
         new._pos = self._pos
         new._blocks = list(self._blocks)
-        new._blk = self._blk.copy() if copy_maps else self._blk
-        new._row = self._row.copy() if copy_maps else self._row
+        new._blk_arr = self._blk_arr.copy() if (copy_maps and self._blk_arr is not None) else None
+        new._row_arr = self._row_arr.copy() if (copy_maps and self._row_arr is not None) else None
         new._full = self._full
         new._list_cache = None
         return new
@@ -299,9 +315,9 @@ class NodeSet:
         new._pos = _DevicePositions(new.positions)
         new._blocks = list(self._blocks)
         n_old = len(self)
-        new._blk[:n_old] = self._blk
-        new._row[:n_old] = self._row
-        new._full = -1
+        blk, row = new._blk, new._row  # fresh maps (new._full is -1)
+        blk[:n_old] = self._blk
+        row[:n_old] = self._row
         return new
 
     def with_stencils(self, indices, stencils):

@@ -118,6 +118,13 @@ def expand_families(families, dim: int):
 # device CSR
 # ---------------------------------------------------------------------------
 
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy array backed by pinned memory (fast D2H; torch caches pinned blocks)."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 def _to_field(field, N):
     """Field argument -> (device f64 tensor, was_numpy)."""
     if isinstance(field, torch.Tensor) and field.is_cuda:
@@ -316,7 +323,7 @@ class DeviceCSR:
         y = self.apply_device(u_d)
         if host:
             self._s.check()
-            return y.cpu().numpy()
+            return _to_host(y)
         return y
 
     def to_scipy(self):
