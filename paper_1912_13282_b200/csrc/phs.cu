@@ -415,6 +415,7 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
         a.flag_count = flag_count;
     }
     rc = launch_phs_fast(a, st, sm_count());
+    if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_ns_cta(a, st, sm_count());
     if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_cta(a, false, nullptr, nullptr, m, st, sm_count());
     if (rc == MF_ERR_UNSUPPORTED) rc = launch_generic<false>(a, nullptr, nullptr, m, st);
     if (rc != MF_OK) return rc;

@@ -11,6 +11,7 @@
 // as the warp kernels do.
 #include "common.cuh"
 #include "phs_params.cuh"
+#include "phs_reg.cuh"  // fast_rcp, fast_rsqrt
 
 namespace mf {
 
@@ -346,6 +347,368 @@ int launch_cta_t(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     phs_cta<REPLAY><<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a, list, list_count);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Nullspace solve for large stencils (HYBRID first pass, r^3, degree >= 1):
+// the CTA counterpart of phs_ns.cuh.  Gauss-Jordan column elimination with
+// partial pivoting over the nodes runs on the stacked matrix [Q; g^T; I]
+// ((n + nrhs + l) x l): after l steps the pivot-node rows of Q are unit
+// vectors, the other node rows hold W = Q2 Q1^-1, the g rows hold the
+// particular solutions w1p = Q1^-T g, and the identity rows hold Q1^-1 (for
+// lambda).  The reduced system K v = Z^T (f - Phi w_p) (K = Z^T Phi Z,
+// (n-l)^2, definite) is solved by pivot-free Gauss-Jordan on [K | b].  Every
+// phase is a parallel sweep over a shared-memory array between barriers.
+// ---------------------------------------------------------------------------
+struct NsCtaLayout {
+    int n, d, l, nrhs, M, RG, GP, KP;
+    size_t loc, E, G, F, Y, K, prow, colk, red, ints, total;
+};
+
+__host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nrhs) {
+    NsCtaLayout L;
+    L.n = n;
+    L.d = d;
+    L.l = l;
+    L.nrhs = nrhs;
+    L.M = n - l;
+    L.RG = n + nrhs + l;
+    L.GP = l | 1;  // odd pitch: column sweeps hit distinct banks
+    L.KP = (L.M + nrhs) | 1;
+    size_t o = 0;
+    auto take = [&](size_t c) { size_t at = o; o += (c + 1) & ~(size_t)1; return at; };
+    L.loc = take((size_t)n * d);
+    L.E = take((size_t)n * n);
+    L.G = take((size_t)L.RG * L.GP);
+    L.F = take((size_t)n * nrhs);
+    L.Y = take((size_t)l * L.M);
+    L.K = take((size_t)L.M * L.KP);
+    L.prow = take((size_t)(l > L.KP ? l : L.KP));
+    const int lnf = l * (nrhs - 1);  // lambda right-hand sides
+    L.colk = take((size_t)(L.RG > lnf ? L.RG : lnf));  // RG >= M
+    L.red = take(4 * CTA_WARPS + 8);
+    L.ints = take(((size_t)2 * n + l + L.M + 1) / 2 + 1);  // isp[n], piv[l], nonpiv[M]
+    L.total = o;
+    return L;
+}
+
+__global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
+    extern __shared__ __align__(16) double smem_n[];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const PhsParams& P = a.P;
+    const int n = a.n, d = P.d, l = P.l, nf = P.nf, nrhs = nf + 1;
+    const NsCtaLayout L = ns_cta_layout(n, d, l, nrhs);
+    const int M = L.M, RG = L.RG, GP = L.GP, KP = L.KP;
+    double* loc = smem_n + L.loc;
+    double* E = smem_n + L.E;
+    double* G = smem_n + L.G;
+    double* F = smem_n + L.F;
+    double* Y = smem_n + L.Y;
+    double* K = smem_n + L.K;
+    double* prow = smem_n + L.prow;
+    double* colk = smem_n + L.colk;
+    double* red = smem_n + L.red;
+    int* redi = reinterpret_cast<int*>(red + 2 * CTA_WARPS);
+    int* isp = reinterpret_cast<int*>(smem_n + L.ints);
+    int* piv = isp + n;
+    int* nonpiv = piv + l;
+
+    for (int64_t idx = blockIdx.x; idx < a.m; idx += gridDim.x) {
+        const int64_t row = a.rows[idx];
+        const int32_t* sti = a.stencils + idx * n;
+        // ---- local coordinates, scale (max r^2, one root), family factors
+        for (int e = tid; e < n * d; e += CTA_THREADS) {
+            const int j = e / d, ax = e - j * d;
+            loc[e] = a.pos[(int64_t)sti[j] * d + ax] - a.pos[row * d + ax];
+        }
+        __syncthreads();
+        int stat = 0;
+        double sc = 1.0;
+        if (P.scale_code != MF_SCALE_NONE) {
+            const bool nearest = P.scale_code == MF_SCALE_NEAREST;
+            double best = nearest ? INFINITY : -1.0;
+            for (int j = tid; j < n; j += CTA_THREADS) {
+                double r2 = 0.0;
+                for (int ax = 0; ax < d; ++ax) r2 = __dadd_rn(r2, __dmul_rn(loc[j * d + ax], loc[j * d + ax]));
+                if (nearest) {
+                    if (r2 > 0.0 && r2 < best) best = r2;
+                } else if (r2 > best) {
+                    best = r2;
+                }
+            }
+            best = nearest ? block_reduce_min(best, red) : block_reduce_max(best, red);
+            if (nearest ? (best == INFINITY) : !(best > 0.0)) stat = 2;
+            else sc = __dsqrt_rn(best);
+        }
+        double facs[MF_MAX_FAMILIES];
+        for (int f = 0; f < nf; ++f) facs[f] = pow_cr_int(sc, -P.orders[f]);
+        const double rs = fast_rcp(sc);
+        for (int e = tid; e < n * d; e += CTA_THREADS) loc[e] *= rs;
+        if (tid < n) isp[tid] = 0;
+        __syncthreads();
+
+        // ---- Phi (zero diagonal), [Q; g; I], node right-hand sides
+        double r2min = INFINITY, rc2max = 0.0;
+        for (int e = tid; e < n * n; e += CTA_THREADS) {
+            const int i = e / n, j = e - i * n;
+            if (j < i) continue;
+            double v = 0.0;
+            if (j > i) {
+                double df = loc[i * d] - loc[j * d];
+                double r2 = df * df;
+                for (int ax = 1; ax < d; ++ax) {
+                    df = loc[i * d + ax] - loc[j * d + ax];
+                    r2 = fma(df, df, r2);
+                }
+                r2min = r2 < r2min ? r2 : r2min;
+                v = r2 * (r2 * fast_rsqrt(fmax(r2, 1e-300)));
+            }
+            E[i * n + j] = v;
+            E[j * n + i] = v;
+        }
+        for (int e = tid; e < n * l; e += CTA_THREADS) {
+            const int i = e / l, m = e - i * l;
+            G[i * GP + m] = phs_monomial(loc + i * d, P.expos + m * d, d);
+        }
+        for (int e = tid; e < nrhs * l; e += CTA_THREADS) {
+            const int f = e / l, m = e - f * l;
+            G[(n + f) * GP + m] = f < nf ? __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + m], facs[f]) : probe_sign(idx, n + m);
+        }
+        for (int e = tid; e < l * l; e += CTA_THREADS) {
+            const int i = e / l, m = e - i * l;
+            G[(n + nrhs + i) * GP + m] = i == m ? 1.0 : 0.0;
+        }
+        for (int i = tid; i < n; i += CTA_THREADS) {
+            double top[MF_MAX_FAMILIES];
+            phs_rhs_top_k3(loc + i * d, d, P, top);
+            for (int f = 0; f < nf; ++f) F[i * nrhs + f] = __dmul_rn(top[f], facs[f]);
+            F[i * nrhs + nf] = probe_sign(idx, i);
+            double rc2 = 0.0;
+            for (int ax = 0; ax < d; ++ax) rc2 = fma(loc[i * d + ax], loc[i * d + ax], rc2);
+            rc2max = fmax(rc2max, rc2);
+        }
+        __syncthreads();
+        r2min = block_reduce_min(r2min, red);
+        rc2max = block_reduce_max(rc2max, red);
+        // ||A||_inf of the saddle-point matrix (estimate only)
+        double anorm = 0.0;
+        for (int r = tid; r < n + l; r += CTA_THREADS) {
+            double acc = 0.0;
+            if (r < n) {
+                for (int j = 0; j < n; ++j) acc += E[r * n + j];  // r^3 >= 0
+                for (int m = 0; m < l; ++m) acc += fabs(G[r * GP + m]);
+            } else {
+                for (int i = 0; i < n; ++i) acc += fabs(G[i * GP + (r - n)]);
+            }
+            anorm = fmax(anorm, acc);
+        }
+        anorm = block_reduce_max(anorm, red);
+
+        // ---- Gauss-Jordan column elimination of [Q; g; I] with node pivoting
+        bool ok = stat == 0;
+        for (int k = 0; k < l && ok; ++k) {
+            double best = -1.0;
+            int pr = 0x7fffffff;
+            for (int r = tid; r < n; r += CTA_THREADS) {
+                const double v = isp[r] ? -1.0 : fabs(G[r * GP + k]);
+                if (v > best) {
+                    best = v;
+                    pr = r;
+                }
+            }
+            block_argmax(best, pr, red, redi, best, pr);
+            if (!(best > 0.0) || !isfinite(best) || pr == 0x7fffffff) {
+                ok = false;
+                break;
+            }
+            {
+                const double inv = fast_rcp(G[pr * GP + k]);
+                for (int j = tid; j < l; j += CTA_THREADS) prow[j] = G[pr * GP + j];
+                for (int r = tid; r < RG; r += CTA_THREADS) colk[r] = G[r * GP + k] * inv;  // scaled column k
+                if (tid == 0) {
+                    isp[pr] = 1;
+                    piv[k] = pr;
+                }
+            }
+            __syncthreads();
+            {
+                // each thread owns one column jj and strides over the rows
+                const int jj = tid % l, r0 = tid / l, rstep = CTA_THREADS / l;
+                if (r0 < rstep) {
+                    const double pj = prow[jj];
+                    for (int r = r0; r < RG; r += rstep) {
+                        const double c = colk[r];
+                        double v = jj == k ? c : fma(-pj, c, G[r * GP + jj]);
+                        if (r == pr) v = jj == k ? 1.0 : 0.0;
+                        G[r * GP + jj] = v;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // free (non-pivot) nodes in node order
+        if (w == 0) {
+            int base = 0;
+            for (int c0 = 0; c0 < n; c0 += 32) {
+                const int i = c0 + lane;
+                const bool fr = i < n && !isp[i];
+                const unsigned bal = __ballot_sync(FULL, fr);
+                const int at = base + __popc(bal & ((1u << lane) - 1u));
+                if (fr && at < M) nonpiv[at] = i;
+                base += __popc(bal);
+            }
+            if (lane == 0) redi[CTA_WARPS] = base;
+        }
+        __syncthreads();
+        ok = ok && redi[CTA_WARPS] == M;
+
+        bool definite = true;
+        if (ok) {
+            // ---- r = f - Phi[:, piv] w1p (in place in F);  Y = Phi12 - Phi11 W^T
+            for (int e = tid; e < n * nrhs; e += CTA_THREADS) {
+                const int i = e / nrhs, f = e - i * nrhs;
+                double r = F[e];
+                for (int k = 0; k < l; ++k) r = fma(-E[i * n + piv[k]], G[(n + f) * GP + k], r);
+                F[e] = r;
+            }
+            for (int e = tid; e < l * M; e += CTA_THREADS) {
+                const int k = e / M, c = e - k * M;
+                const int pk = piv[k], qc = nonpiv[c];
+                double y = E[pk * n + qc];
+                for (int k2 = 0; k2 < l; ++k2) y = fma(-E[pk * n + piv[k2]], G[qc * GP + k2], y);
+                Y[k * M + c] = y;
+            }
+            __syncthreads();
+            // ---- [K | b]: K = Phi22 - H W^T - W Y,  b = r_free - W r_piv
+            for (int e = tid; e < M * M; e += CTA_THREADS) {
+                const int c = e / M, c2 = e - c * M;
+                const int qc = nonpiv[c], qc2 = nonpiv[c2];
+                double v = E[qc * n + qc2];
+                for (int k = 0; k < l; ++k) {
+                    v = fma(-E[qc * n + piv[k]], G[qc2 * GP + k], v);
+                    v = fma(-G[qc * GP + k], Y[k * M + c2], v);
+                }
+                K[c * KP + c2] = v;
+            }
+            for (int e = tid; e < M * nrhs; e += CTA_THREADS) {
+                const int c = e / nrhs, f = e - c * nrhs;
+                const int qc = nonpiv[c];
+                double b = F[qc * nrhs + f];
+                for (int k = 0; k < l; ++k) b = fma(-G[qc * GP + k], F[piv[k] * nrhs + f], b);
+                K[c * KP + M + f] = b;
+            }
+            __syncthreads();
+            // ---- pivot-free Gauss-Jordan on [K | b] (K definite)
+            const double d0 = K[0];
+            for (int k = 0; k < M; ++k) {
+                const double dk = K[k * KP + k];
+                definite = definite && dk * d0 > 0.0;
+                const double inv = fast_rcp(dk);
+                for (int j = tid; j < M + nrhs; j += CTA_THREADS) prow[j] = K[k * KP + j];
+                for (int r = tid; r < M; r += CTA_THREADS) colk[r] = K[r * KP + k] * inv;
+                __syncthreads();
+                {
+                    const int wk = M + nrhs - k - 1;  // columns right of the pivot
+                    const int jj = k + 1 + tid % wk, r0 = tid / wk, rstep = CTA_THREADS / wk;
+                    if (r0 < rstep) {
+                        const double pj = prow[jj];
+                        for (int r = r0; r < M; r += rstep)
+                            K[r * KP + jj] = r == k ? pj * inv : fma(-pj, colk[r], K[r * KP + jj]);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        ok = ok && definite;
+
+        // ---- outputs: free weights v, pivot weights w1p - W^T v; estimate
+        bool bad = !ok;
+        double zw = 0.0, xw[MF_MAX_FAMILIES], la[MF_MAX_FAMILIES];
+        for (int f = 0; f < nf; ++f) xw[f] = la[f] = 0.0;
+        if (ok) {
+            for (int e = tid; e < M * nrhs; e += CTA_THREADS) {
+                const int c = e / nrhs, f = e - c * nrhs;
+                const double v = K[c * KP + M + f];
+                if (f < nf) {
+                    bad |= !isfinite(v);
+                    a.out[((size_t)idx * nf + f) * n + nonpiv[c]] = v;
+                    xw[f] = fmax(xw[f], fabs(v));
+                } else {
+                    zw = fmax(zw, fabs(v));
+                }
+            }
+            for (int e = tid; e < l * nrhs; e += CTA_THREADS) {
+                const int k = e / nrhs, f = e - k * nrhs;
+                double wv = G[(n + f) * GP + k];
+                for (int c = 0; c < M; ++c) wv = fma(-G[nonpiv[c] * GP + k], K[c * KP + M + f], wv);
+                if (f < nf) {
+                    bad |= !isfinite(wv);
+                    a.out[((size_t)idx * nf + f) * n + piv[k]] = wv;
+                    xw[f] = fmax(xw[f], fabs(wv));
+                } else {
+                    zw = fmax(zw, fabs(wv));
+                }
+            }
+            // lambda_f = Q1^-1 (r_piv - Y v)   (family columns)
+            for (int e = tid; e < l * nf; e += CTA_THREADS) {
+                const int k = e / nf, f = e - k * nf;
+                double sv = F[piv[k] * nrhs + f];
+                for (int c = 0; c < M; ++c) sv = fma(-Y[k * M + c], K[c * KP + M + f], sv);
+                colk[k * nf + f] = sv;
+            }
+            __syncthreads();
+            for (int e = tid; e < l * nf; e += CTA_THREADS) {
+                const int m = e / nf, f = e - m * nf;
+                double lam = 0.0;
+                for (int k = 0; k < l; ++k) lam = fma(G[(n + nrhs + m) * GP + k], colk[k * nf + f], lam);
+                la[f] = fmax(la[f], fabs(lam));
+            }
+        }
+        bad = __syncthreads_or(bad) != 0;
+        if (bad && stat == 0) stat = 1;
+        zw = block_reduce_max(zw, red);
+        double ratio = 0.0;
+        for (int f = 0; f < nf; ++f) {
+            const double xwf = block_reduce_max(xw[f], red);
+            const double laf = block_reduce_max(la[f], red);
+            ratio = fmax(ratio, fmax(xwf, laf) / xwf);
+        }
+        if (tid == 0) {
+            const double est = anorm * zw * ratio;
+            const bool close = r2min < a.min_sep2 * rc2max;
+            if (stat != 0 || close || !(est <= a.hybrid_thresh)) {
+                const unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+                a.flag_list[slot] = idx;
+            }
+            a.status[idx] = 0;  // failures are re-derived in reference order by the re-solve
+        }
+        __syncthreads();
+    }
+}
+
+int launch_phs_ns_cta(const PhsArgs& a, cudaStream_t st, int sms) {
+    const int n = a.n, l = a.P.l, nf = a.P.nf;
+    // HYBRID only (rows that fail or lose definiteness are re-solved); r^3 with
+    // degree >= 1 (constant and linear monomials present: l >= d + 1)
+    if (!a.flag_list || a.kappa || a.P.k != 3 || a.P.even || l < a.P.d + 1 || n - l < 1) return MF_ERR_UNSUPPORTED;
+    const NsCtaLayout L = ns_cta_layout(n, a.P.d, l, nf + 1);
+    const size_t bytes = L.total * sizeof(double);
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (bytes > (size_t)max_smem) return MF_ERR_UNSUPPORTED;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(phs_ns_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int per_sm = 0;
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phs_ns_cta, CTA_THREADS, bytes));
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = a.m;
+    const int64_t cap = (int64_t)sms * per_sm * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    phs_ns_cta<<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a);
     MF_LAUNCH_CHECK();
     return MF_OK;
 }

@@ -151,6 +151,7 @@ __device__ __forceinline__ double probe_sign(int64_t idx, int r) {
 }
 
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms);
+int launch_phs_ns_cta(const PhsArgs& a, cudaStream_t st, int sms);
 int launch_phs_cta(const PhsArgs& a, bool replay, const int64_t* list, const int64_t* list_count,
                    int64_t max_count, cudaStream_t st, int sms);
 int launch_phs_replay_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
