@@ -10,11 +10,11 @@
 //   3. the reduced matrix K = Z^T Phi Z (Z = [-W^T; I], (n-l)^2) is symmetric
 //      and definite for a polyharmonic kernel whose order the polynomial degree
 //      covers (conditional positive definiteness), so it is factored by a
-//      pivot-free LDL^T: at step k every lane stores its column-k entry once
-//      and reads the pivot row back as 16-byte broadcasts;
+//      pivot-free Gauss-Jordan elimination: at step k every lane stores its
+//      column-k entry once and reads the pivot row back as 16-byte broadcasts;
 //   4. v solves K v = Z^T (f - Phi w_p), and w = w_p + Z v.
-// One warp per stencil; lane c owns reduced row c (n - l <= 32), so the
-// back-substitution runs on registers and shuffles.  The +-1 probe rides along
+// One warp per stencil; lane c owns reduced row c (n - l <= 32) in registers
+// and ends with its own unknown, v_c = b_c / d_c (no back-substitution).  The +-1 probe rides along
 // as one more right-hand side, and the family multipliers lambda (for the
 // sensitivity estimate) come from Q1 lambda = (f - Phi w)_piv.  Rounding differs from the reference's LU;
 // HYBRID re-solves, in the reference's order, the rows the LU FAST kernel would
@@ -39,7 +39,7 @@ struct NsCfg {
     static constexpr int RN = (NN + 31) / 32;
     static constexpr int RW = LL * NR + LL * NF;  // per-lane products reduced for w_piv and lambda
     static constexpr int WARPS = 4;
-    // per-warp shared layout (doubles); E hosts Phi, then the LDL^T rows, then the reductions
+    // per-warp shared layout (doubles); E hosts Phi, then the elimination rows, then the reductions
     static constexpr int E_DBL = ns_even(ns_max(NN * NN, ns_max(M * MP + M * NR, M * RW + RW)));
     static constexpr int QU_DBL = ns_even(LL * LL);
     static constexpr int QL_DBL = ns_even(LL * LL);
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
         }
         __syncwarp();  // E (Phi) is dead from here on
 
-        // ---- (5) pivot-free LDL^T; lane c keeps U row c (K[j], j >= c) in registers
+        // ---- (5) pivot-free Gauss-Jordan on [K | b]; lane c keeps row c in registers
         double* Us = E;
         double* Bs = E + M * MP;
         double dinv_own = 0.0, d0 = 0.0;
@@ -461,21 +461,16 @@ __global__ void __launch_bounds__(128, 3) phs_ns(PhsArgs a) {
             const double rk = fast_rcp(dk);
             if (k == 0) d0 = dk;
             dinv_own = lane == k ? rk : dinv_own;
-            const double fac = lane > k ? K[k] * rk : 0.0;
+            // Gauss-Jordan: rows above the pivot are eliminated too (those lanes issue
+            // the FMAs anyway), so no back-substitution follows
+            const double fac = lane != k ? K[k] * rk : 0.0;
 #pragma unroll
             for (int j = k + 1; j < M; ++j) K[j] = fma(-fac, urow[j], K[j]);
 #pragma unroll
             for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * NR + f], bb[f]);
         }
-        // back-substitution on registers: v_col = bb_col / U[col][col], broadcast, eliminate
 #pragma unroll
-        for (int col = M - 1; col >= 0; --col) {
-#pragma unroll
-            for (int f = 0; f < NR; ++f) {
-                const double xs = __shfl_sync(FULL, bb[f] * dinv_own, col);
-                bb[f] = lane == col ? xs : (lane < col ? fma(-K[col], xs, bb[f]) : bb[f]);
-            }
-        }
+        for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;  // v_c = b_c / d_c
         __syncwarp();
 
         // ---- (6) outputs: free weights v (lanes c < M), pivot weights w1p - W^T v
