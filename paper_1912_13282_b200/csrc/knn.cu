@@ -29,7 +29,7 @@ constexpr double KNN_OCC = 2.0;   // mean pool points per grid cell
 constexpr int KNN_WARPS = 4;      // warps per block
 constexpr int KNN_SCAP = 256;     // survivor capacity per warp (shared memory)
 constexpr int KNN_RMAX = 255;     // cell-row ranges per cube held in shared memory
-constexpr int KNN_WIN = 16;       // bisection stops at <= K + WIN survivors
+constexpr int KNN_WIN = 16;       // kernel-variant choice: K + WIN > 64 takes 32 candidate rounds
 
 struct GridParams {
     double lo[3], cw[3], inv[3];
@@ -237,6 +237,10 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
     const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
     int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
+    // bisection stops at <= K + win survivors: as wide as keeps the rank pass
+    // within one 64-survivor round (fewer bisection counts), 8..24; windows that
+    // need several rounds anyway keep 16
+    const int win = 64 - K >= 8 ? min(24, 64 - K) : 16;
 
     for (int64_t w = (int64_t)blockIdx.x * KNN_WARPS + wib; w < count; w += (int64_t)gridDim.x * KNN_WARPS) {
         const int trow = order[w];
@@ -326,11 +330,11 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                 }
                 // first guess from the local density of the cube: K' = K + WIN/2 points
                 // lie within r with M/vol * c_d r^d = K'
-                if (chi > K + KNN_WIN) {
+                if (chi > K + win) {
                     double vol = 1.0;
                     for (int ax = 0; ax < d; ++ax) vol *= (double)(b.chi[ax] - b.clo[ax] + 1) * g.cw[ax];
                     const double cdim = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
-                    const double want = (double)K + 0.5 * KNN_WIN;
+                    const double want = (double)K + 0.5 * win;
                     double rg = pow(want * vol / ((double)M * cdim), 1.0 / d);
                     double tg = rg * rg;
                     if (tg > 0.0 && tg < hi) {
@@ -343,13 +347,13 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
                         }
                     }
                 }
-                for (int iter = 0; iter < 80 && chi > K + KNN_WIN; ++iter) {
+                for (int iter = 0; iter < 80 && chi > K + win; ++iter) {
                     // interpolate in r^d (count ~ r^d), fall back to bisection
                     double mid;
                     if (lo >= 0.0) {
                         mid = lo + 0.5 * (hi - lo);
                     } else {
-                        const double scale = pow(((double)K + 0.5 * KNN_WIN) / (double)chi, 2.0 / d);
+                        const double scale = pow(((double)K + 0.5 * win) / (double)chi, 2.0 / d);
                         mid = hi * fmin(fmax(scale, 0.25), 0.95);
                     }
                     if (!(mid < hi) || (lo >= 0.0 && !(mid > lo))) break;
