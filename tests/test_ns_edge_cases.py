@@ -12,15 +12,18 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def _cloud(seed=3):
+def _cloud(seed=3, near_offset=2e-4, patch=1):
+    """Uniform cube plus three isolated patches (each larger than the stencil, so
+    stencils stay inside their patch); `patch` scales the patch point counts."""
     rng = np.random.default_rng(seed)
     base = rng.uniform(0, 1, (6000, 3))
     # an isolated coplanar patch: every stencil inside it has z = const, so the
     # z-monomials are linearly dependent on the others (singular system)
-    plane = np.column_stack([rng.uniform(5, 5.3, 60), rng.uniform(5, 5.3, 60), np.full(60, 5.0)])
+    npl = 60 * patch
+    plane = np.column_stack([rng.uniform(5, 5.3, npl), rng.uniform(5, 5.3, npl), np.full(npl, 5.0)])
     # an isolated patch with exact duplicate points (identical PHS rows)
-    dup_src = rng.uniform(8, 8.3, (40, 3))
-    dup = np.concatenate([dup_src, dup_src[:10]])
+    dup_src = rng.uniform(8, 8.3, (40 * patch, 3))
+    dup = np.concatenate([dup_src, dup_src[:10 * patch]])
     # nearly coincident pairs inside an isolated patch (min-separation criterion):
     # ~5e-4 of the stencil radius (the closest pairs of the full C4 cloud are
     # 2.6e-4), where an FMA solve drifts past the parity bar but the
@@ -28,8 +31,8 @@ def _cloud(seed=3):
     # reference's own weights round-off dominated (cond ~ separation^-2): there
     # the rare one-ulp differences between glibc pow and the correctly rounded
     # r^3 of the re-solve show up in the weights; see DESIGN.md.
-    near_src = rng.uniform(11, 11.3, (50, 3))
-    near = np.concatenate([near_src, near_src[:15] + 2e-4 * rng.standard_normal((15, 3))])
+    near_src = rng.uniform(11, 11.3, (50 * patch, 3))
+    near = np.concatenate([near_src, near_src[:15 * patch] + near_offset * rng.standard_normal((15 * patch, 3))])
     return np.concatenate([base, plane, dup, near])
 
 
@@ -75,3 +78,32 @@ def test_compute_weights_raises_the_reference_error_on_a_singular_stencil():
         mf.compute_weights(nodes, eng, ["laplacian"])
     assert exc.value.node == first
     assert "singular local collocation system" in str(exc.value)
+
+
+def test_cta_nullspace_path_on_degenerate_stencils():
+    """Large stencils (n = 70, degree 4, 4 families: the CTA nullspace pass) on the
+    degenerate cloud with patches larger than the stencil: statuses exact,
+    successful rows within 1e-9."""
+    import torch
+
+    import paper_1912_13282_b200 as mf
+    from paper_1912_13282_b200.storage import expand_families, phs_weights_device
+
+    pts = _cloud(seed=5, near_offset=2e-3, patch=2)
+    N = pts.shape[0]
+    fams_spec = ["laplacian", "gradient"]
+    st, _ = oracle.knn(pts, 70)
+    ref, fail, _ = oracle.phs_weights(pts, np.arange(N), st, fams_spec, degree=4)
+    assert fail.sum() > 0
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=4, scale="support", solver="lu", mode="hybrid")
+    out, status, first_fail, n_rep = phs_weights_device(
+        torch.from_numpy(pts).cuda(), torch.arange(N, dtype=torch.int64, device="cuda"),
+        torch.from_numpy(st.astype(np.int32)).cuda(), eng, expand_families(fams_spec, 3), 3)
+    status = status.cpu().numpy()
+    got = out.cpu().numpy()
+    assert np.array_equal(status != 0, fail != 0)
+    assert int(first_fail.item()) == int(np.flatnonzero(fail)[0])
+    ok = fail == 0
+    for f in range(got.shape[1]):
+        err = np.max(np.abs(got[ok, f] - ref[ok, f]), axis=1) / np.max(np.abs(ref[ok, f]), axis=1)
+        assert err.max() <= 1e-9, (f, err.max())
