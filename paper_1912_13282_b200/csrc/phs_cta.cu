@@ -355,17 +355,16 @@ int launch_cta_t(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
 // ---------------------------------------------------------------------------
 // Nullspace solve for large stencils (HYBRID first pass, r^3, degree >= 1):
 // the CTA counterpart of phs_ns.cuh.  Gauss-Jordan column elimination with
-// partial pivoting over the nodes runs on the stacked matrix [Q; g^T; I]
-// ((n + nrhs + l) x l): after l steps the pivot-node rows of Q are unit
-// vectors, the other node rows hold W = Q2 Q1^-1, the g rows hold the
-// particular solutions w1p = Q1^-T g, and the identity rows hold Q1^-1 (for
-// lambda).  The reduced system K v = Z^T (f - Phi w_p) (K = Z^T Phi Z,
+// partial pivoting over the nodes runs on the stacked matrix [Q; g^T]
+// ((n + nrhs) x l): after l steps the
+// free node rows hold W = Q2 Q1^-1 and the g rows the particular solutions
+// w1p = Q1^-T g; the recorded column operations give Q1^-1 s for lambda.  The reduced system K v = Z^T (f - Phi w_p) (K = Z^T Phi Z,
 // (n-l)^2, definite) is solved by pivot-free Gauss-Jordan on [K | b].  Every
 // phase is a parallel sweep over a shared-memory array between barriers.
 // ---------------------------------------------------------------------------
 struct NsCtaLayout {
     int n, d, l, nrhs, M, RG, GP, KP;
-    size_t loc, E, G, F, Y, K, prow, colk, red, ints, total;
+    size_t loc, E, G, ops, F, Y, K, prow, colk, red, ints, total;
 };
 
 __host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nrhs) {
@@ -375,7 +374,7 @@ __host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nr
     L.l = l;
     L.nrhs = nrhs;
     L.M = n - l;
-    L.RG = n + nrhs + l;
+    L.RG = n + nrhs;  // node rows, then one row per right-hand side
     L.GP = l | 1;  // odd pitch: column sweeps hit distinct banks
     L.KP = (L.M + nrhs) | 1;
     size_t o = 0;
@@ -383,6 +382,7 @@ __host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nr
     L.loc = take((size_t)n * d);
     L.E = take((size_t)n * n);
     L.G = take((size_t)L.RG * L.GP);
+    L.ops = take((size_t)l * L.GP + l);  // per step: pivot-row snapshot, then 1 / pivot
     L.F = take((size_t)n * nrhs);
     L.Y = take((size_t)l * L.M);
     L.K = take((size_t)L.M * L.KP);
@@ -390,7 +390,7 @@ __host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nr
     const int lnf = l * (nrhs - 1);  // lambda right-hand sides
     L.colk = take((size_t)(L.RG > lnf ? L.RG : lnf));  // RG >= M
     L.red = take(4 * CTA_WARPS + 8);
-    L.ints = take(((size_t)2 * n + l + L.M + 1) / 2 + 1);  // isp[n], piv[l], nonpiv[M]
+    L.ints = take(((size_t)n + l + L.M + 1) / 2 + 1);  // isp[n], piv[l], nonpiv[M]
     L.total = o;
     return L;
 }
@@ -412,6 +412,8 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
     double* colk = smem_n + L.colk;
     double* red = smem_n + L.red;
     int* redi = reinterpret_cast<int*>(red + 2 * CTA_WARPS);
+    double* ops = smem_n + L.ops;
+    double* invs = ops + (size_t)l * GP;
     int* isp = reinterpret_cast<int*>(smem_n + L.ints);
     int* piv = isp + n;
     int* nonpiv = piv + l;
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
         for (int f = 0; f < nf; ++f) facs[f] = pow_cr_int(sc, -P.orders[f]);
         const double rs = fast_rcp(sc);
         for (int e = tid; e < n * d; e += CTA_THREADS) loc[e] *= rs;
-        if (tid < n) isp[tid] = 0;
+        for (int i = tid; i < n; i += CTA_THREADS) isp[i] = 0;
         __syncthreads();
 
         // ---- Phi (zero diagonal), [Q; g; I], node right-hand sides
@@ -476,10 +478,6 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
         for (int e = tid; e < nrhs * l; e += CTA_THREADS) {
             const int f = e / l, m = e - f * l;
             G[(n + f) * GP + m] = f < nf ? __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + m], facs[f]) : probe_sign(idx, n + m);
-        }
-        for (int e = tid; e < l * l; e += CTA_THREADS) {
-            const int i = e / l, m = e - i * l;
-            G[(n + nrhs + i) * GP + m] = i == m ? 1.0 : 0.0;
         }
         for (int i = tid; i < n; i += CTA_THREADS) {
             double top[MF_MAX_FAMILIES];
@@ -526,24 +524,28 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
             }
             {
                 const double inv = fast_rcp(G[pr * GP + k]);
-                for (int j = tid; j < l; j += CTA_THREADS) prow[j] = G[pr * GP + j];
+                for (int j = tid; j < l; j += CTA_THREADS) {
+                    const double v = G[pr * GP + j];
+                    prow[j] = v;
+                    ops[k * GP + j] = v;  // kept for lambda (the column operations, replayed backwards)
+                }
                 for (int r = tid; r < RG; r += CTA_THREADS) colk[r] = G[r * GP + k] * inv;  // scaled column k
                 if (tid == 0) {
                     isp[pr] = 1;
                     piv[k] = pr;
+                    invs[k] = inv;
                 }
             }
             __syncthreads();
             {
-                // each thread owns one column jj and strides over the rows
+                // each thread owns one column jj and strides over the rows (pivot rows
+                // keep being swept harmlessly: they are never read again)
                 const int jj = tid % l, r0 = tid / l, rstep = CTA_THREADS / l;
                 if (r0 < rstep) {
                     const double pj = prow[jj];
                     for (int r = r0; r < RG; r += rstep) {
-                        const double c = colk[r];
-                        double v = jj == k ? c : fma(-pj, c, G[r * GP + jj]);
-                        if (r == pr) v = jj == k ? 1.0 : 0.0;
-                        G[r * GP + jj] = v;
+                        const double cr = colk[r];
+                        G[r * GP + jj] = jj == k ? cr : fma(-pj, cr, G[r * GP + jj]);
                     }
                 }
             }
@@ -652,7 +654,8 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
                     zw = fmax(zw, fabs(wv));
                 }
             }
-            // lambda_f = Q1^-1 (r_piv - Y v)   (family columns)
+            // lambda_f = Q1^-1 (r_piv - Y v)   (family columns): Q1^-1 is the product
+            // of the sweep's column operations, applied to s last step first
             for (int e = tid; e < l * nf; e += CTA_THREADS) {
                 const int k = e / nf, f = e - k * nf;
                 double sv = F[piv[k] * nrhs + f];
@@ -660,11 +663,21 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
                 colk[k * nf + f] = sv;
             }
             __syncthreads();
-            for (int e = tid; e < l * nf; e += CTA_THREADS) {
-                const int m = e / nf, f = e - m * nf;
-                double lam = 0.0;
-                for (int k = 0; k < l; ++k) lam = fma(G[(n + nrhs + m) * GP + k], colk[k * nf + f], lam);
-                la[f] = fmax(la[f], fabs(lam));
+            for (int f = w; f < nf; f += CTA_WARPS) {
+                for (int k = l - 1; k >= 0; --k) {
+                    double part = 0.0;
+                    for (int j = lane; j < l; j += 32)
+                        if (j != k) part = fma(ops[k * GP + j], colk[j * nf + f], part);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+                    if (lane == 0) colk[k * nf + f] = invs[k] * (colk[k * nf + f] - part);
+                    __syncwarp();
+                }
+                double mx = 0.0;
+                for (int j = lane; j < l; j += 32) mx = fmax(mx, fabs(colk[j * nf + f]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+                la[f] = mx;
             }
         }
         bad = __syncthreads_or(bad) != 0;
