@@ -1,0 +1,730 @@
+// Nullspace shape solve, pivots-first layout: the HYBRID first pass for the hot
+// stencil shapes (sm_100a).  Same mathematics as phs_ns.cuh (nullspace of Q^T,
+// pivot-free Gauss-Jordan on the reduced definite system); the work is ordered
+// so that every phase has instruction-level parallelism and regular shared
+// memory addressing:
+//
+//   0. the next stencil's node positions are staged with cp.async while the
+//      current one is solved (the index -> position gather is two dependent
+//      global loads; issuing them one stencil ahead takes them off the chain);
+//   1. local coordinates, scale (warp max by two REDUX on the IEEE bits),
+//      monomials and node right-hand sides in registers, one node per lane
+//      (nodes 32.. ride in a second slot of lanes 0..);
+//   2. LU with partial pivoting of Q over the lane-resident nodes (one REDUX
+//      per step picks value and lane at once; nodes 32.. are never pivots, so
+//      the pivot search is one compare per lane);
+//   3. the PHS block Phi is evaluated AFTER the pivots are known, directly in
+//      the order [pivot nodes; free nodes], so the blocks Phi11, Phi12, Phi22
+//      are contiguous and the tensor-core fragments for Y = Phi12 - Phi11 W^T
+//      and K = Phi22 - [H W][W^T; Y] are plain strided loads;
+//   4. every triangular solve (W, the particular solution, lambda) runs in
+//      right-looking order, whose dependency chain is one FMA per level;
+//   5. W^T v and Y v (pivot weights and the estimate's multipliers) are one
+//      small tensor-core product instead of a shared-memory reduction.
+//
+// Rounding differs from the reference's LU exactly as phs_ns.cuh does; the
+// HYBRID flags (near-coincident nodes, sensitivity estimate, failed or
+// indefinite reduction, non-finite weights) are the same.
+#pragma once
+
+#include "phs_ns.cuh"
+
+namespace mf {
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// warp max of a non-negative double (or +0 for lanes that do not take part):
+// the IEEE bit pattern of non-negative doubles is ordered like the values
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_max_sync(FULL, hi);
+    const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+// warp min of a non-negative double (+inf for lanes that do not take part)
+__device__ __forceinline__ double warp_min_nonneg(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_min_sync(FULL, hi);
+    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+
+// smallest pitch >= x that is 4 mod 8 doubles: the tensor-core fragment loads
+// (8 rows g x 4 columns t, or 4 rows x 8 columns) then hit 16 distinct 8-byte
+// bank pairs per half warp
+__host__ __device__ constexpr int ns_pitch(int x) { return x % 8 <= 4 ? x + (4 - x % 8) : x + (12 - x % 8); }
+
+template <int NN, int DEG, int DD, int NF>
+struct Ns2Cfg {
+    static constexpr int LL = binom(DEG + DD, DD);
+    static constexpr int M = NN - LL;           // reduced system size
+    static constexpr int MP = ns_even(M);       // elimination row pitch
+    static constexpr int NR = NF + 1;           // families + probe
+    static constexpr int RN = (NN + 31) / 32;   // node slots per lane
+    static constexpr int XN = NN - 32 > 0 ? NN - 32 : 0;  // nodes in slot 1
+    static constexpr int NP = ns_even(NN);      // pitch of the coordinate arrays
+    static constexpr int P = ns_pitch(NN + 1);  // Phi row pitch
+    static constexpr int LP = ns_pitch(LL);     // W / Y row pitch
+    static constexpr int WARPS = 4;
+    // per-warp shared layout (doubles)
+    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * MP + M * NR));
+    static constexpr int XS_DBL = ns_even(DD * NP + DD);  // scaled coords (permuted), then the staged raw positions
+    static constexpr int QLU_DBL = ns_even(LL * LL + LL); // L1 (strict lower), U1 (upper), 1/U1[k][k]
+    static constexpr int W_DBL = M * LP;
+    static constexpr int Y_DBL = M * LP;
+    static constexpr int F_DBL = ns_even(NN * NR + NN);   // node rhs (permuted) + |Q| row sums
+    static constexpr int V_DBL = ns_even(3 * LL * NR + M * NR);  // w1p, r_piv, lambda rhs, v
+    static constexpr int IDX_DBL = ns_even((NN + 1) / 2);
+    static constexpr int WARP_DBL = PH_DBL + XS_DBL + QLU_DBL + W_DBL + Y_DBL + F_DBL + V_DBL + IDX_DBL;
+    static constexpr size_t SMEM = (size_t)WARPS * WARP_DBL * sizeof(double);
+    static_assert(M >= 1 && M <= 32, "the reduced system must fit one warp");
+    static_assert(RN <= 2 && LL <= 32 && NR <= 8, "shape outside the kernel's layout");
+    static_assert(NN % 2 == 1, "pair enumeration assumes an odd stencil size");
+};
+
+template <int NN, int DEG, int DD, int NF>
+__global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
+    using Cfg = Ns2Cfg<NN, DEG, DD, NF>;
+    constexpr int LL = Cfg::LL, M = Cfg::M, MP = Cfg::MP, NR = Cfg::NR, RN = Cfg::RN, XN = Cfg::XN,
+                  NP = Cfg::NP, P = Cfg::P, LP = Cfg::LP;
+    extern __shared__ __align__(16) double smem_n2[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    double* PH = smem_n2 + (size_t)wib * Cfg::WARP_DBL;  // Phi (permuted), then K / elimination rows
+    double* XS = PH + Cfg::PH_DBL;     // scaled coords SoA [ax*NP + t]; staged raw positions (next stencil)
+    double* QLU = XS + Cfg::XS_DBL;    // row k: L1[k][0..k-1], U1[k][k..]; QLU[LL*LL + k] = 1/U1[k][k]
+    double* Wm = QLU + Cfg::QLU_DBL;   // L2 rows, then W rows (reduced index c at c*LP)
+    double* Ym = Wm + Cfg::W_DBL;      // Y column c at c*LP
+    double* FS = Ym + Cfg::Y_DBL;      // node rhs FS[t*NR + f] (permuted t); |Q| row sums at NN*NR + t
+    double* VS = FS + Cfg::F_DBL;      // w1p[k*NR+f], r_piv at LL*NR, lambda rhs at 2*LL*NR, v at 3*LL*NR
+    int* IDX = reinterpret_cast<int*>(VS + Cfg::V_DBL);  // permuted index -> stencil node
+    const PhsParams& P_ = a.P;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int g8 = lane >> 2, t4 = lane & 3;  // tensor-core fragment coordinates
+
+    const int64_t stride = (int64_t)gridDim.x * Cfg::WARPS;
+    int64_t idx = (int64_t)blockIdx.x * Cfg::WARPS + wib;
+
+    // node indices of the stencil staged next (loaded one stencil ahead of the
+    // staging, so the cp.async addresses never wait on a global load)
+    int64_t srow = 0;
+    int ssti[RN] = {};
+    auto load_idx = [&](int64_t id) {
+        if (id < a.m) {
+            srow = a.rows[id];
+#pragma unroll
+            for (int s = 0; s < RN; ++s) {
+                const int j = lane + 32 * s;
+                ssti[s] = j < NN ? a.stencils[id * NN + j] : 0;
+            }
+        }
+    };
+    // stage the raw positions of stencil `id` (nodes SoA, then the centre)
+    auto stage = [&](int64_t id) {
+        if (id < a.m) {
+#pragma unroll
+            for (int s = 0; s < RN; ++s) {
+                const int j = lane + 32 * s;
+                if (j < NN) {
+#pragma unroll
+                    for (int ax = 0; ax < DD; ++ax) cp_async8(XS + ax * NP + j, a.pos + (int64_t)ssti[s] * DD + ax);
+                }
+            }
+            if (lane < DD) cp_async8(XS + DD * NP + lane, a.pos + srow * DD + lane);
+        }
+        cp_async_commit();
+    };
+    load_idx(idx);
+    stage(idx);
+    load_idx(idx + stride);
+
+#pragma unroll 1
+    for (; idx < a.m; idx += stride) {
+        cp_async_wait_all();
+        __syncwarp();
+
+        // ---- (1) local coordinates, scale, monomials, node right-hand sides
+        double x[RN][DD], r2[RN];
+#pragma unroll
+        for (int s = 0; s < RN; ++s) {
+            const int j = lane + 32 * s;
+            const bool in = j < NN;
+#pragma unroll
+            for (int ax = 0; ax < DD; ++ax) x[s][ax] = in ? XS[ax * NP + j] - XS[DD * NP + ax] : 0.0;
+            r2[s] = x[s][0] * x[s][0];
+#pragma unroll
+            for (int ax = 1; ax < DD; ++ax) r2[s] = fma(x[s][ax], x[s][ax], r2[s]);
+        }
+        __syncwarp();  // staged positions consumed: XS is free for the scaled coordinates
+        int stat = 0;
+        double rs = 1.0, r2max;
+        {
+            double mx = r2[0];
+            if (RN > 1) mx = fmax(mx, r2[RN - 1]);
+            r2max = warp_max_nonneg(mx);
+            const int sc_code = P_.scale_code;
+            if (sc_code == MF_SCALE_SUPPORT) {
+                if (r2max > 0.0) rs = fast_rsqrt(r2max);
+                else stat = 2;
+            } else if (sc_code == MF_SCALE_NEAREST) {
+                double mn = INFINITY;
+#pragma unroll
+                for (int s = 0; s < RN; ++s)
+                    if (r2[s] > 0.0) mn = fmin(mn, r2[s]);
+                mn = warp_min_nonneg(mn);
+                if (mn < INFINITY) rs = fast_rsqrt(mn);
+                else stat = 2;
+            }
+        }
+        const double rc2max = r2max * rs * rs;
+        double facs[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const int o = P_.orders[f];
+            facs[f] = o == 0 ? 1.0 : (o == 1 ? rs : rs * rs);
+        }
+        double q[RN][LL], fr[RN][NF], qsum[RN];
+#pragma unroll
+        for (int s = 0; s < RN; ++s) {
+#pragma unroll
+            for (int ax = 0; ax < DD; ++ax) x[s][ax] *= rs;
+            monomials_reg<DD, DEG, 0, LL>(q[s], x[s]);
+            qsum[s] = 0.0;
+#pragma unroll
+            for (int m = 0; m < LL; ++m) qsum[s] += fabs(q[s][m]);
+            // FAST k = 3 right-hand side (phs_rhs_top_k3 with reciprocal roots)
+            double rr2 = x[s][0] * x[s][0];
+#pragma unroll
+            for (int ax = 1; ax < DD; ++ax) rr2 = fma(x[s][ax], x[s][ax], rr2);
+            const double rsq = rr2 > 0.0 ? fast_rsqrt(rr2) : 0.0;
+            const double r = rr2 * rsq, ir2 = rsq * rsq;
+            const double d1r = 3.0 * r, d2v = 6.0 * r;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int kind = P_.kinds[f];
+                double t;
+                if (kind == MF_KIND_IDENTITY) {
+                    t = rr2 * r;
+                } else if (kind == MF_KIND_D1) {
+                    t = -d1r * x[s][P_.ax_a[f]];
+                } else if (kind == MF_KIND_D2) {
+                    const double ee = x[s][P_.ax_a[f]] * x[s][P_.ax_b[f]] * ir2;
+                    const double delta = P_.ax_a[f] == P_.ax_b[f] ? 1.0 : 0.0;
+                    t = fma(d2v, ee, d1r * (delta - ee));
+                } else {
+                    t = fma((double)(DD - 1), d1r, d2v);
+                }
+                fr[s][f] = t * facs[f];
+            }
+        }
+
+        // ---- (2) LU with partial pivoting of Q over the lane-resident nodes
+        bool ok = stat == 0;
+        bool live = lane < NN;  // slot 0 is a pivot candidate until it wins
+        int myk = 0;
+#pragma unroll
+        for (int k = 0; k < LL; ++k) {
+            unsigned key = 0u;
+            if (live) {
+                const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(fabs(q[0][k])) >> 32);
+                key = (hi & ~31u) | (unsigned)(31 - lane);
+            }
+            const unsigned mk = __reduce_max_sync(FULL, key);
+            const int wl = 31 - (int)(mk & 31u);
+            ok = ok && (mk >> 5) != 0u;
+            if (lane == wl && live) {
+#pragma unroll
+                for (int m = 0; m < LL; ++m) QLU[k * LL + m] = q[0][m];
+                live = false;
+                myk = k;
+            }
+            __syncwarp();
+            const double inv = fast_rcp(QLU[k * LL + k]);
+            if (lane == 0) QLU[LL * LL + k] = inv;
+#pragma unroll
+            for (int s = 0; s < RN; ++s) {
+                const bool upd = s == 0 ? live : lane < XN;
+                const double l = upd ? q[s][k] * inv : 0.0;
+                q[s][k] = l;
+#pragma unroll
+                for (int m = k + 1; m < LL; ++m) q[s][m] = fma(-l, QLU[k * LL + m], q[s][m]);
+            }
+        }
+        // free nodes: live slot-0 lanes in lane order, then the slot-1 nodes
+        const unsigned fb = __ballot_sync(FULL, live);
+        const int nfl = __popc(fb);
+        ok = ok && nfl + XN == M;
+        const int c0 = live ? LL + __popc(fb & lt_mask) : myk;  // permuted index of node `lane`
+        if (lane < NN) {
+            IDX[c0] = lane;
+#pragma unroll
+            for (int ax = 0; ax < DD; ++ax) XS[ax * NP + c0] = x[0][ax];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) FS[c0 * NR + f] = fr[0][f];
+            FS[c0 * NR + NF] = probe_sign(idx, lane);
+            FS[NN * NR + c0] = qsum[0];
+            if (live) {
+#pragma unroll
+                for (int m = 0; m < LL; ++m) Wm[(c0 - LL) * LP + m] = q[0][m];
+            }
+        }
+        if (RN > 1 && lane < XN) {
+            const int c1 = LL + nfl + lane;
+            if (c1 < NN) {
+                IDX[c1] = 32 + lane;
+#pragma unroll
+                for (int ax = 0; ax < DD; ++ax) XS[ax * NP + c1] = x[RN - 1][ax];
+#pragma unroll
+                for (int f = 0; f < NF; ++f) FS[c1 * NR + f] = fr[RN - 1][f];
+                FS[c1 * NR + NF] = probe_sign(idx, 32 + lane);
+                FS[NN * NR + c1] = qsum[RN - 1];
+#pragma unroll
+                for (int m = 0; m < LL; ++m) Wm[(c1 - LL) * LP + m] = q[RN - 1][m];
+            }
+        }
+        ok = __all_sync(FULL, ok);
+        __syncwarp();
+
+        double r2min = INFINITY, anorm = 0.0;
+        bool bad = !ok;
+        if (ok) {
+            // ---- (3) Phi in the permuted order [pivots; free]: lane t owns node t and
+            //      walks t+1 .. t+(NN-1)/2 (mod NN); nodes 32.. take the tail
+            {
+                constexpr int H = (NN - 1) / 2;
+                auto phi = [&](const double (&xi)[DD], int j) {
+                    double df = xi[0] - XS[j];
+                    double d2 = df * df;
+#pragma unroll
+                    for (int ax = 1; ax < DD; ++ax) {
+                        df = xi[ax] - XS[ax * NP + j];
+                        d2 = fma(df, df, d2);
+                    }
+                    r2min = fmin(r2min, d2);
+                    return d2 * (d2 * fast_rsqrt(fmax(d2, 1e-300)));
+                };
+                if (lane < NN) {
+                    double xi[DD];
+#pragma unroll
+                    for (int ax = 0; ax < DD; ++ax) xi[ax] = XS[ax * NP + lane];
+                    int j = lane;
+#pragma unroll 4
+                    for (int st = 1; st <= H; ++st) {
+                        j = j + 1 == NN ? 0 : j + 1;
+                        const double v = phi(xi, j);
+                        PH[lane * P + j] = v;
+                        PH[j * P + lane] = v;
+                    }
+                    PH[lane * P + lane] = 0.0;
+                }
+                if constexpr (XN > 0) {
+                    constexpr int REM = XN * H;
+#pragma unroll
+                    for (int t = 0; t < (REM + 31) / 32; ++t) {
+                        const int p = lane + 32 * t;
+                        if (p < REM) {
+                            const int i = 32 + p / H;
+                            int jj = i + p % H + 1;
+                            if (jj >= NN) jj -= NN;
+                            double xi[DD];
+#pragma unroll
+                            for (int ax = 0; ax < DD; ++ax) xi[ax] = XS[ax * NP + i];
+                            const double v = phi(xi, jj);
+                            PH[i * P + jj] = v;
+                            PH[jj * P + i] = v;
+                        }
+                    }
+                    if (lane < XN) PH[(32 + lane) * P + 32 + lane] = 0.0;
+                }
+            }
+            __syncwarp();
+        }
+        // the coordinates are consumed: stage the next stencil's positions into XS
+        stage(idx + stride);
+        load_idx(idx + 2 * stride);
+        if (ok) {
+            // ||A||_inf of the saddle-point matrix (estimate only): node rows
+#pragma unroll
+            for (int s = 0; s < RN; ++s) {
+                const int t = lane + 32 * s;
+                if (t < NN) {
+                    // row t == column t (Phi is symmetric): lanes read consecutive words
+                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int j = 0; j < NN; ++j) acc[j & 3] += fabs(PH[j * P + t]);
+                    anorm = fmax(anorm, ((acc[0] + acc[1]) + (acc[2] + acc[3])) + FS[NN * NR + t]);
+                }
+            }
+            anorm = warp_max_nonneg(anorm);
+            if (P_.scale_code == MF_SCALE_SUPPORT) {
+                // constraint rows: the constant column sums to n, every other |monomial| <= 1
+                anorm = fmax(anorm, (double)NN);
+            } else {
+                // constraint rows sum |Q_im| over the nodes (no scale bound): use the node rows' bound n * max
+                anorm = fmax(anorm, (double)NN * warp_max_nonneg(fmax(qsum[0], qsum[RN - 1])));
+            }
+
+            // ---- (4) W row c (lane c): x L1 = l2, right-looking
+            const bool act = lane < M;
+            const int cc = act ? lane : 0;
+            double wr[LL];
+#pragma unroll
+            for (int m = 0; m < LL; ++m) wr[m] = Wm[cc * LP + m];
+#pragma unroll
+            for (int j = LL - 1; j >= 1; --j) {
+#pragma unroll
+                for (int k = 0; k < j; ++k) wr[k] = fma(-wr[j], QLU[j * LL + k], wr[k]);
+            }
+            if (act) {
+#pragma unroll
+                for (int m = 0; m < LL; ++m) Wm[lane * LP + m] = wr[m];
+            }
+            // particular solution w1p = L1^-T U1^-T g (uniform), right-looking
+            {
+                double w1p[LL][NR];
+#pragma unroll
+                for (int k = 0; k < LL; ++k) {
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) w1p[k][f] = P_.base_bot[f * MF_MAX_MONOMIALS + k] * facs[f];
+                    w1p[k][NF] = probe_sign(idx, NN + k);
+                }
+#pragma unroll
+                for (int j = 0; j < LL; ++j) {
+                    const double di = QLU[LL * LL + j];
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) w1p[j][f] *= di;
+#pragma unroll
+                    for (int k = j + 1; k < LL; ++k) {
+                        const double u = QLU[j * LL + k];
+#pragma unroll
+                        for (int f = 0; f < NR; ++f) w1p[k][f] = fma(-u, w1p[j][f], w1p[k][f]);
+                    }
+                }
+#pragma unroll
+                for (int j = LL - 1; j >= 1; --j) {
+#pragma unroll
+                    for (int k = 0; k < j; ++k) {
+                        const double l = QLU[j * LL + k];
+#pragma unroll
+                        for (int f = 0; f < NR; ++f) w1p[k][f] = fma(-l, w1p[j][f], w1p[k][f]);
+                    }
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int k = 0; k < LL; ++k)
+#pragma unroll
+                        for (int f = 0; f < NR; ++f) VS[k * NR + f] = w1p[k][f];
+                }
+                // residuals r_t = f_t - Phi[t][piv] w1p: pivot rows (lanes k < LL) to VS
+                if (lane < LL) {
+                    double rr[NR];
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) rr[f] = FS[lane * NR + f];
+#pragma unroll
+                    for (int k = 0; k < LL; ++k) {
+                        const double ph = PH[k * P + lane];
+#pragma unroll
+                        for (int f = 0; f < NR; ++f) rr[f] = fma(-ph, w1p[k][f], rr[f]);
+                    }
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) VS[LL * NR + lane * NR + f] = rr[f];
+                }
+            }
+            __syncwarp();  // W rows, w1p, r_piv visible
+            // free rows: bb_c = r_c - W_c r_piv  (= Z^T (f - Phi w_p))
+            double bb[NR];
+            {
+                const int t = LL + cc;
+#pragma unroll
+                for (int f = 0; f < NR; ++f) bb[f] = FS[t * NR + f];
+#pragma unroll
+                for (int k = 0; k < LL; ++k) {
+                    const double ph = PH[k * P + t];
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) bb[f] = fma(-ph, VS[k * NR + f], bb[f]);
+                }
+#pragma unroll
+                for (int k = 0; k < LL; ++k)
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) bb[f] = fma(-wr[k], VS[LL * NR + k * NR + f], bb[f]);
+            }
+
+            // ---- (5) Y = Phi12 - Phi11 W^T (l x m) on the fp64 tensor core
+            {
+                constexpr int LT = (LL + 7) / 8, MT = (M + 7) / 8, KS = (LL + 3) / 4;
+                double acc[LT][MT][2];
+#pragma unroll
+                for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int k = lt * 8 + g8, c = mt * 8 + 2 * t4 + h;
+                            acc[lt][mt][h] = (k < LL && c < M) ? PH[k * P + LL + c] : 0.0;
+                        }
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int k2 = ks * 4 + t4;
+                    double af[LT], bf[MT];
+#pragma unroll
+                    for (int lt = 0; lt < LT; ++lt) {
+                        const int k = lt * 8 + g8;
+                        af[lt] = (k2 < LL && k < LL) ? -PH[k * P + k2] : 0.0;
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int c = mt * 8 + g8;
+                        bf[mt] = (k2 < LL && c < M) ? Wm[c * LP + k2] : 0.0;
+                    }
+#pragma unroll
+                    for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) dmma_f64(acc[lt][mt][0], acc[lt][mt][1], af[lt], bf[mt]);
+                }
+#pragma unroll
+                for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int k = lt * 8 + g8, c = mt * 8 + 2 * t4 + h;
+                            if (k < LL && c < M) Ym[c * LP + k] = acc[lt][mt][h];
+                        }
+            }
+            __syncwarp();  // Y visible
+
+            // ---- (6) K = Phi22 - [H W] [W^T; Y] on the fp64 tensor core; row c -> lane c
+            double K[M];
+            {
+                constexpr int MT = (M + 7) / 8, KS = (2 * LL + 3) / 4;
+                double acc[MT][MT][2];
+#pragma unroll
+                for (int rt = 0; rt < MT; ++rt)
+#pragma unroll
+                    for (int ct = 0; ct < MT; ++ct)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c = rt * 8 + g8, c2 = ct * 8 + 2 * t4 + h;
+                            acc[rt][ct][h] = (c < M && c2 < M) ? PH[(LL + c) * P + LL + c2] : 0.0;
+                        }
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int kk = ks * 4 + t4;  // < LL: H column kk, else W / Y row kk - LL
+                    const bool hp = kk < LL, kv = kk < 2 * LL;
+                    const int kh = hp ? kk : 0, kw = hp ? 0 : (kv ? kk - LL : 0);
+                    double af[MT], bf[MT];
+#pragma unroll
+                    for (int rt = 0; rt < MT; ++rt) {
+                        const int c = rt * 8 + g8;
+                        const int cr = c < M ? c : 0;
+                        const double v = hp ? PH[(LL + cr) * P + kh] : Wm[cr * LP + kw];
+                        af[rt] = (c < M && kv) ? -v : 0.0;
+                    }
+#pragma unroll
+                    for (int ct = 0; ct < MT; ++ct) {
+                        const int c2 = ct * 8 + g8;
+                        const int cr = c2 < M ? c2 : 0;
+                        const double v = hp ? Wm[cr * LP + kh] : Ym[cr * LP + kw];
+                        bf[ct] = (c2 < M && kv) ? v : 0.0;
+                    }
+#pragma unroll
+                    for (int rt = 0; rt < MT; ++rt)
+#pragma unroll
+                        for (int ct = 0; ct < MT; ++ct) dmma_f64(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
+                }
+                __syncwarp();  // every read of Phi is done: K takes its place
+#pragma unroll
+                for (int rt = 0; rt < MT; ++rt)
+#pragma unroll
+                    for (int ct = 0; ct < MT; ++ct) {
+                        const int c = rt * 8 + g8, c2 = ct * 8 + 2 * t4;
+                        if (c < M && c2 < M) {
+                            if (c2 + 1 < MP) {
+                                *reinterpret_cast<double2*>(PH + c * MP + c2) = make_double2(acc[rt][ct][0], acc[rt][ct][1]);
+                            } else {
+                                PH[c * MP + c2] = acc[rt][ct][0];
+                            }
+                        }
+                    }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < M; ++j) K[j] = PH[cc * MP + j];
+            }
+            __syncwarp();
+
+            // ---- (7) pivot-free Gauss-Jordan on [K | b]; lane c keeps row c
+            double* Us = PH;
+            double* Bs = PH + M * MP;
+            double dinv_own = 0.0, d0 = 0.0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+                if (act) Us[k * MP + lane] = K[k];
+                if (lane == k) {
+#pragma unroll
+                    for (int f = 0; f < NR; ++f) Bs[k * NR + f] = bb[f];
+                }
+                __syncwarp();
+                const double* urow = Us + k * MP;
+                const double dk = urow[k];
+                const double rk = fast_rcp(dk);
+                if (k == 0) d0 = dk;
+                dinv_own = lane == k ? rk : dinv_own;
+                const double fac = lane != k ? K[k] * rk : 0.0;
+#pragma unroll
+                for (int j = k + 1; j < M; ++j) K[j] = fma(-fac, urow[j], K[j]);
+#pragma unroll
+                for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * NR + f], bb[f]);
+            }
+#pragma unroll
+            for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;  // v_c = b_c / d_c
+            bad = bad || !__all_sync(FULL, !act || dinv_own * d0 > 0.0);
+
+            // ---- (8) outputs: free weights; pivot weights w1p - W^T v and the
+            //      multipliers' right-hand side r_piv - Y v as one tensor-core product
+            double zw = 0.0, xw[NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) xw[f] = 0.0;
+            if (act) {
+                const int node = IDX[LL + lane];
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    bad |= !isfinite(bb[f]);
+                    a.out[((size_t)idx * NF + f) * NN + node] = bb[f];
+                    xw[f] = fabs(bb[f]);
+                }
+                zw = fabs(bb[NF]);
+#pragma unroll
+                for (int f = 0; f < NR; ++f) VS[3 * LL * NR + lane * NR + f] = bb[f];
+            }
+            __syncwarp();
+            {
+                constexpr int RT = (2 * LL + 7) / 8, CS = (M + 3) / 4;
+                double acc[RT][2];
+#pragma unroll
+                for (int rt = 0; rt < RT; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+#pragma unroll
+                for (int cs = 0; cs < CS; ++cs) {
+                    const int c = cs * 4 + t4;
+                    const int cr = c < M ? c : 0;
+                    const double bv = (c < M && g8 < NR) ? VS[3 * LL * NR + cr * NR + (g8 < NR ? g8 : 0)] : 0.0;
+#pragma unroll
+                    for (int rt = 0; rt < RT; ++rt) {
+                        const int r = rt * 8 + g8;
+                        double av = 0.0;
+                        if (c < M && r < 2 * LL) av = r < LL ? Wm[cr * LP + r] : Ym[cr * LP + (r - LL)];
+                        dmma_f64(acc[rt][0], acc[rt][1], av, bv);
+                    }
+                }
+#pragma unroll
+                for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = rt * 8 + g8, f = 2 * t4 + h;
+                        if (f < NR && r < LL) {
+                            const double w = VS[r * NR + f] - acc[rt][h];
+                            if (f < NF) {
+                                bad |= !isfinite(w);
+                                a.out[((size_t)idx * NF + f) * NN + IDX[r]] = w;
+                                xw[f] = fmax(xw[f], fabs(w));
+                            } else {
+                                zw = fmax(zw, fabs(w));
+                            }
+                        } else if (f < NF && r >= LL && r < 2 * LL) {
+                            VS[2 * LL * NR + (r - LL) * NR + f] = VS[LL * NR + (r - LL) * NR + f] - acc[rt][h];
+                        }
+                    }
+            }
+            __syncwarp();
+            // lambda from Q1 lambda = r_piv - Y v (L1 then U1, uniform, right-looking)
+            double la[NF];
+            {
+                double lam[LL][NF];
+#pragma unroll
+                for (int k = 0; k < LL; ++k)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) lam[k][f] = VS[2 * LL * NR + k * NR + f];
+#pragma unroll
+                for (int j = 0; j < LL; ++j)
+#pragma unroll
+                    for (int k = j + 1; k < LL; ++k) {
+                        const double l = QLU[k * LL + j];
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) lam[k][f] = fma(-l, lam[j][f], lam[k][f]);
+                    }
+#pragma unroll
+                for (int f = 0; f < NF; ++f) la[f] = 0.0;
+#pragma unroll
+                for (int j = LL - 1; j >= 0; --j) {
+                    const double di = QLU[LL * LL + j];
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        lam[j][f] *= di;
+                        la[f] = fmax(la[f], fabs(lam[j][f]));
+                    }
+#pragma unroll
+                    for (int k = 0; k < j; ++k) {
+                        const double u = QLU[k * LL + j];
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) lam[k][f] = fma(-u, lam[j][f], lam[k][f]);
+                    }
+                }
+            }
+            zw = warp_max_nonneg(zw);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) xw[f] = warp_max_nonneg(xw[f]);
+            double ratio = 0.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) ratio = fmax(ratio, fmax(xw[f], la[f]) / xw[f]);
+            const double est = anorm * zw * ratio;
+            r2min = warp_min_nonneg(r2min);
+            const bool close = r2min < a.min_sep2 * rc2max;
+            bad = __any_sync(FULL, bad);
+            if (!bad && lane == 0 && (close || !(est <= a.hybrid_thresh))) {
+                unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+                a.flag_list[slot] = idx;
+            }
+        }
+        // failed / indefinite / non-finite rows are re-solved in the reference's order
+        if (bad && lane == 0) {
+            unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+            a.flag_list[slot] = idx;
+        }
+        if (lane == 0) a.status[idx] = 0;
+        __syncwarp();
+    }
+    cp_async_wait_all();
+}
+
+template <int NN, int DEG, int DD, int NF>
+int launch_ns2(const PhsArgs& a, cudaStream_t st, int sms) {
+    using Cfg = Ns2Cfg<NN, DEG, DD, NF>;
+    constexpr GradedLex<DD, DEG> g{};
+    if (!a.flag_list || a.kappa || a.P.l != Cfg::LL || a.P.nf != NF) return MF_ERR_UNSUPPORTED;
+    for (int m = 0; m < Cfg::LL; ++m)
+        for (int ax = 0; ax < DD; ++ax)
+            if (a.P.expos[m * DD + ax] != g.e[m][ax]) return MF_ERR_UNSUPPORTED;
+    if (a.P.k != 3 || a.P.even || DEG < 1) return MF_ERR_UNSUPPORTED;
+    auto kern = phs_ns2<NN, DEG, DD, NF>;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    int per_sm = 0;
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::WARPS * 32, Cfg::SMEM));
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (a.m + Cfg::WARPS - 1) / Cfg::WARPS;
+    const int64_t cap = (int64_t)sms * per_sm * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, Cfg::WARPS * 32, Cfg::SMEM, st>>>(a);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+#define MF_INSTANTIATE_NS2(NN, DEG, DD, NF) template int launch_ns2<NN, DEG, DD, NF>(const PhsArgs&, cudaStream_t, int);
+
+}  // namespace mf
