@@ -35,8 +35,28 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// 1/x from the MUFU seed (high word, ~2^-22) by one cubically convergent step:
+// r (1 + e + e^2), e = 1 - x r
+__device__ __forceinline__ double rcp_c3(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
+}
+// 1/sqrt(x), x > 0, likewise: y (1 + e/2 + 3 e^2 / 8), e = 1 - x y^2
+__device__ __forceinline__ double rsqrt_c3(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
+}
 
 // warp max of a non-negative double (or +0 for lanes that do not take part):
 // the IEEE bit pattern of non-negative doubles is ordered like the values
@@ -74,15 +94,20 @@ struct Ns2Cfg {
     static constexpr int LP = ns_pitch(LL);     // W / Y row pitch
     static constexpr int WARPS = 4;
     // per-warp shared layout (doubles)
-    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * MP + M * NR));
+    static constexpr int UP = ns_even(M + 1);   // Gauss-Jordan column pitch
+    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * UP + M * NR));
     static constexpr int XS_DBL = ns_even(DD * NP + DD);  // scaled coords (permuted), then the staged raw positions
-    static constexpr int QLU_DBL = ns_even(LL * LL + LL); // L1 (strict lower), U1 (upper), 1/U1[k][k]
+    static constexpr int NC = NN + NR + LL;     // columns of [Q^T | g | I] in the Gauss-Jordan sweep
+    static constexpr int CS = (NC + 31) / 32;   // column slots per lane
+    static constexpr int QLU_DBL = ns_even(LL * LL + 2 * LL);  // rows of Q1^-1, then two pivot-column buffers
     static constexpr int W_DBL = M * LP;
     static constexpr int Y_DBL = M * LP;
     static constexpr int F_DBL = ns_even(NN * NR + NN);   // node rhs (permuted) + |Q| row sums
     static constexpr int V_DBL = ns_even(3 * LL * NR + M * NR);  // w1p, r_piv, lambda rhs, v
     static constexpr int IDX_DBL = ns_even((NN + 1) / 2);
-    static constexpr int WARP_DBL = PH_DBL + XS_DBL + QLU_DBL + W_DBL + Y_DBL + F_DBL + V_DBL + IDX_DBL;
+    static constexpr int IB_ROW = 2 * ns_even((NN + 1) / 2);  // int offset of the staged row index (8-byte aligned)
+    static constexpr int IB_DBL = IB_ROW / 2 + 2;
+    static constexpr int WARP_DBL = PH_DBL + XS_DBL + QLU_DBL + W_DBL + Y_DBL + F_DBL + V_DBL + IDX_DBL + IB_DBL;
     static constexpr size_t SMEM = (size_t)WARPS * WARP_DBL * sizeof(double);
     static_assert(M >= 1 && M <= 32, "the reduced system must fit one warp");
     static_assert(RN <= 2 && LL <= 32 && NR <= 8, "shape outside the kernel's layout");
@@ -93,18 +118,20 @@ template <int NN, int DEG, int DD, int NF>
 __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
     using Cfg = Ns2Cfg<NN, DEG, DD, NF>;
     constexpr int LL = Cfg::LL, M = Cfg::M, MP = Cfg::MP, NR = Cfg::NR, RN = Cfg::RN, XN = Cfg::XN,
-                  NP = Cfg::NP, P = Cfg::P, LP = Cfg::LP;
+                  NP = Cfg::NP, P = Cfg::P, LP = Cfg::LP, NC = Cfg::NC, CS = Cfg::CS;
     extern __shared__ __align__(16) double smem_n2[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     double* PH = smem_n2 + (size_t)wib * Cfg::WARP_DBL;  // Phi (permuted), then K / elimination rows
     double* XS = PH + Cfg::PH_DBL;     // scaled coords SoA [ax*NP + t]; staged raw positions (next stencil)
-    double* QLU = XS + Cfg::XS_DBL;    // row k: L1[k][0..k-1], U1[k][k..]; QLU[LL*LL + k] = 1/U1[k][k]
-    double* Wm = QLU + Cfg::QLU_DBL;   // L2 rows, then W rows (reduced index c at c*LP)
+    double* QI = XS + Cfg::XS_DBL;     // row m of Q1^-1 at m*LL; pivot columns (double-buffered) at LL*LL
+    double* PV = QI + LL * LL;
+    double* Wm = QI + Cfg::QLU_DBL;    // W rows (reduced index c at c*LP)
     double* Ym = Wm + Cfg::W_DBL;      // Y column c at c*LP
     double* FS = Ym + Cfg::Y_DBL;      // node rhs FS[t*NR + f] (permuted t); |Q| row sums at NN*NR + t
     double* VS = FS + Cfg::F_DBL;      // w1p[k*NR+f], r_piv at LL*NR, lambda rhs at 2*LL*NR, v at 3*LL*NR
     int* IDX = reinterpret_cast<int*>(VS + Cfg::V_DBL);  // permuted index -> stencil node
+    int* IB = IDX + 2 * Cfg::IDX_DBL;  // staged node indices of the next-but-one stencil, then its row
     const PhsParams& P_ = a.P;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int g8 = lane >> 2, t4 = lane & 3;  // tensor-core fragment coordinates
@@ -112,38 +139,45 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * Cfg::WARPS;
     int64_t idx = (int64_t)blockIdx.x * Cfg::WARPS + wib;
 
-    // node indices of the stencil staged next (loaded one stencil ahead of the
-    // staging, so the cp.async addresses never wait on a global load)
-    int64_t srow = 0;
-    int ssti[RN] = {};
-    auto load_idx = [&](int64_t id) {
+    // Two-stage prefetch, all through cp.async (no register ever waits on a
+    // global load): the node indices of stencil i+2 go to IB while the
+    // positions of stencil i+1 (addressed by the indices staged one stencil
+    // earlier) go to XS.
+    auto stage_idx = [&](int64_t id) {
         if (id < a.m) {
-            srow = a.rows[id];
 #pragma unroll
             for (int s = 0; s < RN; ++s) {
                 const int j = lane + 32 * s;
-                ssti[s] = j < NN ? a.stencils[id * NN + j] : 0;
+                if (j < NN) cp_async4(IB + j, a.stencils + id * NN + j);
             }
+            if (lane == 0) cp_async8(IB + Cfg::IB_ROW, a.rows + id);
         }
     };
-    // stage the raw positions of stencil `id` (nodes SoA, then the centre)
     auto stage = [&](int64_t id) {
         if (id < a.m) {
+            int nd[RN];
+#pragma unroll
+            for (int s = 0; s < RN; ++s) nd[s] = lane + 32 * s < NN ? IB[lane + 32 * s] : 0;
+            const int64_t rw = *reinterpret_cast<const int64_t*>(IB + Cfg::IB_ROW);
+            __syncwarp();  // IB is read: the next indices may land
 #pragma unroll
             for (int s = 0; s < RN; ++s) {
                 const int j = lane + 32 * s;
                 if (j < NN) {
 #pragma unroll
-                    for (int ax = 0; ax < DD; ++ax) cp_async8(XS + ax * NP + j, a.pos + (int64_t)ssti[s] * DD + ax);
+                    for (int ax = 0; ax < DD; ++ax) cp_async8(XS + ax * NP + j, a.pos + (int64_t)nd[s] * DD + ax);
                 }
             }
-            if (lane < DD) cp_async8(XS + DD * NP + lane, a.pos + srow * DD + lane);
+            if (lane < DD) cp_async8(XS + DD * NP + lane, a.pos + rw * DD + lane);
         }
+        stage_idx(id + stride);
         cp_async_commit();
     };
-    load_idx(idx);
+    stage_idx(idx);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
     stage(idx);
-    load_idx(idx + stride);
 
 #pragma unroll 1
     for (; idx < a.m; idx += stride) {
@@ -171,7 +205,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             r2max = warp_max_nonneg(mx);
             const int sc_code = P_.scale_code;
             if (sc_code == MF_SCALE_SUPPORT) {
-                if (r2max > 0.0) rs = fast_rsqrt(r2max);
+                if (r2max > 0.0) rs = rsqrt_c3(r2max);
                 else stat = 2;
             } else if (sc_code == MF_SCALE_NEAREST) {
                 double mn = INFINITY;
@@ -179,7 +213,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 for (int s = 0; s < RN; ++s)
                     if (r2[s] > 0.0) mn = fmin(mn, r2[s]);
                 mn = warp_min_nonneg(mn);
-                if (mn < INFINITY) rs = fast_rsqrt(mn);
+                if (mn < INFINITY) rs = rsqrt_c3(mn);
                 else stat = 2;
             }
         }
@@ -190,7 +224,9 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             const int o = P_.orders[f];
             facs[f] = o == 0 ? 1.0 : (o == 1 ? rs : rs * rs);
         }
-        double q[RN][LL], fr[RN][NF], qsum[RN];
+        // columns of [Q^T | g | I]: column j = lane + 32 s is node j (its monomials),
+        // then the constraint right-hand sides (families, probe), then the identity
+        double q[CS][LL], fr[RN][NF], qsum[RN];
 #pragma unroll
         for (int s = 0; s < RN; ++s) {
 #pragma unroll
@@ -203,7 +239,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             double rr2 = x[s][0] * x[s][0];
 #pragma unroll
             for (int ax = 1; ax < DD; ++ax) rr2 = fma(x[s][ax], x[s][ax], rr2);
-            const double rsq = rr2 > 0.0 ? fast_rsqrt(rr2) : 0.0;
+            const double rsq = rr2 > 0.0 ? rsqrt_c3(rr2) : 0.0;
             const double r = rr2 * rsq, ir2 = rsq * rsq;
             const double d1r = 3.0 * r, d2v = 6.0 * r;
 #pragma unroll
@@ -224,8 +260,26 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 fr[s][f] = t * facs[f];
             }
         }
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+            const int j = lane + 32 * s;
+            if (j >= NN) {
+                const int f = j - NN, m = j - NN - NR;
+#pragma unroll
+                for (int k = 0; k < LL; ++k) {
+                    double v = 0.0;
+                    if (f < NF) v = P_.base_bot[(f < NF ? f : 0) * MF_MAX_MONOMIALS + k] * facs[f < NF ? f : 0];
+                    else if (f == NF) v = probe_sign(idx, NN + k);
+                    else if (m == k) v = 1.0;
+                    q[s][k] = v;
+                }
+            }
+        }
 
-        // ---- (2) LU with partial pivoting of Q over the lane-resident nodes
+        // ---- (2) Gauss-Jordan on [Q^T | g | I] with node (column) pivoting over the
+        //      lane-resident nodes: the row operations are Q1^-T, so the free node
+        //      columns become W^T, the g columns the particular solution w1p and the
+        //      identity columns the rows of Q1^-1
         bool ok = stat == 0;
         bool live = lane < NN;  // slot 0 is a pivot candidate until it wins
         int myk = 0;
@@ -239,22 +293,25 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             const unsigned mk = __reduce_max_sync(FULL, key);
             const int wl = 31 - (int)(mk & 31u);
             ok = ok && (mk >> 5) != 0u;
+            double* pc = PV + (k & 1) * LL;  // two buffers: the next step's winner never overwrites a column being read
             if (lane == wl && live) {
 #pragma unroll
-                for (int m = 0; m < LL; ++m) QLU[k * LL + m] = q[0][m];
+                for (int r = 0; r < LL; ++r) pc[r] = q[0][r];
                 live = false;
                 myk = k;
             }
             __syncwarp();
-            const double inv = fast_rcp(QLU[k * LL + k]);
-            if (lane == 0) QLU[LL * LL + k] = inv;
+            double pv[LL];
 #pragma unroll
-            for (int s = 0; s < RN; ++s) {
-                const bool upd = s == 0 ? live : lane < XN;
-                const double l = upd ? q[s][k] * inv : 0.0;
-                q[s][k] = l;
+            for (int r = 0; r < LL; ++r) pv[r] = pc[r];
+            const double inv = rcp_c3(pv[k]);
 #pragma unroll
-                for (int m = k + 1; m < LL; ++m) q[s][m] = fma(-l, QLU[k * LL + m], q[s][m]);
+            for (int s = 0; s < CS; ++s) {
+                const double t = q[s][k] * inv;
+#pragma unroll
+                for (int r = 0; r < LL; ++r)
+                    if (r != k) q[s][r] = fma(-t, pv[r], q[s][r]);
+                q[s][k] = t;
             }
         }
         // free nodes: live slot-0 lanes in lane order, then the slot-1 nodes
@@ -289,56 +346,110 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 for (int m = 0; m < LL; ++m) Wm[(c1 - LL) * LP + m] = q[RN - 1][m];
             }
         }
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+            const int j = lane + 32 * s;
+            if (j >= NN && j < NN + NR) {
+#pragma unroll
+                for (int k = 0; k < LL; ++k) VS[k * NR + (j - NN)] = q[s][k];  // w1p
+            } else if (j >= NN + NR && j < NC) {
+#pragma unroll
+                for (int r = 0; r < LL; ++r) QI[(j - NN - NR) * LL + r] = q[s][r];  // Q1^-1 row
+            }
+        }
         ok = __all_sync(FULL, ok);
         __syncwarp();
 
-        double r2min = INFINITY, anorm = 0.0;
+        const double close_thr = a.min_sep2 * rc2max;  // HYBRID: (min separation / radius)^2 threshold
+        bool close = false;
+        double anorm = 0.0;
         bool bad = !ok;
         if (ok) {
             // ---- (3) Phi in the permuted order [pivots; free]: lane t owns node t and
             //      walks t+1 .. t+(NN-1)/2 (mod NN); nodes 32.. take the tail
             {
                 constexpr int H = (NN - 1) / 2;
-                auto phi = [&](const double (&xi)[DD], int j) {
-                    double df = xi[0] - XS[j];
-                    double d2 = df * df;
-#pragma unroll
-                    for (int ax = 1; ax < DD; ++ax) {
-                        df = xi[ax] - XS[ax * NP + j];
-                        d2 = fma(df, df, d2);
-                    }
-                    r2min = fmin(r2min, d2);
-                    return d2 * (d2 * fast_rsqrt(fmax(d2, 1e-300)));
-                };
+                // loads of a chunk of pairs first, then the arithmetic, then the
+                // stores: shared stores would otherwise order every pair's loads
+                // behind the previous pair's stores and serialise the chains
+                constexpr int CH = 6;
                 if (lane < NN) {
                     double xi[DD];
 #pragma unroll
                     for (int ax = 0; ax < DD; ++ax) xi[ax] = XS[ax * NP + lane];
-                    int j = lane;
-#pragma unroll 4
-                    for (int st = 1; st <= H; ++st) {
-                        j = j + 1 == NN ? 0 : j + 1;
-                        const double v = phi(xi, j);
-                        PH[lane * P + j] = v;
-                        PH[j * P + lane] = v;
+#pragma unroll
+                    for (int st0 = 1; st0 <= H; st0 += CH) {
+                        int jc[CH];
+                        double xj[CH][DD], v[CH];
+                        bool cl = false;
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) {
+                            if (st0 + u <= H) {
+                                const int t = lane + st0 + u;
+                                jc[u] = t >= NN ? t - NN : t;
+#pragma unroll
+                                for (int ax = 0; ax < DD; ++ax) xj[u][ax] = XS[ax * NP + jc[u]];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) {
+                            if (st0 + u <= H) {
+                                double df = xi[0] - xj[u][0];
+                                double d2 = df * df;
+#pragma unroll
+                                for (int ax = 1; ax < DD; ++ax) {
+                                    df = xi[ax] - xj[u][ax];
+                                    d2 = fma(df, df, d2);
+                                }
+                                cl = cl | (d2 < close_thr);
+                                // (+1e-300: coincident nodes give r^3 = 0 instead of 0 * inf)
+                                v[u] = d2 * (d2 * rsqrt_c3(d2 + 1e-300));
+                            }
+                        }
+                        close = close | cl;
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) {
+                            if (st0 + u <= H) {
+                                PH[lane * P + jc[u]] = v[u];
+                                PH[jc[u] * P + lane] = v[u];
+                            }
+                        }
                     }
                     PH[lane * P + lane] = 0.0;
                 }
                 if constexpr (XN > 0) {
-                    constexpr int REM = XN * H;
+                    constexpr int REM = XN * H, RT = (REM + 31) / 32;
+                    int ic[RT], jc[RT];
+                    double xa[RT][DD], xb[RT][DD], v[RT];
 #pragma unroll
-                    for (int t = 0; t < (REM + 31) / 32; ++t) {
-                        const int p = lane + 32 * t;
-                        if (p < REM) {
-                            const int i = 32 + p / H;
-                            int jj = i + p % H + 1;
-                            if (jj >= NN) jj -= NN;
-                            double xi[DD];
+                    for (int t = 0; t < RT; ++t) {
+                        const int p = lane + 32 * t < REM ? lane + 32 * t : 0;
+                        ic[t] = 32 + p / H;
+                        jc[t] = ic[t] + p % H + 1;
+                        if (jc[t] >= NN) jc[t] -= NN;
 #pragma unroll
-                            for (int ax = 0; ax < DD; ++ax) xi[ax] = XS[ax * NP + i];
-                            const double v = phi(xi, jj);
-                            PH[i * P + jj] = v;
-                            PH[jj * P + i] = v;
+                        for (int ax = 0; ax < DD; ++ax) {
+                            xa[t][ax] = XS[ax * NP + ic[t]];
+                            xb[t][ax] = XS[ax * NP + jc[t]];
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        double df = xa[t][0] - xb[t][0];
+                        double d2 = df * df;
+#pragma unroll
+                        for (int ax = 1; ax < DD; ++ax) {
+                            df = xa[t][ax] - xb[t][ax];
+                            d2 = fma(df, df, d2);
+                        }
+                        close = close | (d2 < close_thr);
+                        v[t] = d2 * (d2 * rsqrt_c3(d2 + 1e-300));
+                    }
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        if (lane + 32 * t < REM) {
+                            PH[ic[t] * P + jc[t]] = v[t];
+                            PH[jc[t] * P + ic[t]] = v[t];
                         }
                     }
                     if (lane < XN) PH[(32 + lane) * P + 32 + lane] = 0.0;
@@ -348,7 +459,6 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
         }
         // the coordinates are consumed: stage the next stencil's positions into XS
         stage(idx + stride);
-        load_idx(idx + 2 * stride);
         if (ok) {
             // ||A||_inf of the saddle-point matrix (estimate only): node rows
 #pragma unroll
@@ -371,57 +481,10 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 anorm = fmax(anorm, (double)NN * warp_max_nonneg(fmax(qsum[0], qsum[RN - 1])));
             }
 
-            // ---- (4) W row c (lane c): x L1 = l2, right-looking
+            // ---- (4) residuals of the particular solution
             const bool act = lane < M;
             const int cc = act ? lane : 0;
-            double wr[LL];
-#pragma unroll
-            for (int m = 0; m < LL; ++m) wr[m] = Wm[cc * LP + m];
-#pragma unroll
-            for (int j = LL - 1; j >= 1; --j) {
-#pragma unroll
-                for (int k = 0; k < j; ++k) wr[k] = fma(-wr[j], QLU[j * LL + k], wr[k]);
-            }
-            if (act) {
-#pragma unroll
-                for (int m = 0; m < LL; ++m) Wm[lane * LP + m] = wr[m];
-            }
-            // particular solution w1p = L1^-T U1^-T g (uniform), right-looking
             {
-                double w1p[LL][NR];
-#pragma unroll
-                for (int k = 0; k < LL; ++k) {
-#pragma unroll
-                    for (int f = 0; f < NF; ++f) w1p[k][f] = P_.base_bot[f * MF_MAX_MONOMIALS + k] * facs[f];
-                    w1p[k][NF] = probe_sign(idx, NN + k);
-                }
-#pragma unroll
-                for (int j = 0; j < LL; ++j) {
-                    const double di = QLU[LL * LL + j];
-#pragma unroll
-                    for (int f = 0; f < NR; ++f) w1p[j][f] *= di;
-#pragma unroll
-                    for (int k = j + 1; k < LL; ++k) {
-                        const double u = QLU[j * LL + k];
-#pragma unroll
-                        for (int f = 0; f < NR; ++f) w1p[k][f] = fma(-u, w1p[j][f], w1p[k][f]);
-                    }
-                }
-#pragma unroll
-                for (int j = LL - 1; j >= 1; --j) {
-#pragma unroll
-                    for (int k = 0; k < j; ++k) {
-                        const double l = QLU[j * LL + k];
-#pragma unroll
-                        for (int f = 0; f < NR; ++f) w1p[k][f] = fma(-l, w1p[j][f], w1p[k][f]);
-                    }
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int k = 0; k < LL; ++k)
-#pragma unroll
-                        for (int f = 0; f < NR; ++f) VS[k * NR + f] = w1p[k][f];
-                }
                 // residuals r_t = f_t - Phi[t][piv] w1p: pivot rows (lanes k < LL) to VS
                 if (lane < LL) {
                     double rr[NR];
@@ -431,7 +494,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                     for (int k = 0; k < LL; ++k) {
                         const double ph = PH[k * P + lane];
 #pragma unroll
-                        for (int f = 0; f < NR; ++f) rr[f] = fma(-ph, w1p[k][f], rr[f]);
+                        for (int f = 0; f < NR; ++f) rr[f] = fma(-ph, VS[k * NR + f], rr[f]);
                     }
 #pragma unroll
                     for (int f = 0; f < NR; ++f) VS[LL * NR + lane * NR + f] = rr[f];
@@ -451,9 +514,11 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                     for (int f = 0; f < NR; ++f) bb[f] = fma(-ph, VS[k * NR + f], bb[f]);
                 }
 #pragma unroll
-                for (int k = 0; k < LL; ++k)
+                for (int k = 0; k < LL; ++k) {
+                    const double wk = Wm[cc * LP + k];
 #pragma unroll
-                    for (int f = 0; f < NR; ++f) bb[f] = fma(-wr[k], VS[LL * NR + k * NR + f], bb[f]);
+                    for (int f = 0; f < NR; ++f) bb[f] = fma(-wk, VS[LL * NR + k * NR + f], bb[f]);
+                }
             }
 
             // ---- (5) Y = Phi12 - Phi11 W^T (l x m) on the fp64 tensor core
@@ -560,31 +625,38 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             __syncwarp();
 
             // ---- (7) pivot-free Gauss-Jordan on [K | b]; lane c keeps row c
+            // column k (== row k of the symmetric trailing matrix) is stored with
+            // entry k+1 on a 16-byte boundary, so the pivot row streams in pairs
             double* Us = PH;
-            double* Bs = PH + M * MP;
-            double dinv_own = 0.0, d0 = 0.0;
+            double* Bs = PH + M * Cfg::UP;
 #pragma unroll
             for (int k = 0; k < M; ++k) {
-                if (act) Us[k * MP + lane] = K[k];
+                double* urow = Us + k * Cfg::UP + ((k + 1) & 1);
+                if (act) urow[lane] = K[k];
                 if (lane == k) {
 #pragma unroll
                     for (int f = 0; f < NR; ++f) Bs[k * NR + f] = bb[f];
                 }
                 __syncwarp();
-                const double* urow = Us + k * MP;
-                const double dk = urow[k];
-                const double rk = fast_rcp(dk);
-                if (k == 0) d0 = dk;
-                dinv_own = lane == k ? rk : dinv_own;
+                const double rk = rcp_c3(urow[k]);
                 const double fac = lane != k ? K[k] * rk : 0.0;
+                int j = k + 1;
 #pragma unroll
-                for (int j = k + 1; j < M; ++j) K[j] = fma(-fac, urow[j], K[j]);
+                for (; j + 1 < M; j += 2) {
+                    const double2 u = *reinterpret_cast<const double2*>(urow + j);
+                    K[j] = fma(-fac, u.x, K[j]);
+                    K[j + 1] = fma(-fac, u.y, K[j + 1]);
+                }
+                if (j < M) K[j] = fma(-fac, urow[j], K[j]);
 #pragma unroll
                 for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * NR + f], bb[f]);
             }
+            // v_c = b_c / d_c with d_c the pivot lane c stored at its step
+            const double d0 = Us[1], dc = Us[cc * Cfg::UP + ((cc + 1) & 1) + cc];
+            const double dinv_own = rcp_c3(dc);
 #pragma unroll
-            for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;  // v_c = b_c / d_c
-            bad = bad || !__all_sync(FULL, !act || dinv_own * d0 > 0.0);
+            for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;
+            bad = bad || !__all_sync(FULL, !act || dc * d0 > 0.0);
 
             // ---- (8) outputs: free weights; pivot weights w1p - W^T v and the
             //      multipliers' right-hand side r_piv - Y v as one tensor-core product
@@ -642,39 +714,21 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                     }
             }
             __syncwarp();
-            // lambda from Q1 lambda = r_piv - Y v (L1 then U1, uniform, right-looking)
+            // lambda = Q1^-1 (r_piv - Y v): lane m owns row m of Q1^-1
             double la[NF];
             {
-                double lam[LL][NF];
+                const int mm = lane < LL ? lane : 0;
+                double lam[NF];
 #pragma unroll
-                for (int k = 0; k < LL; ++k)
+                for (int f = 0; f < NF; ++f) lam[f] = 0.0;
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) lam[k][f] = VS[2 * LL * NR + k * NR + f];
+                for (int r = 0; r < LL; ++r) {
+                    const double qi = QI[mm * LL + r];
 #pragma unroll
-                for (int j = 0; j < LL; ++j)
-#pragma unroll
-                    for (int k = j + 1; k < LL; ++k) {
-                        const double l = QLU[k * LL + j];
-#pragma unroll
-                        for (int f = 0; f < NF; ++f) lam[k][f] = fma(-l, lam[j][f], lam[k][f]);
-                    }
-#pragma unroll
-                for (int f = 0; f < NF; ++f) la[f] = 0.0;
-#pragma unroll
-                for (int j = LL - 1; j >= 0; --j) {
-                    const double di = QLU[LL * LL + j];
-#pragma unroll
-                    for (int f = 0; f < NF; ++f) {
-                        lam[j][f] *= di;
-                        la[f] = fmax(la[f], fabs(lam[j][f]));
-                    }
-#pragma unroll
-                    for (int k = 0; k < j; ++k) {
-                        const double u = QLU[k * LL + j];
-#pragma unroll
-                        for (int f = 0; f < NF; ++f) lam[k][f] = fma(-u, lam[j][f], lam[k][f]);
-                    }
+                    for (int f = 0; f < NF; ++f) lam[f] = fma(qi, VS[2 * LL * NR + r * NR + f], lam[f]);
                 }
+#pragma unroll
+                for (int f = 0; f < NF; ++f) la[f] = warp_max_nonneg(lane < LL ? fabs(lam[f]) : 0.0);
             }
             zw = warp_max_nonneg(zw);
 #pragma unroll
@@ -683,8 +737,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) ratio = fmax(ratio, fmax(xw[f], la[f]) / xw[f]);
             const double est = anorm * zw * ratio;
-            r2min = warp_min_nonneg(r2min);
-            const bool close = r2min < a.min_sep2 * rc2max;
+            close = __any_sync(FULL, close);
             bad = __any_sync(FULL, bad);
             if (!bad && lane == 0 && (close || !(est <= a.hybrid_thresh))) {
                 unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);

@@ -70,13 +70,17 @@ def main():
             key = ("?", 0)
         a = agg[key]
         a["inst"] += float(r["Instructions Executed"] or 0)
+        a["wf"] += float(r.get("L1 Wavefronts Shared") or 0)
+        a["wfi"] += float(r.get("L1 Wavefronts Shared Ideal") or 0)
+        tot["wf"] += float(r.get("L1 Wavefronts Shared") or 0)
         a["samples"] += float(r["Warp Stall Sampling (All Samples)"] or 0)
         for c in stall_cols:
             a[c] += float(r[c] or 0)
         tot["inst"] += float(r["Instructions Executed"] or 0)
         tot["samples"] += float(r["Warp Stall Sampling (All Samples)"] or 0)
     print(f"kernel: {kname[:160]}")
-    print(f"sass rows {len(rows)}, unmapped {nomap}; total inst {tot['inst']:.4g}, samples {tot['samples']:.4g}")
+    print(f"sass rows {len(rows)}, unmapped {nomap}; total inst {tot['inst']:.4g}, samples {tot['samples']:.4g}, "
+          f"shared wavefronts {tot['wf']:.4g}")
     src_cache = {}
 
     def src(f, l):
@@ -102,17 +106,19 @@ def main():
             name = marker.get(l, "?") if f.endswith(regions.split("/")[-1]) else "other:" + f.split("/")[-1]
             for k, v in a.items():
                 ragg[name][k] += v
-        print(f"\n{'region':62s} {'inst%':>6s} {'samp%':>6s}  top stalls")
+        print(f"\n{'region':62s} {'inst%':>6s} {'samp%':>6s} {'smem wf%':>8s} {'(ideal)':>8s}  top stalls")
         for name, a in sorted(ragg.items(), key=lambda kv: -kv[1]["samples"]):
             st = sorted(((a[c], c[6:]) for c in stall_cols), reverse=True)[:4]
             sts = " ".join(f"{n}:{100 * v / max(a['samples'], 1):.0f}" for v, n in st if v > 0)
-            print(f"{name:62s} {100 * a['inst'] / tot['inst']:6.1f} {100 * a['samples'] / tot['samples']:6.1f}  {sts}")
-    print(f"\n{'file:line':28s} {'inst%':>6s} {'samp%':>6s}  top stalls | source")
-    for (f, l), a in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]:
+            print(f"{name:62s} {100 * a['inst'] / tot['inst']:6.1f} {100 * a['samples'] / tot['samples']:6.1f} "
+                  f"{100 * a['wf'] / max(tot['wf'], 1):8.1f} {100 * a['wfi'] / max(tot['wf'], 1):8.1f}  {sts}")
+    key = "wf" if "--by-wf" in args else "samples"
+    print(f"\n{'file:line':28s} {'inst%':>6s} {'samp%':>6s} {'wf%':>6s}  top stalls | source")
+    for (f, l), a in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
         st = sorted(((a[c], c[6:]) for c in stall_cols), reverse=True)[:3]
         sts = " ".join(f"{n}:{100 * v / max(a['samples'], 1):.0f}" for v, n in st if v > 0)
         print(f"{f.split('/')[-1] + ':' + str(l):28s} {100 * a['inst'] / tot['inst']:6.1f} "
-              f"{100 * a['samples'] / tot['samples']:6.1f}  {sts:32s} | {src(f, l)}")
+              f"{100 * a['samples'] / tot['samples']:6.1f} {100 * a['wf'] / max(tot['wf'], 1):6.1f}  {sts:32s} | {src(f, l)}")
 
 
 if __name__ == "__main__":
