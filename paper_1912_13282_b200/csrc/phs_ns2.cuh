@@ -101,7 +101,7 @@ struct Ns2Cfg {
     static constexpr int CS = (NC + 31) / 32;   // column slots per lane
     static constexpr int QLU_DBL = ns_even(LL * LL + 2 * LL);  // rows of Q1^-1, then two pivot-column buffers
     static constexpr int W_DBL = M * LP;
-    static constexpr int Y_DBL = M * LP;
+    static constexpr int Y_DBL = (M + NR) * LP;  // Y columns, then the pivot residuals (rows M..)
     static constexpr int F_DBL = ns_even(NN * NR + NN);   // node rhs (permuted) + |Q| row sums
     static constexpr int V_DBL = ns_even(3 * LL * NR + M * NR);  // w1p, r_piv, lambda rhs, v
     static constexpr int IDX_DBL = ns_even((NN + 1) / 2);
@@ -117,7 +117,7 @@ struct Ns2Cfg {
 template <int NN, int DEG, int DD, int NF>
 __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
     using Cfg = Ns2Cfg<NN, DEG, DD, NF>;
-    constexpr int LL = Cfg::LL, M = Cfg::M, MP = Cfg::MP, NR = Cfg::NR, RN = Cfg::RN, XN = Cfg::XN,
+    constexpr int LL = Cfg::LL, M = Cfg::M, NR = Cfg::NR, RN = Cfg::RN, XN = Cfg::XN,
                   NP = Cfg::NP, P = Cfg::P, LP = Cfg::LP, NC = Cfg::NC, CS = Cfg::CS;
     extern __shared__ __align__(16) double smem_n2[];
     const int lane = threadIdx.x & 31;
@@ -127,9 +127,9 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
     double* QI = XS + Cfg::XS_DBL;     // row m of Q1^-1 at m*LL; pivot columns (double-buffered) at LL*LL
     double* PV = QI + LL * LL;
     double* Wm = QI + Cfg::QLU_DBL;    // W rows (reduced index c at c*LP)
-    double* Ym = Wm + Cfg::W_DBL;      // Y column c at c*LP
+    double* Ym = Wm + Cfg::W_DBL;      // Y column c at c*LP; r_piv[.][f] at (M + f)*LP
     double* FS = Ym + Cfg::Y_DBL;      // node rhs FS[t*NR + f] (permuted t); |Q| row sums at NN*NR + t
-    double* VS = FS + Cfg::F_DBL;      // w1p[k*NR+f], r_piv at LL*NR, lambda rhs at 2*LL*NR, v at 3*LL*NR
+    double* VS = FS + Cfg::F_DBL;      // w1p[k*NR+f], lambda rhs at 2*LL*NR, v at 3*LL*NR
     int* IDX = reinterpret_cast<int*>(VS + Cfg::V_DBL);  // permuted index -> stencil node
     int* IB = IDX + 2 * Cfg::IDX_DBL;  // staged node indices of the next-but-one stencil, then its row
     const PhsParams& P_ = a.P;
@@ -481,152 +481,136 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 anorm = fmax(anorm, (double)NN * warp_max_nonneg(fmax(qsum[0], qsum[RN - 1])));
             }
 
-            // ---- (4) residuals of the particular solution
-            const bool act = lane < M;
-            const int cc = act ? lane : 0;
+            // ---- (4) Y = Phi12 - Phi11 W^T on the fp64 tensor core, with NR extra
+            //      columns that carry the pivot residuals of the particular solution:
+            //      C-init f(p_k), B column w1p  ->  r_piv[k] = f(p_k) - Phi11[k] w1p
+            constexpr int MR = M + NR;  // columns of [K | b]
             {
-                // residuals r_t = f_t - Phi[t][piv] w1p: pivot rows (lanes k < LL) to VS
-                if (lane < LL) {
-                    double rr[NR];
-#pragma unroll
-                    for (int f = 0; f < NR; ++f) rr[f] = FS[lane * NR + f];
-#pragma unroll
-                    for (int k = 0; k < LL; ++k) {
-                        const double ph = PH[k * P + lane];
-#pragma unroll
-                        for (int f = 0; f < NR; ++f) rr[f] = fma(-ph, VS[k * NR + f], rr[f]);
-                    }
-#pragma unroll
-                    for (int f = 0; f < NR; ++f) VS[LL * NR + lane * NR + f] = rr[f];
-                }
-            }
-            __syncwarp();  // W rows, w1p, r_piv visible
-            // free rows: bb_c = r_c - W_c r_piv  (= Z^T (f - Phi w_p))
-            double bb[NR];
-            {
-                const int t = LL + cc;
-#pragma unroll
-                for (int f = 0; f < NR; ++f) bb[f] = FS[t * NR + f];
-#pragma unroll
-                for (int k = 0; k < LL; ++k) {
-                    const double ph = PH[k * P + t];
-#pragma unroll
-                    for (int f = 0; f < NR; ++f) bb[f] = fma(-ph, VS[k * NR + f], bb[f]);
-                }
-#pragma unroll
-                for (int k = 0; k < LL; ++k) {
-                    const double wk = Wm[cc * LP + k];
-#pragma unroll
-                    for (int f = 0; f < NR; ++f) bb[f] = fma(-wk, VS[LL * NR + k * NR + f], bb[f]);
-                }
-            }
-
-            // ---- (5) Y = Phi12 - Phi11 W^T (l x m) on the fp64 tensor core
-            {
-                constexpr int LT = (LL + 7) / 8, MT = (M + 7) / 8, KS = (LL + 3) / 4;
-                double acc[LT][MT][2];
+                constexpr int LT = (LL + 7) / 8, YT = (MR + 7) / 8, KS = (LL + 3) / 4;
+                double acc[LT][YT][2];
 #pragma unroll
                 for (int lt = 0; lt < LT; ++lt)
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
+                    for (int mt = 0; mt < YT; ++mt)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int k = lt * 8 + g8, c = mt * 8 + 2 * t4 + h;
-                            acc[lt][mt][h] = (k < LL && c < M) ? PH[k * P + LL + c] : 0.0;
+                            double v = 0.0;
+                            if (k < LL && c < M) v = PH[k * P + LL + c];
+                            else if (k < LL && c < MR) v = FS[k * NR + (c - M)];
+                            acc[lt][mt][h] = v;
                         }
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
                     const int k2 = ks * 4 + t4;
-                    double af[LT], bf[MT];
+                    double af[LT], bf[YT];
 #pragma unroll
                     for (int lt = 0; lt < LT; ++lt) {
                         const int k = lt * 8 + g8;
-                        af[lt] = (k2 < LL && k < LL) ? -PH[k * P + k2] : 0.0;
+                        af[lt] = (k2 < LL && k < LL) ? -PH[k2 * P + k] : 0.0;
                     }
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
+                    for (int mt = 0; mt < YT; ++mt) {
                         const int c = mt * 8 + g8;
-                        bf[mt] = (k2 < LL && c < M) ? Wm[c * LP + k2] : 0.0;
+                        double v = 0.0;
+                        if (k2 < LL && c < M) v = Wm[c * LP + k2];
+                        else if (k2 < LL && c < MR) v = VS[k2 * NR + (c - M)];
+                        bf[mt] = v;
                     }
 #pragma unroll
                     for (int lt = 0; lt < LT; ++lt)
 #pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) dmma_f64(acc[lt][mt][0], acc[lt][mt][1], af[lt], bf[mt]);
+                        for (int mt = 0; mt < YT; ++mt) dmma_f64(acc[lt][mt][0], acc[lt][mt][1], af[lt], bf[mt]);
                 }
 #pragma unroll
                 for (int lt = 0; lt < LT; ++lt)
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
+                    for (int mt = 0; mt < YT; ++mt)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int k = lt * 8 + g8, c = mt * 8 + 2 * t4 + h;
-                            if (k < LL && c < M) Ym[c * LP + k] = acc[lt][mt][h];
+                            if (k < LL && c < MR) Ym[c * LP + k] = acc[lt][mt][h];
                         }
             }
-            __syncwarp();  // Y visible
+            __syncwarp();  // Y and r_piv (Y rows M..) visible
 
-            // ---- (6) K = Phi22 - [H W] [W^T; Y] on the fp64 tensor core; row c -> lane c
-            double K[M];
+            // ---- (5) [K | b] = [Phi22 | f_free] - [H W] [W^T w1p; Y r_piv] on the fp64
+            //      tensor core: b = Z^T (f - Phi w_p) comes out as NR extra columns
+            constexpr int RT = (M + 7) / 8, CT = (MR + 7) / 8;
+            static_assert(MR <= 32, "[K | b] must fit 32 columns");
+            double acc[RT][CT][2];
             {
-                constexpr int MT = (M + 7) / 8, KS = (2 * LL + 3) / 4;
-                double acc[MT][MT][2];
+                constexpr int KS = (2 * LL + 3) / 4;
 #pragma unroll
-                for (int rt = 0; rt < MT; ++rt)
+                for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
-                    for (int ct = 0; ct < MT; ++ct)
+                    for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int c = rt * 8 + g8, c2 = ct * 8 + 2 * t4 + h;
-                            acc[rt][ct][h] = (c < M && c2 < M) ? PH[(LL + c) * P + LL + c2] : 0.0;
+                            double v = 0.0;
+                            if (c < M && c2 < M) v = PH[(LL + c) * P + LL + c2];
+                            else if (c < M && c2 < MR) v = FS[(LL + c) * NR + (c2 - M)];
+                            acc[rt][ct][h] = v;
                         }
 #pragma unroll
                 for (int ks = 0; ks < KS; ++ks) {
                     const int kk = ks * 4 + t4;  // < LL: H column kk, else W / Y row kk - LL
                     const bool hp = kk < LL, kv = kk < 2 * LL;
                     const int kh = hp ? kk : 0, kw = hp ? 0 : (kv ? kk - LL : 0);
-                    double af[MT], bf[MT];
+                    double af[RT], bf[CT];
 #pragma unroll
-                    for (int rt = 0; rt < MT; ++rt) {
+                    for (int rt = 0; rt < RT; ++rt) {
                         const int c = rt * 8 + g8;
                         const int cr = c < M ? c : 0;
                         const double v = hp ? PH[(LL + cr) * P + kh] : Wm[cr * LP + kw];
                         af[rt] = (c < M && kv) ? -v : 0.0;
                     }
 #pragma unroll
-                    for (int ct = 0; ct < MT; ++ct) {
+                    for (int ct = 0; ct < CT; ++ct) {
                         const int c2 = ct * 8 + g8;
-                        const int cr = c2 < M ? c2 : 0;
-                        const double v = hp ? Wm[cr * LP + kh] : Ym[cr * LP + kw];
-                        bf[ct] = (c2 < M && kv) ? v : 0.0;
-                    }
-#pragma unroll
-                    for (int rt = 0; rt < MT; ++rt)
-#pragma unroll
-                        for (int ct = 0; ct < MT; ++ct) dmma_f64(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
-                }
-                __syncwarp();  // every read of Phi is done: K takes its place
-#pragma unroll
-                for (int rt = 0; rt < MT; ++rt)
-#pragma unroll
-                    for (int ct = 0; ct < MT; ++ct) {
-                        const int c = rt * 8 + g8, c2 = ct * 8 + 2 * t4;
-                        if (c < M && c2 < M) {
-                            if (c2 + 1 < MP) {
-                                *reinterpret_cast<double2*>(PH + c * MP + c2) = make_double2(acc[rt][ct][0], acc[rt][ct][1]);
-                            } else {
-                                PH[c * MP + c2] = acc[rt][ct][0];
-                            }
+                        double v = 0.0;
+                        if (kv && c2 < MR) {
+                            if (!hp) v = Ym[c2 * LP + kw];
+                            else v = c2 < M ? Wm[c2 * LP + kh] : VS[kh * NR + (c2 - M)];
                         }
+                        bf[ct] = v;
                     }
-                __syncwarp();
 #pragma unroll
-                for (int j = 0; j < M; ++j) K[j] = PH[cc * MP + j];
+                    for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+                        for (int ct = 0; ct < CT; ++ct) dmma_f64(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
+                }
             }
+            __syncwarp();  // every read of Phi is done: the panel buffers take its place
+
+            // ---- (6) [K | b] to one row per lane through shared memory: element (r, c)
+            //      at r * 36 + (c ^ r), which keeps both the accumulator-fragment stores
+            //      and the row reads free of bank conflicts
+            constexpr int KTP = (MR <= 16 && M <= 16) ? 20 : 36;  // 4 mod 16 doubles
+            static_assert(M * KTP <= Cfg::PH_DBL && MR <= 32, "[K | b] staging");
+            const bool act = lane < M;
+            const int cc = act ? lane : 0;
+#pragma unroll
+            for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = rt * 8 + g8, c = ct * 8 + 2 * t4 + h;
+                        if (r < M && c < MR) PH[r * KTP + (c ^ r)] = acc[rt][ct][h];
+                    }
+            __syncwarp();
+            double K[M], bb[NR];
+#pragma unroll
+            for (int j = 0; j < M; ++j) K[j] = PH[cc * KTP + (j ^ cc)];
+#pragma unroll
+            for (int f = 0; f < NR; ++f) bb[f] = PH[cc * KTP + ((M + f) ^ cc)];
             __syncwarp();
 
-            // ---- (7) pivot-free Gauss-Jordan on [K | b]; lane c keeps row c
-            // column k (== row k of the symmetric trailing matrix) is stored with
-            // entry k+1 on a 16-byte boundary, so the pivot row streams in pairs
+            // ---- (7) pivot-free Gauss-Jordan on [K | b]; lane c keeps row c.  Column k
+            //      (== row k of the symmetric trailing matrix) is stored with entry k+1
+            //      on a 16-byte boundary, so the pivot row streams in pairs
             double* Us = PH;
             double* Bs = PH + M * Cfg::UP;
 #pragma unroll
@@ -652,11 +636,13 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                 for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * NR + f], bb[f]);
             }
             // v_c = b_c / d_c with d_c the pivot lane c stored at its step
-            const double d0 = Us[1], dc = Us[cc * Cfg::UP + ((cc + 1) & 1) + cc];
-            const double dinv_own = rcp_c3(dc);
+            {
+                const double d0 = Us[1], dc = Us[cc * Cfg::UP + ((cc + 1) & 1) + cc];
+                const double dinv_own = rcp_c3(dc);
 #pragma unroll
-            for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;
-            bad = bad || !__all_sync(FULL, !act || dc * d0 > 0.0);
+                for (int f = 0; f < NR; ++f) bb[f] *= dinv_own;
+                bad = bad || !__all_sync(FULL, !act || dc * d0 > 0.0);
+            }
 
             // ---- (8) outputs: free weights; pivot weights w1p - W^T v and the
             //      multipliers' right-hand side r_piv - Y v as one tensor-core product
@@ -677,30 +663,30 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             }
             __syncwarp();
             {
-                constexpr int RT = (2 * LL + 7) / 8, CS = (M + 3) / 4;
-                double acc[RT][2];
+                constexpr int R2 = (2 * LL + 7) / 8, CSN = (M + 3) / 4;
+                double oacc[R2][2];
 #pragma unroll
-                for (int rt = 0; rt < RT; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+                for (int rt = 0; rt < R2; ++rt) oacc[rt][0] = oacc[rt][1] = 0.0;
 #pragma unroll
-                for (int cs = 0; cs < CS; ++cs) {
+                for (int cs = 0; cs < CSN; ++cs) {
                     const int c = cs * 4 + t4;
                     const int cr = c < M ? c : 0;
                     const double bv = (c < M && g8 < NR) ? VS[3 * LL * NR + cr * NR + (g8 < NR ? g8 : 0)] : 0.0;
 #pragma unroll
-                    for (int rt = 0; rt < RT; ++rt) {
+                    for (int rt = 0; rt < R2; ++rt) {
                         const int r = rt * 8 + g8;
                         double av = 0.0;
                         if (c < M && r < 2 * LL) av = r < LL ? Wm[cr * LP + r] : Ym[cr * LP + (r - LL)];
-                        dmma_f64(acc[rt][0], acc[rt][1], av, bv);
+                        dmma_f64(oacc[rt][0], oacc[rt][1], av, bv);
                     }
                 }
 #pragma unroll
-                for (int rt = 0; rt < RT; ++rt)
+                for (int rt = 0; rt < R2; ++rt)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int r = rt * 8 + g8, f = 2 * t4 + h;
                         if (f < NR && r < LL) {
-                            const double w = VS[r * NR + f] - acc[rt][h];
+                            const double w = VS[r * NR + f] - oacc[rt][h];
                             if (f < NF) {
                                 bad |= !isfinite(w);
                                 a.out[((size_t)idx * NF + f) * NN + IDX[r]] = w;
@@ -709,7 +695,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                                 zw = fmax(zw, fabs(w));
                             }
                         } else if (f < NF && r >= LL && r < 2 * LL) {
-                            VS[2 * LL * NR + (r - LL) * NR + f] = VS[LL * NR + (r - LL) * NR + f] - acc[rt][h];
+                            VS[2 * LL * NR + (r - LL) * NR + f] = Ym[(M + f) * LP + (r - LL)] - oacc[rt][h];
                         }
                     }
             }
