@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
             double* pc = PV + (k & 1) * LL;  // two buffers: the next step's winner never overwrites a column being read
             if (lane == wl && live) {
 #pragma unroll
-                for (int r = 0; r < LL; ++r) pc[r] = q[0][r];
+                for (int r = 0; r + 1 < LL; r += 2) *reinterpret_cast<double2*>(pc + r) = make_double2(q[0][r], q[0][r + 1]);
+                if (LL & 1) pc[LL - 1] = q[0][LL - 1];
                 live = false;
                 myk = k;
             }
@@ -360,6 +361,11 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
         ok = __all_sync(FULL, ok);
         __syncwarp();
 
+        // constraint rows of ||A||_inf: the constant column sums to n and every other
+        // |monomial| <= 1 under the support scale; otherwise bound them by n * max |Q row|
+        const double qbound = P_.scale_code == MF_SCALE_SUPPORT
+                                  ? (double)NN
+                                  : (double)NN * warp_max_nonneg(fmax(qsum[0], qsum[RN - 1]));
         const double close_thr = a.min_sep2 * rc2max;  // HYBRID: (min separation / radius)^2 threshold
         bool close = false;
         double anorm = 0.0;
@@ -460,27 +466,10 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
         // the coordinates are consumed: stage the next stencil's positions into XS
         stage(idx + stride);
         if (ok) {
-            // ||A||_inf of the saddle-point matrix (estimate only): node rows
-#pragma unroll
-            for (int s = 0; s < RN; ++s) {
-                const int t = lane + 32 * s;
-                if (t < NN) {
-                    // row t == column t (Phi is symmetric): lanes read consecutive words
-                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                    for (int j = 0; j < NN; ++j) acc[j & 3] += fabs(PH[j * P + t]);
-                    anorm = fmax(anorm, ((acc[0] + acc[1]) + (acc[2] + acc[3])) + FS[NN * NR + t]);
-                }
-            }
-            anorm = warp_max_nonneg(anorm);
-            if (P_.scale_code == MF_SCALE_SUPPORT) {
-                // constraint rows: the constant column sums to n, every other |monomial| <= 1
-                anorm = fmax(anorm, (double)NN);
-            } else {
-                // constraint rows sum |Q_im| over the nodes (no scale bound): use the node rows' bound n * max
-                anorm = fmax(anorm, (double)NN * warp_max_nonneg(fmax(qsum[0], qsum[RN - 1])));
-            }
-
+            // ||A||_inf of the saddle-point matrix (estimate only): the node rows of Phi
+            // are summed from the tensor-core operands below (every entry of Phi is
+            // loaded exactly once as a Y / K operand: Phi11, Phi12 in Y; H, Phi22 in K)
+            double rs_y[(LL + 7) / 8] = {}, rs_k[(M + 7) / 8] = {};
             // ---- (4) Y = Phi12 - Phi11 W^T on the fp64 tensor core, with NR extra
             //      columns that carry the pivot residuals of the particular solution:
             //      C-init f(p_k), B column w1p  ->  r_piv[k] = f(p_k) - Phi11[k] w1p
@@ -496,8 +485,12 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                         for (int h = 0; h < 2; ++h) {
                             const int k = lt * 8 + g8, c = mt * 8 + 2 * t4 + h;
                             double v = 0.0;
-                            if (k < LL && c < M) v = PH[k * P + LL + c];
-                            else if (k < LL && c < MR) v = FS[k * NR + (c - M)];
+                            if (k < LL && c < M) {
+                                v = PH[k * P + LL + c];
+                                rs_y[lt] += v;
+                            } else if (k < LL && c < MR) {
+                                v = FS[k * NR + (c - M)];
+                            }
                             acc[lt][mt][h] = v;
                         }
 #pragma unroll
@@ -507,7 +500,9 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
 #pragma unroll
                     for (int lt = 0; lt < LT; ++lt) {
                         const int k = lt * 8 + g8;
-                        af[lt] = (k2 < LL && k < LL) ? -PH[k2 * P + k] : 0.0;
+                        const double v = (k2 < LL && k < LL) ? PH[k2 * P + k] : 0.0;
+                        rs_y[lt] += v;
+                        af[lt] = -v;
                     }
 #pragma unroll
                     for (int mt = 0; mt < YT; ++mt) {
@@ -549,8 +544,12 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                         for (int h = 0; h < 2; ++h) {
                             const int c = rt * 8 + g8, c2 = ct * 8 + 2 * t4 + h;
                             double v = 0.0;
-                            if (c < M && c2 < M) v = PH[(LL + c) * P + LL + c2];
-                            else if (c < M && c2 < MR) v = FS[(LL + c) * NR + (c2 - M)];
+                            if (c < M && c2 < M) {
+                                v = PH[(LL + c) * P + LL + c2];
+                                rs_k[rt] += v;
+                            } else if (c < M && c2 < MR) {
+                                v = FS[(LL + c) * NR + (c2 - M)];
+                            }
                             acc[rt][ct][h] = v;
                         }
 #pragma unroll
@@ -564,6 +563,7 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
                         const int c = rt * 8 + g8;
                         const int cr = c < M ? c : 0;
                         const double v = hp ? PH[(LL + cr) * P + kh] : Wm[cr * LP + kw];
+                        if (hp && c < M) rs_k[rt] += v;
                         af[rt] = (c < M && kv) ? -v : 0.0;
                     }
 #pragma unroll
@@ -581,6 +581,26 @@ __global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
 #pragma unroll
                         for (int ct = 0; ct < CT; ++ct) dmma_f64(acc[rt][ct][0], acc[rt][ct][1], af[rt], bf[ct]);
                 }
+            }
+            {
+                // row sums: each row's entries sit in the four lanes t4 = 0..3 of its g
+#pragma unroll
+                for (int lt = 0; lt < (LL + 7) / 8; ++lt) {
+                    double v = rs_y[lt];
+                    v += __shfl_xor_sync(FULL, v, 1);
+                    v += __shfl_xor_sync(FULL, v, 2);
+                    const int k = lt * 8 + g8;
+                    if (k < LL) anorm = fmax(anorm, v + FS[NN * NR + k]);
+                }
+#pragma unroll
+                for (int rt = 0; rt < RT; ++rt) {
+                    double v = rs_k[rt];
+                    v += __shfl_xor_sync(FULL, v, 1);
+                    v += __shfl_xor_sync(FULL, v, 2);
+                    const int c = rt * 8 + g8;
+                    if (c < M) anorm = fmax(anorm, v + FS[NN * NR + LL + c]);
+                }
+                anorm = fmax(warp_max_nonneg(anorm), qbound);
             }
             __syncwarp();  // every read of Phi is done: the panel buffers take its place
 
