@@ -18,6 +18,8 @@
 //      memory; the cube grows until the K-th key is provably inside it;
 //   4. straddle rows are re-run with the sequential-sum metric (K = n);
 //   5. the self-first rule is applied before the row is written.
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -481,6 +483,224 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
     }
 }
 
+// ---- fast path ------------------------------------------------------------------
+// The common case (d = 2 or 3, K <= 56, one cube of half-width rho around the home
+// cell, at most 32 * SLOTS candidates) with a fixed register layout: candidate c
+// of the cube sits in slot c / 32 of lane c % 32.  The threshold search starts
+// from the previous target's final threshold (targets run in cell order, so the
+// local density barely changes), the survivors are ranked exactly as in the
+// general kernel, and every row the fast path cannot prove (too many candidates,
+// the K-th key outside the cube's inner ball, more than KF_SCAP survivors) goes
+// to a list that the general kernel re-solves from scratch.  Results are the
+// same object either way: the K smallest (d2, node, candidate) keys.
+constexpr int KF_WARPS = 4;
+constexpr int KF_SCAP = 64;  // survivors ranked by the fast path
+
+template <int SLOTS>
+struct FastSmem {
+    int32_t cq[32 * SLOTS];  // sorted-pool position of each candidate
+    KnnKey skey[KF_SCAP];
+    double sd2[KF_SCAP + 2];
+    int32_t srank[KF_SCAP];
+    int32_t slot[KF_SCAP];
+    int32_t sel[KF_SCAP];
+    double seld2[KF_SCAP];
+};
+
+template <int DD, int SLOTS>
+__global__ void __launch_bounds__(KF_WARPS * 32, 4) knn_fast(KnnArgs a, const int32_t* __restrict__ order,
+                                                          int64_t count, int K, int rho, int32_t* __restrict__ fb_list,
+                                                          unsigned long long* __restrict__ fb_count) {
+    extern __shared__ __align__(16) unsigned char kf_smem[];
+    const int lane = threadIdx.x & 31;
+    FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
+    const GridParams g = *a.gp;
+    constexpr int d = DD;
+    const int n = a.n;
+    const int win = min(KF_SCAP - K, 16);
+    // first threshold: the d2 of the (K + win/2)-th neighbour at the nominal grid
+    // density (KNN_OCC points per cell); afterwards the previous target's
+    double cellvol = 1.0;
+    for (int ax = 0; ax < d; ++ax) cellvol *= g.cw[ax];
+    const double cdim = d == 2 ? 3.141592653589793 : 4.1887902047863905;
+    double tguess = pow(((double)K + 0.5 * win) * cellvol / (KNN_OCC * cdim), 2.0 / d);
+
+    for (int64_t w = (int64_t)blockIdx.x * KF_WARPS + (threadIdx.x >> 5); w < count;
+         w += (int64_t)gridDim.x * KF_WARPS) {
+        const int trow = order[w];
+        const int64_t tnode = a.targets[trow];
+        double p[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int ax = 0; ax < d; ++ax) p[ax] = a.pos[tnode * d + ax];
+        int home[3] = {0, 0, 0};
+#pragma unroll
+        for (int ax = 0; ax < d; ++ax) home[ax] = cell_coord(g, ax, p[ax]);
+        const Box b = make_box(g, p, home, rho, d);
+        const int R = box_ranges(b, d);  // <= 32 for the shapes this path is launched on
+        int lo = 0, hi = 0;
+        if (lane < R) range_bounds(g, b, d, lane, a.start, lo, hi);
+        const int len = hi - lo;
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int M = __shfl_sync(FULL, incl, 31);
+        bool fail = M > 32 * SLOTS || M < K;
+        if (!fail) {
+            const int off = incl - len;
+            for (int t = 0; t < len; ++t) sm.cq[off + t] = lo + t;
+        }
+        __syncwarp();
+        double cd[SLOTS];
+        int ci[SLOTS];
+#pragma unroll
+        for (int it = 0; it < SLOTS; ++it) {
+            const int c = it * 32 + lane;
+            cd[it] = INFINITY;
+            ci[it] = 0x7fffffff;
+            if (!fail && c < M) {
+                const int q = sm.cq[c];
+                cd[it] = metric<false>(a.spos + (size_t)q * d, p, d);
+                ci[it] = a.sidx[q];
+            }
+        }
+        auto count_le = [&](double t) {
+            int c = 0;
+#pragma unroll
+            for (int it = 0; it < SLOTS; ++it) c += __popc(__ballot_sync(FULL, cd[it] <= t));
+            return c;
+        };
+        // threshold t with K <= count(d2 <= t) <= K + win
+        double t = tguess, tlo = 0.0, thi = INFINITY;
+        int ct = 0;
+        if (!fail) {
+            int iter = 0;
+            for (; iter < 40; ++iter) {
+                ct = count_le(t);
+                if (ct < K) {
+                    tlo = t;
+                    t = thi < INFINITY ? tlo + 0.5 * (thi - tlo) : t * 1.5;
+                } else if (ct > K + win) {
+                    thi = t;
+                    if (tlo > 0.0) {
+                        t = tlo + 0.5 * (thi - tlo);
+                    } else {
+                        // count ~ t^(d/2): aim at K + win/2
+                        const float x = (float)((double)K + 0.5 * win) / (float)ct;
+                        t = thi * (double)__powf(x, 2.0f / d);
+                    }
+                } else {
+                    break;
+                }
+                if (!(t > tlo && t < thi)) break;  // exhausted the d2 resolution (heavy ties)
+            }
+            fail = ct < K || ct > K + win;
+        }
+        if (!fail) {
+            // aim the next target's first threshold at K + win/2 points
+            const float x = (float)((double)K + 0.5 * win) / (float)ct;
+            tguess = t * (double)__powf(x, 2.0f / d);
+            // compact the survivors as packed keys, in candidate order
+            int base = 0;
+#pragma unroll
+            for (int it = 0; it < SLOTS; ++it) {
+                const bool keep = cd[it] <= t;
+                const unsigned bal = __ballot_sync(FULL, keep);
+                if (keep) {
+                    const int at = base + __popc(bal & ((1u << lane) - 1u));
+                    KnnKey kk;
+                    kk.d2 = cd[it];
+                    kk.ic = ((unsigned long long)(unsigned)ci[it] << 32) | (unsigned)(it * 32 + lane);
+                    sm.skey[at] = kk;
+                    sm.sd2[at] = cd[it];
+                }
+                base += __popc(bal);
+            }
+            const int S = base;
+            if (lane == 0) sm.sd2[S] = INFINITY;  // pad to an even count
+            __syncwarp();
+            // ranks on d2 alone (two survivors per lane, two keys per 16-byte load);
+            // equal d2 values collide in `slot` and fall back to the full key
+            {
+                const int ea = lane, eb = lane + 32;
+                const double da = ea < S ? sm.sd2[ea] : INFINITY;
+                const double db = eb < S ? sm.sd2[eb] : INFINITY;
+                int ra = 0, rb = 0;
+#pragma unroll 4
+                for (int f = 0; f < S; f += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(sm.sd2 + f);
+                    ra += (v.x < da) + (v.y < da);
+                    rb += (v.x < db) + (v.y < db);
+                }
+                if (ea < S) sm.srank[ea] = ra;
+                if (eb < S) sm.srank[eb] = rb;
+            }
+            __syncwarp();
+            for (int e = lane; e < S; e += 32) sm.slot[sm.srank[e]] = e;
+            __syncwarp();
+            bool clash = false;
+            for (int e = lane; e < S; e += 32) clash |= sm.slot[sm.srank[e]] != e;
+            __syncwarp();
+            if (__any_sync(FULL, clash)) {
+                for (int e = lane; e < S; e += 32) {
+                    const KnnKey ke = sm.skey[e];
+                    int r = 0;
+                    for (int f = 0; f < S; ++f) {
+                        const KnnKey kf = sm.skey[f];
+                        r += (kf.d2 < ke.d2) | ((kf.d2 == ke.d2) & (kf.ic < ke.ic));
+                    }
+                    sm.srank[e] = r;
+                }
+                __syncwarp();
+            }
+            for (int e = lane; e < S; e += 32) {
+                const int r = sm.srank[e];
+                if (r < K) {
+                    sm.sel[r] = (int)(sm.skey[e].ic >> 32);
+                    sm.seld2[r] = sm.skey[e].d2;
+                }
+            }
+            __syncwarp();
+            // the K-th key must be provably inside the cube's inner ball
+            const double dK = sm.seld2[K - 1];
+            fail = !b.all && !(dK <= b.limit);
+            if (!fail) {
+                // straddle rows: the (K-1)-th and (n-1)-th keys tie to 1e-12 (stencils.py:61-65)
+                if (K > n) {
+                    const double edge = sm.seld2[n - 1];
+                    if (fabs(dK - edge) <= 1e-18 + 1e-12 * edge && lane == 0) {
+                        const unsigned long long sl = atomicAdd(a.straddle_count, 1ull);
+                        a.straddle_list[sl] = trow;
+                    }
+                }
+                // self-first (stencils.py:77-91)
+                if (a.in_pool[tnode] && sm.sel[0] != (int)tnode) {
+                    int hitv = 0x7fffffff;
+                    for (int j = lane; j < n; j += 32)
+                        if (sm.sel[j] == (int)tnode) hitv = min(hitv, j);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) hitv = min(hitv, __shfl_xor_sync(FULL, hitv, o));
+                    const int last = hitv == 0x7fffffff ? n - 1 : hitv;
+                    if (lane == 0) {
+                        for (int j = last; j > 0; --j) sm.sel[j] = sm.sel[j - 1];
+                        sm.sel[0] = (int)tnode;
+                    }
+                    __syncwarp();
+                }
+                int32_t* row = a.out + (int64_t)trow * n;
+                for (int j = lane; j < n; j += 32) row[j] = sm.sel[j];
+            }
+        }
+        if (fail && lane == 0) {
+            const unsigned long long sl = atomicAdd(fb_count, 1ull);
+            fb_list[sl] = trow;
+        }
+        __syncwarp();
+    }
+}
+
 // ---- grid construction ------------------------------------------------------
 __global__ void knn_bbox(const double* __restrict__ pos, int d, const int64_t* __restrict__ pool, int64_t P,
                          unsigned long long* bb) {
@@ -599,6 +819,8 @@ struct KnnLayout {
     int32_t* tkey[2];
     int32_t* tval[2];
     int32_t* straddle_list;  // T
+    int32_t* fb_list;        // T: rows the fast path hands to the general kernel
+    unsigned long long* fb_count;
     char* cub_tmp;
     size_t cub_bytes;
 };
@@ -631,6 +853,8 @@ inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
         L.tval[i] = ar.take<int32_t>(T);
     }
     L.straddle_list = ar.take<int32_t>(T);
+    L.fb_list = ar.take<int32_t>(T);
+    L.fb_count = ar.take<unsigned long long>(1);
     L.cub_bytes = knn_cub_bytes(P, T);
     L.cub_tmp = ar.take<char>(L.cub_bytes);
     return L;
@@ -672,6 +896,7 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb, 0xff, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb + 3, 0, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.straddle_count, 0, sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.fb_count, 0, sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.cnt, 0, sizeof(int32_t) * (nc + 1), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.in_pool, 0, (size_t)N, st));
     knn_bbox<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.bb);
@@ -705,8 +930,30 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     constexpr int smem_bytes = KNN_WARPS * (int)sizeof(WarpSmem);
     MF_CUDA_CHECK(cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
     MF_CUDA_CHECK(cudaFuncSetAttribute(strd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, smem_bytes, st>>>(a, order, T, nullptr, K);
-    MF_LAUNCH_CHECK();
+    // fast path where it applies (cube of half-width rho0 with <= 32 cell rows),
+    // the general kernel for everything else and for the rows the fast path hands back
+    const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
+    int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
+    if (rho0 < 1) rho0 = 1;
+    const double expect = KNN_OCC * pow(2.0 * rho0 + 1.0, (double)d);
+    static const bool no_fast = [] {
+        const char* e = getenv("MF_KNN_FAST");
+        return e && e[0] == '0';
+    }();
+    const bool fast3 = d == 3 && K <= 56 && 2 * rho0 + 1 <= 5 && expect <= 0.8 * 32 * 10;
+    const bool fast2 = d == 2 && K <= 56 && 2 * rho0 + 1 <= 32 && expect <= 0.8 * 32 * 4;
+    if (!no_fast && (fast3 || fast2)) {
+        auto fk = fast3 ? knn_fast<3, 10> : knn_fast<2, 4>;
+        const int fsm = KF_WARPS * (fast3 ? (int)sizeof(FastSmem<10>) : (int)sizeof(FastSmem<4>));
+        MF_CUDA_CHECK(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+        fk<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, fsm, st>>>(a, order, T, K, rho0, L.fb_list, L.fb_count);
+        MF_LAUNCH_CHECK();
+        main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list, T, L.fb_count, K);
+        MF_LAUNCH_CHECK();
+    } else {
+        main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, smem_bytes, st>>>(a, order, T, nullptr, K);
+        MF_LAUNCH_CHECK();
+    }
     if (K > n) {
         // straddle rows: top-n by the sequential-sum metric (stencils.py:67-75)
         strd_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.straddle_list, T, L.straddle_count,
