@@ -18,6 +18,7 @@
 //      memory; the cube grows until the K-th key is provably inside it;
 //   4. straddle rows are re-run with the sequential-sum metric (K = n);
 //   5. the self-first rule is applied before the row is written.
+#include <cstdio>
 #include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -508,9 +509,9 @@ struct FastSmem {
 };
 
 template <int DD, int SLOTS>
-__global__ void __launch_bounds__(KF_WARPS * 32, 4) knn_fast(KnnArgs a, const int32_t* __restrict__ order,
-                                                          int64_t count, int K, int rho, int32_t* __restrict__ fb_list,
-                                                          unsigned long long* __restrict__ fb_count) {
+__global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 10 ? 4 : 2)
+    knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
+             int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count) {
     extern __shared__ __align__(16) unsigned char kf_smem[];
     const int lane = threadIdx.x & 31;
     FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(KF_WARPS * 32, 4) knn_fast(KnnArgs a, const in
     constexpr int d = DD;
     const int n = a.n;
     const int win = min(KF_SCAP - K, 16);
+    if (count_dev) count = (int64_t)*count_dev;
     // first threshold: the d2 of the (K + win/2)-th neighbour at the nominal grid
     // density (KNN_OCC points per cell); afterwards the previous target's
     double cellvol = 1.0;
@@ -536,22 +538,24 @@ __global__ void __launch_bounds__(KF_WARPS * 32, 4) knn_fast(KnnArgs a, const in
 #pragma unroll
         for (int ax = 0; ax < d; ++ax) home[ax] = cell_coord(g, ax, p[ax]);
         const Box b = make_box(g, p, home, rho, d);
-        const int R = box_ranges(b, d);  // <= 32 for the shapes this path is launched on
-        int lo = 0, hi = 0;
-        if (lane < R) range_bounds(g, b, d, lane, a.start, lo, hi);
-        const int len = hi - lo;
-        int incl = len;
+        const int R = box_ranges(b, d);
+        int M = 0;
+        for (int r0 = 0; r0 < R; r0 += 32) {
+            int lo = 0, hi = 0;
+            if (r0 + lane < R) range_bounds(g, b, d, r0 + lane, a.start, lo, hi);
+            const int len = hi - lo;
+            int incl = len;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int off = M + incl - len;
+            const int lim = min(len, 32 * SLOTS - off);
+            for (int t = 0; t < lim; ++t) sm.cq[off + t] = lo + t;
+            M += __shfl_sync(FULL, incl, 31);
         }
-        const int M = __shfl_sync(FULL, incl, 31);
         bool fail = M > 32 * SLOTS || M < K;
-        if (!fail) {
-            const int off = incl - len;
-            for (int t = 0; t < len; ++t) sm.cq[off + t] = lo + t;
-        }
         __syncwarp();
         double cd[SLOTS];
         int ci[SLOTS];
@@ -819,8 +823,8 @@ struct KnnLayout {
     int32_t* tkey[2];
     int32_t* tval[2];
     int32_t* straddle_list;  // T
-    int32_t* fb_list;        // T: rows the fast path hands to the general kernel
-    unsigned long long* fb_count;
+    int32_t* fb_list[2];     // T each: rows a fast pass hands to the next pass
+    unsigned long long* fb_count;  // 2
     char* cub_tmp;
     size_t cub_bytes;
 };
@@ -853,8 +857,9 @@ inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
         L.tval[i] = ar.take<int32_t>(T);
     }
     L.straddle_list = ar.take<int32_t>(T);
-    L.fb_list = ar.take<int32_t>(T);
-    L.fb_count = ar.take<unsigned long long>(1);
+    L.fb_list[0] = ar.take<int32_t>(T);
+    L.fb_list[1] = ar.take<int32_t>(T);
+    L.fb_count = ar.take<unsigned long long>(2);
     L.cub_bytes = knn_cub_bytes(P, T);
     L.cub_tmp = ar.take<char>(L.cub_bytes);
     return L;
@@ -896,7 +901,7 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb, 0xff, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb + 3, 0, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.straddle_count, 0, sizeof(unsigned long long), st));
-    MF_CUDA_CHECK(cudaMemsetAsync(L.fb_count, 0, sizeof(unsigned long long), st));
+    MF_CUDA_CHECK(cudaMemsetAsync(L.fb_count, 0, 2 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.cnt, 0, sizeof(int32_t) * (nc + 1), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.in_pool, 0, (size_t)N, st));
     knn_bbox<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.bb);
@@ -930,26 +935,44 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     constexpr int smem_bytes = KNN_WARPS * (int)sizeof(WarpSmem);
     MF_CUDA_CHECK(cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
     MF_CUDA_CHECK(cudaFuncSetAttribute(strd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    // fast path where it applies (cube of half-width rho0 with <= 32 cell rows),
-    // the general kernel for everything else and for the rows the fast path hands back
+    // fast passes where they apply: a cube that usually proves the K-th key
+    // (2D: rho0 + 1; 3D: rho0), then the rows it hands back with one more cell of
+    // half-width, then the general kernel for whatever is left
     const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
     int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
-    const double expect = KNN_OCC * pow(2.0 * rho0 + 1.0, (double)d);
     static const bool no_fast = [] {
         const char* e = getenv("MF_KNN_FAST");
         return e && e[0] == '0';
     }();
-    const bool fast3 = d == 3 && K <= 56 && 2 * rho0 + 1 <= 5 && expect <= 0.8 * 32 * 10;
-    const bool fast2 = d == 2 && K <= 56 && 2 * rho0 + 1 <= 32 && expect <= 0.8 * 32 * 4;
-    if (!no_fast && (fast3 || fast2)) {
-        auto fk = fast3 ? knn_fast<3, 10> : knn_fast<2, 4>;
-        const int fsm = KF_WARPS * (fast3 ? (int)sizeof(FastSmem<10>) : (int)sizeof(FastSmem<4>));
-        MF_CUDA_CHECK(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
-        fk<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, fsm, st>>>(a, order, T, K, rho0, L.fb_list, L.fb_count);
+    auto fits = [&](int rho, int slots) {
+        return KNN_OCC * pow(2.0 * rho + 1.0, (double)d) <= 0.8 * 32 * slots;
+    };
+    const int rho1 = d == 2 ? rho0 + 1 : rho0, rho2 = rho1 + 1;
+    const bool fast = !no_fast && K <= 56 &&
+                      ((d == 3 && fits(rho1, 10) && fits(rho2, 28)) || (d == 2 && fits(rho1, 5) && fits(rho2, 8)));
+    if (fast) {
+        auto f1 = d == 3 ? knn_fast<3, 10> : knn_fast<2, 5>;
+        auto f2 = d == 3 ? knn_fast<3, 28> : knn_fast<2, 8>;
+        const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<10>) : (int)sizeof(FastSmem<5>));
+        const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
+        MF_CUDA_CHECK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
+        MF_CUDA_CHECK(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
+        f1<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, sm1, st>>>(a, order, T, nullptr, K, rho1, L.fb_list[0],
+                                                                  L.fb_count);
         MF_LAUNCH_CHECK();
-        main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list, T, L.fb_count, K);
+        f2<<<grid_for(T, KF_WARPS, 4), KF_WARPS * 32, sm2, st>>>(a, L.fb_list[0], T, L.fb_count, K, rho2,
+                                                                 L.fb_list[1], L.fb_count + 1);
         MF_LAUNCH_CHECK();
+        main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list[1], T, L.fb_count + 1, K);
+        MF_LAUNCH_CHECK();
+        if (getenv("MF_KNN_DEBUG")) {
+            unsigned long long nfb[2] = {0, 0};
+            MF_CUDA_CHECK(cudaMemcpyAsync(nfb, L.fb_count, sizeof(nfb), cudaMemcpyDeviceToHost, st));
+            MF_CUDA_CHECK(cudaStreamSynchronize(st));
+            fprintf(stderr, "[mf_knn] rows handed on: %llu (rho %d -> %d), %llu (-> general) of %lld\n", nfb[0], rho1,
+                    rho2, nfb[1], (long long)T);
+        }
     } else {
         main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, smem_bytes, st>>>(a, order, T, nullptr, K);
         MF_LAUNCH_CHECK();
