@@ -501,7 +501,7 @@ template <int SLOTS>
 struct FastSmem {
     int32_t cq[32 * SLOTS];  // sorted-pool position of each candidate
     KnnKey skey[KF_SCAP];
-    double sd2[KF_SCAP + 2];
+    uint32_t sk32[KF_SCAP + 4];  // high words of the survivor d2 (monotone in d2), padded to 4
     int32_t srank[KF_SCAP];
     int32_t slot[KF_SCAP];
     int32_t sel[KF_SCAP];
@@ -511,7 +511,8 @@ struct FastSmem {
 template <int DD, int SLOTS>
 __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 10 ? 4 : 2)
     knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
-             int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count) {
+             int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count,
+             const double* __restrict__ tpos) {
     extern __shared__ __align__(16) unsigned char kf_smem[];
     const int lane = threadIdx.x & 31;
     FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
@@ -527,13 +528,34 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 10 ? 4 : 2)
     const double cdim = d == 2 ? 3.141592653589793 : 4.1887902047863905;
     double tguess = pow(((double)K + 0.5 * win) * cellvol / (KNN_OCC * cdim), 2.0 / d);
 
-    for (int64_t w = (int64_t)blockIdx.x * KF_WARPS + (threadIdx.x >> 5); w < count;
-         w += (int64_t)gridDim.x * KF_WARPS) {
-        const int trow = order[w];
+    // tpos (first pass): target positions gathered in processing order, so the
+    // next target's position is one coalesced load issued a target ahead
+    const int64_t wstride = (int64_t)gridDim.x * KF_WARPS;
+    int64_t w = (int64_t)blockIdx.x * KF_WARPS + (threadIdx.x >> 5);
+    double pn[3] = {0.0, 0.0, 0.0};
+    int trn = 0;
+    auto fetch = [&](int64_t ww) {
+        if (ww < count) {
+            trn = order[ww];
+            if (tpos) {
+#pragma unroll
+                for (int ax = 0; ax < d; ++ax) pn[ax] = tpos[ww * d + ax];
+            }
+        }
+    };
+    fetch(w);
+    for (; w < count; w += wstride) {
+        const int trow = trn;
         const int64_t tnode = a.targets[trow];
         double p[3] = {0.0, 0.0, 0.0};
+        if (tpos) {
 #pragma unroll
-        for (int ax = 0; ax < d; ++ax) p[ax] = a.pos[tnode * d + ax];
+            for (int ax = 0; ax < d; ++ax) p[ax] = pn[ax];
+        } else {
+#pragma unroll
+            for (int ax = 0; ax < d; ++ax) p[ax] = a.pos[tnode * d + ax];
+        }
+        fetch(w + wstride);
         int home[3] = {0, 0, 0};
 #pragma unroll
         for (int ax = 0; ax < d; ++ax) home[ax] = cell_coord(g, ax, p[ax]);
@@ -618,25 +640,26 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 10 ? 4 : 2)
                     kk.d2 = cd[it];
                     kk.ic = ((unsigned long long)(unsigned)ci[it] << 32) | (unsigned)(it * 32 + lane);
                     sm.skey[at] = kk;
-                    sm.sd2[at] = cd[it];
+                    sm.sk32[at] = (uint32_t)((unsigned long long)__double_as_longlong(cd[it]) >> 32);
                 }
                 base += __popc(bal);
             }
             const int S = base;
-            if (lane == 0) sm.sd2[S] = INFINITY;  // pad to an even count
+            if (lane < 4) sm.sk32[S + lane] = 0xffffffffu;  // pad to a multiple of 4
             __syncwarp();
-            // ranks on d2 alone (two survivors per lane, two keys per 16-byte load);
-            // equal d2 values collide in `slot` and fall back to the full key
+            // ranks on the high word of d2 (monotone in d2: four keys per 16-byte load,
+            // two survivors per lane); equal high words collide in `slot` and fall back
+            // to the full key
             {
                 const int ea = lane, eb = lane + 32;
-                const double da = ea < S ? sm.sd2[ea] : INFINITY;
-                const double db = eb < S ? sm.sd2[eb] : INFINITY;
+                const uint32_t da = ea < S ? sm.sk32[ea] : 0xffffffffu;
+                const uint32_t db = eb < S ? sm.sk32[eb] : 0xffffffffu;
                 int ra = 0, rb = 0;
 #pragma unroll 4
-                for (int f = 0; f < S; f += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(sm.sd2 + f);
-                    ra += (v.x < da) + (v.y < da);
-                    rb += (v.x < db) + (v.y < db);
+                for (int f = 0; f < S; f += 4) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(sm.sk32 + f);
+                    ra += (v.x < da) + (v.y < da) + (v.z < da) + (v.w < da);
+                    rb += (v.x < db) + (v.y < db) + (v.z < db) + (v.w < db);
                 }
                 if (ea < S) sm.srank[ea] = ra;
                 if (eb < S) sm.srank[eb] = rb;
@@ -800,6 +823,13 @@ __global__ void knn_target_keys(const double* __restrict__ pos, int d, const int
     }
 }
 
+__global__ void knn_target_gather(const double* __restrict__ pos, int d, const int64_t* __restrict__ targets,
+                                  const int32_t* __restrict__ order, int64_t T, double* __restrict__ tpos) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < T; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t node = targets[order[w]];
+        for (int a = 0; a < d; ++a) tpos[w * d + a] = pos[node * d + a];
+    }
+}
 inline int grid_for(int64_t work, int threads, int per_sm = 8) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -823,6 +853,7 @@ struct KnnLayout {
     int32_t* tkey[2];
     int32_t* tval[2];
     int32_t* straddle_list;  // T
+    double* tpos;            // T * d: target positions in processing (cell) order
     int32_t* fb_list[2];     // T each: rows a fast pass hands to the next pass
     unsigned long long* fb_count;  // 2
     char* cub_tmp;
@@ -857,6 +888,7 @@ inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
         L.tval[i] = ar.take<int32_t>(T);
     }
     L.straddle_list = ar.take<int32_t>(T);
+    L.tpos = ar.take<double>((size_t)T * d);
     L.fb_list[0] = ar.take<int32_t>(T);
     L.fb_list[1] = ar.take<int32_t>(T);
     L.fb_count = ar.take<unsigned long long>(2);
@@ -958,11 +990,13 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
         const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
         MF_CUDA_CHECK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
         MF_CUDA_CHECK(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
+        knn_target_gather<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, order, T, L.tpos);
+        MF_LAUNCH_CHECK();
         f1<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, sm1, st>>>(a, order, T, nullptr, K, rho1, L.fb_list[0],
-                                                                  L.fb_count);
+                                                                  L.fb_count, L.tpos);
         MF_LAUNCH_CHECK();
         f2<<<grid_for(T, KF_WARPS, 4), KF_WARPS * 32, sm2, st>>>(a, L.fb_list[0], T, L.fb_count, K, rho2,
-                                                                 L.fb_list[1], L.fb_count + 1);
+                                                                 L.fb_list[1], L.fb_count + 1, nullptr);
         MF_LAUNCH_CHECK();
         main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list[1], T, L.fb_count + 1, K);
         MF_LAUNCH_CHECK();
