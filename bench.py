@@ -446,7 +446,7 @@ def main():
             "apply_gbs": apply_gbs,
             "roofline": {"bound": "fp64", "kernel": "mf_phs_weights (shape solve)",
                          "achieved": phs_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": phs_tflops / fp64_peak, "traffic": ncu_traffic("phs_ns"),
+                         "frac": phs_tflops / fp64_peak, "traffic": ncu_traffic("phs_ns2"),
                          "note": "F=(2/3)s^3+2rs^2 per stencil (s=45, r=1); peak = DFMA probe measured "
                                  "in this run (MEASURED_PEAKS.json has no fp64 entry)"},
             "apply_roofline": {"bound": "hbm", "kernel": "plan_apply_k (Morton-ordered ELL-32 row sums)",
