@@ -509,7 +509,7 @@ struct FastSmem {
 };
 
 template <int DD, int SLOTS>
-__global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 10 ? 6 : 2)
+__global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ? 6 : 2))
     knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
              int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count,
              const double* __restrict__ tpos) {
