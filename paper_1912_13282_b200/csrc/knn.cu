@@ -508,18 +508,18 @@ struct FastSmem {
     double seld2[KF_SCAP];
 };
 
-template <int DD, int SLOTS>
+template <int DD, int SLOTS, bool TPOS>
 __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ? 6 : 2))
     knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
              int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count,
-             const double* __restrict__ tpos) {
+             const double* __restrict__ tpos, int win_max) {
     extern __shared__ __align__(16) unsigned char kf_smem[];
     const int lane = threadIdx.x & 31;
     FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
     const GridParams g = *a.gp;
     constexpr int d = DD;
     const int n = a.n;
-    const int win = min(KF_SCAP - K, 16);
+    const int win = min(KF_SCAP - K, win_max);
     if (count_dev) count = (int64_t)*count_dev;
     // first threshold: the d2 of the (K + win/2)-th neighbour at the nominal grid
     // density (KNN_OCC points per cell); afterwards the previous target's
@@ -534,10 +534,14 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
     int64_t w = (int64_t)blockIdx.x * KF_WARPS + (threadIdx.x >> 5);
     double pn[3] = {0.0, 0.0, 0.0};
     int trn = 0;
+    int64_t tnn = 0;
+    bool inp = false;
     auto fetch = [&](int64_t ww) {
         if (ww < count) {
             trn = order[ww];
-            if (tpos) {
+            if constexpr (TPOS) {
+                tnn = a.targets[trn];
+                inp = a.in_pool[tnn] != 0;
 #pragma unroll
                 for (int ax = 0; ax < d; ++ax) pn[ax] = tpos[ww * d + ax];
             }
@@ -546,12 +550,17 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
     fetch(w);
     for (; w < count; w += wstride) {
         const int trow = trn;
-        const int64_t tnode = a.targets[trow];
+        int64_t tnode;
+        bool in_pool;
         double p[3] = {0.0, 0.0, 0.0};
-        if (tpos) {
+        if constexpr (TPOS) {
+            tnode = tnn;
+            in_pool = inp;
 #pragma unroll
             for (int ax = 0; ax < d; ++ax) p[ax] = pn[ax];
         } else {
+            tnode = a.targets[trow];
+            in_pool = a.in_pool[tnode] != 0;
 #pragma unroll
             for (int ax = 0; ax < d; ++ax) p[ax] = a.pos[tnode * d + ax];
         }
@@ -703,7 +712,7 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
                     }
                 }
                 // self-first (stencils.py:77-91)
-                if (a.in_pool[tnode] && sm.sel[0] != (int)tnode) {
+                if (in_pool && sm.sel[0] != (int)tnode) {
                     int hitv = 0x7fffffff;
                     for (int j = lane; j < n; j += 32)
                         if (sm.sel[j] == (int)tnode) hitv = min(hitv, j);
@@ -983,9 +992,14 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     const int rho1 = d == 2 ? rho0 + 1 : rho0, rho2 = rho1 + 1;
     const bool fast = !no_fast && K <= 56 &&
                       ((d == 3 && fits(rho1, 10) && fits(rho2, 28)) || (d == 2 && fits(rho1, 5) && fits(rho2, 8)));
+    static const int kf_win = [] {
+        const char* e = getenv("MF_KNN_WIN");
+        const int v = e ? atoi(e) : 16;
+        return v < 4 ? 4 : (v > 32 ? 32 : v);
+    }();
     if (fast) {
-        auto f1 = d == 3 ? knn_fast<3, 10> : knn_fast<2, 5>;
-        auto f2 = d == 3 ? knn_fast<3, 28> : knn_fast<2, 8>;
+        auto f1 = d == 3 ? knn_fast<3, 10, true> : knn_fast<2, 5, true>;
+        auto f2 = d == 3 ? knn_fast<3, 28, false> : knn_fast<2, 8, false>;
         const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<10>) : (int)sizeof(FastSmem<5>));
         const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
         MF_CUDA_CHECK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
@@ -993,10 +1007,10 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
         knn_target_gather<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, order, T, L.tpos);
         MF_LAUNCH_CHECK();
         f1<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, sm1, st>>>(a, order, T, nullptr, K, rho1, L.fb_list[0],
-                                                                  L.fb_count, L.tpos);
+                                                                  L.fb_count, L.tpos, kf_win);
         MF_LAUNCH_CHECK();
         f2<<<grid_for(T, KF_WARPS, 4), KF_WARPS * 32, sm2, st>>>(a, L.fb_list[0], T, L.fb_count, K, rho2,
-                                                                 L.fb_list[1], L.fb_count + 1, nullptr);
+                                                                 L.fb_list[1], L.fb_count + 1, nullptr, 16);
         MF_LAUNCH_CHECK();
         main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list[1], T, L.fb_count + 1, K);
         MF_LAUNCH_CHECK();
