@@ -395,11 +395,14 @@ __host__ __device__ inline NsCtaLayout ns_cta_layout(int n, int d, int l, int nr
     return L;
 }
 
+// NN > 0: sizes fixed at compile time (every index split and loop bound folds);
+// NN = 0: sizes from the call (any shape the launcher accepts)
+template <int NN, int DD, int LL, int NF>
 __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
     extern __shared__ __align__(16) double smem_n[];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const PhsParams& P = a.P;
-    const int n = a.n, d = P.d, l = P.l, nf = P.nf, nrhs = nf + 1;
+    const int n = NN ? NN : a.n, d = NN ? DD : P.d, l = NN ? LL : P.l, nf = NN ? NF : P.nf, nrhs = nf + 1;
     const NsCtaLayout L = ns_cta_layout(n, d, l, nrhs);
     const int M = L.M, RG = L.RG, GP = L.GP, KP = L.KP;
     double* loc = smem_n + L.loc;
@@ -713,15 +716,17 @@ int launch_phs_ns_cta(const PhsArgs& a, cudaStream_t st, int sms) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (bytes > (size_t)max_smem) return MF_ERR_UNSUPPORTED;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(phs_ns_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // the C5 shape (n = 70, degree 4 in 3D, four families) with compile-time sizes
+    auto kern = (n == 70 && l == 35 && a.P.d == 3 && nf == 4) ? phs_ns_cta<70, 3, 35, 4> : phs_ns_cta<0, 0, 0, 0>;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     int per_sm = 0;
-    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phs_ns_cta, CTA_THREADS, bytes));
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CTA_THREADS, bytes));
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = a.m;
     const int64_t cap = (int64_t)sms * per_sm * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    phs_ns_cta<<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a);
+    kern<<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a);
     MF_LAUNCH_CHECK();
     return MF_OK;
 }
