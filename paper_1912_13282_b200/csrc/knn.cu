@@ -147,6 +147,47 @@ __device__ __forceinline__ void range_bounds(const GridParams& g, const Box& b, 
     hi = start[c_hi + 1];
 }
 
+// range r clipped to the ball of squared radius R2 around p (R2 = inf: the whole
+// row): rows whose cells all lie farther than R from p are empty, the others keep
+// the cells along the last axis that the ball reaches.  Monotone cell_coord makes
+// every point within R of p fall in a kept cell (the radius carries a relative
+// margin for the floor in cell_coord).
+__device__ __forceinline__ void range_bounds_ball(const GridParams& g, const Box& b, int d, int r,
+                                                  const int32_t* start, const double* p, double R2, int& lo,
+                                                  int& hi) {
+    int rem = r;
+    int coords[2] = {0, 0};
+    for (int a = d - 2; a >= 0; --a) {
+        const int span = b.chi[a] - b.clo[a] + 1;
+        coords[a] = b.clo[a] + rem % span;
+        rem /= span;
+    }
+    int zl = b.clo[d - 1], zh = b.chi[d - 1];
+    if (R2 < INFINITY) {
+        double t2 = 0.0;
+        for (int a = 0; a < d - 1; ++a) {
+            const double e0 = g.lo[a] + (double)coords[a] * g.cw[a];
+            const double dd = fmax(fmax(e0 - p[a], p[a] - (e0 + g.cw[a])), 0.0);
+            t2 += dd * dd;
+        }
+        if (t2 > R2) {
+            lo = hi = 0;
+            return;
+        }
+        const double h = sqrt(R2 - t2);
+        zl = max(zl, cell_coord(g, d - 1, p[d - 1] - h));
+        zh = min(zh, cell_coord(g, d - 1, p[d - 1] + h));
+        if (zl > zh) {
+            lo = hi = 0;
+            return;
+        }
+    }
+    int lead = 0;
+    for (int a = 0; a < d - 1; ++a) lead = lead * g.G[a] + coords[a];
+    lo = start[lead * g.G[d - 1] + zl];
+    hi = start[lead * g.G[d - 1] + zh + 1];
+}
+
 __device__ __forceinline__ int box_ranges(const Box& b, int d) {
     int R = 1;
     for (int a = 0; a < d - 1; ++a) R *= b.chi[a] - b.clo[a] + 1;
@@ -570,10 +611,12 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
         for (int ax = 0; ax < d; ++ax) home[ax] = cell_coord(g, ax, p[ax]);
         const Box b = make_box(g, p, home, rho, d);
         const int R = box_ranges(b, d);
+        // candidates: the cube's cells that reach the ball the proof covers
+        const double R2 = (d == 2 || b.all) ? INFINITY : b.limit * (1.0 + 1e-6);  // (2D rows are few: no clipping)
         int M = 0;
         for (int r0 = 0; r0 < R; r0 += 32) {
             int lo = 0, hi = 0;
-            if (r0 + lane < R) range_bounds(g, b, d, r0 + lane, a.start, lo, hi);
+            if (r0 + lane < R) range_bounds_ball(g, b, d, r0 + lane, a.start, p, R2, lo, hi);
             const int len = hi - lo;
             int incl = len;
 #pragma unroll
@@ -992,15 +1035,17 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     const int rho1 = d == 2 ? rho0 + 1 : rho0, rho2 = rho1 + 1;
     const bool fast = !no_fast && K <= 56 &&
                       ((d == 3 && fits(rho1, 10) && fits(rho2, 28)) || (d == 2 && fits(rho1, 5) && fits(rho2, 8)));
+    // (the first pass keeps only the cells that reach the proof's ball: ~0.7 of the
+    // cube, so 8 slots hold it in 3D)
     static const int kf_win = [] {
         const char* e = getenv("MF_KNN_WIN");
         const int v = e ? atoi(e) : 16;
         return v < 4 ? 4 : (v > 32 ? 32 : v);
     }();
     if (fast) {
-        auto f1 = d == 3 ? knn_fast<3, 10, true> : knn_fast<2, 5, true>;
+        auto f1 = d == 3 ? knn_fast<3, 8, true> : knn_fast<2, 5, true>;
         auto f2 = d == 3 ? knn_fast<3, 28, false> : knn_fast<2, 8, false>;
-        const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<10>) : (int)sizeof(FastSmem<5>));
+        const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<8>) : (int)sizeof(FastSmem<5>));
         const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
         MF_CUDA_CHECK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
         MF_CUDA_CHECK(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
