@@ -100,6 +100,94 @@ __global__ void __launch_bounds__(256) csr_fill_smem(const int64_t* __restrict__
     }
 }
 
+// Thread per row, rows staged through shared memory: a warp loads the keys
+// column*64 + slot of its 32 rows with coalesced loads, each lane sorts its row
+// in registers with a Batcher odd-even merge network over 64 positions pruned at
+// compile time for the NR real inputs (positions >= NR hold +inf: comparators
+// between two infs are dropped, one whose low input is inf is a register
+// rename, one whose high input is inf a no-op), writes the sorted row back, and
+// the warp stores the rows with coalesced writes.  The keys are unique, so the
+// order is the stable (column, slot) lexsort of csr_fill.
+template <int NR>
+struct SortNet {
+    int c[700][2];
+    int nc;
+    int out[64];
+    constexpr SortNet() : c{}, nc(0), out{} {
+        int map[64] = {};
+        bool inf[64] = {};
+        for (int i = 0; i < 64; ++i) {
+            map[i] = i;
+            inf[i] = i >= NR;
+        }
+        for (int p = 1; p < 64; p <<= 1)
+            for (int k = p; k >= 1; k >>= 1)
+                for (int j = k % p; j + k < 64; j += 2 * k)
+                    for (int i = 0; i < k && i + j + k < 64; ++i)
+                        if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+                            const int a = i + j, b = i + j + k;
+                            if (inf[b]) continue;  // (both inf, or only the high one: no-op)
+                            if (inf[a]) {          // low input inf: the values swap places
+                                const int t = map[a];
+                                map[a] = map[b];
+                                map[b] = t;
+                                inf[a] = false;
+                                inf[b] = true;
+                                continue;
+                            }
+                            c[nc][0] = map[a];
+                            c[nc][1] = map[b];
+                            ++nc;
+                        }
+        for (int i = 0; i < 64; ++i) out[i] = map[i];
+    }
+};
+
+template <int NR>
+__global__ void __launch_bounds__(256, 4) csr_fill_net(const int64_t* __restrict__ rows, const int32_t* __restrict__ st,
+                                                       int64_t m, const int32_t* __restrict__ indptr,
+                                                       int32_t* __restrict__ indices, int32_t* __restrict__ perm) {
+    constexpr int PITCH = NR | 1;  // odd: lane-per-row accesses hit distinct banks
+    constexpr SortNet<NR> net{};
+    __shared__ int32_t sk[8][32 * PITCH];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int32_t* k = sk[wib];
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + wib) * 32; r0 < m; r0 += (int64_t)gridDim.x * 8 * 32) {
+        const int nr = (int)(m - r0 < 32 ? m - r0 : 32);
+        // coalesced staging of the tile's keys (rows are contiguous in `st`)
+        for (int e = lane; e < nr * NR; e += 32) {
+            const int rr = e / NR, j = e - rr * NR;
+            k[rr * PITCH + j] = (st[r0 * NR + e] << 6) | j;
+        }
+        __syncwarp();
+        if (lane < nr) {
+            int key[NR];
+#pragma unroll
+            for (int j = 0; j < NR; ++j) key[j] = k[lane * PITCH + j];
+#pragma unroll
+            for (int t = 0; t < net.nc; ++t) {
+                const int a = net.c[t][0], b = net.c[t][1];
+                const int lo = min(key[a], key[b]), hi = max(key[a], key[b]);
+                key[a] = lo;
+                key[b] = hi;
+            }
+#pragma unroll
+            for (int q = 0; q < NR; ++q) k[lane * PITCH + q] = key[net.out[q]];
+        }
+        __syncwarp();
+        for (int rr = 0; rr < nr; ++rr) {
+            const int64_t r = r0 + rr;
+            const int64_t base = indptr[rows[r]];
+            for (int q = lane; q < NR; q += 32) {
+                const int kk = k[rr * PITCH + q];
+                indices[base + q] = kk >> 6;
+                perm[base + q] = (int32_t)(r * NR + (kk & 63));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void csr_gather_k(const int32_t* __restrict__ perm, const double* __restrict__ w, int64_t nnz,
                              double* __restrict__ data) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
@@ -357,7 +445,10 @@ extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_
     MF_LAUNCH_CHECK();
     MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, indptr, (int)(N + 1), st));
     if (m > 0) {
-        if (N < (1 << 25) && n <= 64) {
+        if (N < (1 << 25) && (n == 15 || n == 25 || n == 35)) {
+            auto k = n == 15 ? csr_fill_net<15> : (n == 25 ? csr_fill_net<25> : csr_fill_net<35>);
+            k<<<grid_for((m + 255) / 256 * 256, 256, 16), 256, 0, st>>>(rows, stencils, m, indptr, indices, perm);
+        } else if (N < (1 << 25) && n <= 64) {
             const int smem = CSR_ROWS * ((n + 3) & ~3) * (int)sizeof(int32_t);
             csr_fill_smem<<<grid_for((m + CSR_ROWS - 1) / CSR_ROWS, 1, 8), 256, smem, st>>>(rows, stencils, m, n,
                                                                                          indptr, indices, perm);
