@@ -143,6 +143,31 @@ def workspace(nbytes: int) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device())
 
 
+_COPY_STREAM = None
+
+
+def to_device_async(a, dtype):
+    """Host array -> (device tensor, event): the copy runs on a side stream (async
+    from pinned memory) so the caller can enqueue independent work meanwhile; the
+    current stream must wait on the event before using the tensor."""
+    global _COPY_STREAM
+    if _COPY_STREAM is None:
+        _COPY_STREAM = torch.cuda.Stream(device=device())
+    arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    main = torch.cuda.current_stream(device())
+    with torch.cuda.stream(_COPY_STREAM):
+        d = t.to(device(), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(_COPY_STREAM)
+    d.record_stream(main)
+    return d, ev
+
+
 def to_device(a, dtype) -> torch.Tensor:
     """Host array or tensor -> contiguous device tensor of `dtype`."""
     if isinstance(a, torch.Tensor):

@@ -500,7 +500,19 @@ class WeightStore:
 
     def apply_all(self, key: str, field):
         """(L u) at every stored node as a length-N vector (zeros elsewhere)."""
-        return self.matrix(key) @ field
+        if isinstance(field, torch.Tensor) and field.is_cuda:
+            return self.matrix(key) @ field
+        arr = np.asarray(field, dtype=float)
+        if arr.shape != (self.n_nodes,):
+            arr = np.broadcast_to(arr, (self.n_nodes,))
+        # the field's host-to-device copy overlaps the CSR and apply-plan builds
+        u_d, ready = _lib.to_device_async(arr, torch.float64)
+        mat = self.matrix(key)
+        mat.plan(True)
+        torch.cuda.current_stream(u_d.device).wait_event(ready)
+        y = mat.apply_device(u_d)
+        mat._s.check()
+        return _to_host(y)
 
     def gradient(self, field, i: int):
         d = self._dim()
