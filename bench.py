@@ -454,6 +454,12 @@ def main():
                                "kernel_ms": ell_ms, "stage_gbs_incl_permutes": apply_gbs,
                                "traffic": ncu_traffic("plan_apply_k"), "bytes_per_launch": b_apply,
                                "note": "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"},
+            "knn_roofline": {"bound": "latency/issue (reported against HBM)", "kernel": "mf_knn (fast passes + fallback)",
+                             "achieved": (N * 3 * 8 + N * n * 4) / (knn_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                             "unit": "GB/s", "frac": (N * 3 * 8 + N * n * 4) / (knn_ms * 1e-3) / 1e9 / hbm_peak,
+                             "traffic": ncu_traffic("knn_fast"),
+                             "note": "B_knn = N*d*8 + T*n*4 (SURVEY 8d); the search is bound by dependent "
+                                     "loads and issue, not by these bytes"},
             "replayed_stencils": n_replayed,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
