@@ -9,9 +9,13 @@
 // REPLAY follows _solve_multi (_phs_batch.py:142-184) op for op; FAST uses FMA
 // and carries the +-1 probe right-hand side for the HYBRID criterion, exactly
 // as the warp kernels do.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "phs_params.cuh"
 #include "phs_reg.cuh"  // fast_rcp, fast_rsqrt
+#include "phs_ns.cuh"   // dmma_f64, monomials_reg
 
 namespace mf {
 
@@ -705,11 +709,515 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Nullspace pass for one large stencil shape with compile-time sizes (the C5
+// shape: n = 70, degree 4 in 3D, 35 monomials, four families), same mathematics
+// as phs_ns_cta with the data held where the work is:
+//   * the Gauss-Jordan sweep over [Q; g] keeps every element in a register of
+//     the thread that owns its column (rows strided over the row groups); per
+//     step only the pivot row and the pivot column go through shared memory
+//     (double-buffered: two barriers per step, no read-modify-write of the
+//     matrix in shared memory);
+//   * Y = Phi12 - Phi11 W^T and [K | b] = [Phi22 | f] - [H W][W^T w1p; Y r_piv]
+//     are tensor-core products (mma.sync.m8n8k4.f64), 8 x 8 tiles spread over
+//     the warps, the particular solution's residuals riding as extra columns;
+//   * the pivot-free Gauss-Jordan on [K | b] is register-resident the same way.
+// ---------------------------------------------------------------------------
+template <int NN, int DD, int DEG, int NF>
+struct Cta2Cfg {
+    static constexpr int LL = binom(DEG + DD, DD);
+    static constexpr int M = NN - LL;
+    static constexpr int NR = NF + 1;        // families + probe
+    static constexpr int MR = M + NR;        // columns of [K | b]
+    static constexpr int RG = NN + NR;       // rows of [Q; g]
+    static constexpr int EP = NN | 1;        // Phi pitch (odd: column sweeps hit distinct banks)
+    static constexpr int GP = LL | 1;        // [Q; g] pitch
+    static constexpr int YP = ((LL + 3) / 8) * 8 + 4;  // Y column pitch, 4 mod 8 (conflict-free fragments)
+    static constexpr int KP = MR | 1;
+    // register-resident sweeps: thread = (column, row group)
+    static constexpr int QG = CTA_THREADS / LL;          // row groups of the [Q; g] sweep
+    static constexpr int QI = (RG + QG - 1) / QG;        // rows per thread
+    static constexpr int KG = CTA_THREADS / MR;          // row groups of the [K | b] sweep
+    static constexpr int KI = (M + KG - 1) / KG;
+    static constexpr int RT = (LL + 7) / 8, CT = (MR + 7) / 8, MT = (M + 7) / 8;
+    // shared layout (doubles)
+    static constexpr int LOC = 0;
+    static constexpr int E = LOC + ((NN * DD + 1) & ~1);
+    static constexpr int G = E + ((NN * EP + 1) & ~1);
+    static constexpr int F = G + ((RG * GP + 1) & ~1);
+    static constexpr int Y = F + NN * NR;
+    static constexpr int K = Y + ((MR * YP + 1) & ~1);
+    static constexpr int OPS = K + ((M * KP + 1) & ~1);  // pivot rows per step, then 1 / pivot
+    static constexpr int V = OPS + ((LL * GP + LL + 1) & ~1);
+    static constexpr int PROW = V + M * NR;              // 2 x 64
+    static constexpr int COLK = PROW + 128;              // 2 x 80
+    static constexpr int RED = COLK + 160;               // reductions / candidates
+    static constexpr int INTS = RED + 4 * CTA_WARPS + 16;  // isp[NN], piv[LL], nonpiv[M] (ints)
+    static constexpr int TOTAL = INTS + (NN + LL + M + 16) / 2 + 2;
+    static_assert(QG * LL <= CTA_THREADS && KG * MR <= CTA_THREADS, "sweep layouts");
+    static_assert(MR <= 64 && RG <= 80 && M <= 80, "pivot buffers");
+};
+
+template <int NN, int DD, int DEG, int NF>
+__global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
+    using C = Cta2Cfg<NN, DD, DEG, NF>;
+    constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, EP = C::EP, GP = C::GP, YP = C::YP,
+                  KP = C::KP, QG = C::QG, QI = C::QI, KG = C::KG, KI = C::KI;
+    extern __shared__ __align__(16) double sm2[];
+    double* loc = sm2 + C::LOC;
+    double* E = sm2 + C::E;
+    double* G = sm2 + C::G;
+    double* F = sm2 + C::F;
+    double* Y = sm2 + C::Y;
+    double* K = sm2 + C::K;
+    double* ops = sm2 + C::OPS;
+    double* invs = ops + LL * GP;
+    double* V = sm2 + C::V;
+    double* prow = sm2 + C::PROW;
+    double* colk = sm2 + C::COLK;
+    double* red = sm2 + C::RED;
+    int* redi = reinterpret_cast<int*>(red + 2 * CTA_WARPS);
+    int* isp = reinterpret_cast<int*>(sm2 + C::INTS);
+    int* piv = isp + NN;
+    int* nonpiv = piv + LL;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const PhsParams& P = a.P;
+
+    for (int64_t idx = blockIdx.x; idx < a.m; idx += gridDim.x) {
+        const int64_t row = a.rows[idx];
+        const int32_t* sti = a.stencils + idx * NN;
+        // ---- local coordinates, scale, family factors
+        for (int e = tid; e < NN * DD; e += CTA_THREADS) {
+            const int j = e / DD, ax = e - j * DD;
+            loc[e] = a.pos[(int64_t)sti[j] * DD + ax] - a.pos[row * DD + ax];
+        }
+        for (int i = tid; i < NN; i += CTA_THREADS) isp[i] = 0;
+        __syncthreads();
+        int stat = 0;
+        double sc = 1.0;
+        if (P.scale_code != MF_SCALE_NONE) {
+            const bool nearest = P.scale_code == MF_SCALE_NEAREST;
+            double best = nearest ? INFINITY : -1.0;
+            for (int j = tid; j < NN; j += CTA_THREADS) {
+                double r2 = 0.0;
+                for (int ax = 0; ax < DD; ++ax) r2 = __dadd_rn(r2, __dmul_rn(loc[j * DD + ax], loc[j * DD + ax]));
+                if (nearest) {
+                    if (r2 > 0.0 && r2 < best) best = r2;
+                } else if (r2 > best) {
+                    best = r2;
+                }
+            }
+            best = nearest ? block_reduce_min(best, red) : block_reduce_max(best, red);
+            if (nearest ? (best == INFINITY) : !(best > 0.0)) stat = 2;
+            else sc = __dsqrt_rn(best);
+        }
+        double facs[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) facs[f] = pow_cr_int(sc, -P.orders[f]);
+        const double rs = fast_rcp(sc);
+        for (int e = tid; e < NN * DD; e += CTA_THREADS) loc[e] *= rs;
+        __syncthreads();
+
+        // ---- Phi (zero diagonal), [Q; g], node right-hand sides, ||A||_inf
+        double r2min = INFINITY, rc2max = 0.0;
+        for (int e = tid; e < NN * NN; e += CTA_THREADS) {
+            const int i = e / NN, j = e - i * NN;
+            if (j < i) continue;
+            double v = 0.0;
+            if (j > i) {
+                double df = loc[i * DD] - loc[j * DD];
+                double r2 = df * df;
+#pragma unroll
+                for (int ax = 1; ax < DD; ++ax) {
+                    df = loc[i * DD + ax] - loc[j * DD + ax];
+                    r2 = fma(df, df, r2);
+                }
+                r2min = r2 < r2min ? r2 : r2min;
+                v = r2 * (r2 * fast_rsqrt(fmax(r2, 1e-300)));
+            }
+            E[i * EP + j] = v;
+            E[j * EP + i] = v;
+        }
+        for (int i = tid; i < NN; i += CTA_THREADS) {
+            double x[DD], q[LL];
+#pragma unroll
+            for (int ax = 0; ax < DD; ++ax) x[ax] = loc[i * DD + ax];
+            monomials_reg<DD, DEG, 0, LL>(q, x);
+#pragma unroll
+            for (int m = 0; m < LL; ++m) G[i * GP + m] = q[m];
+            double top[MF_MAX_FAMILIES];
+            phs_rhs_top_k3(x, DD, P, top);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) F[i * NR + f] = __dmul_rn(top[f], facs[f]);
+            F[i * NR + NF] = probe_sign(idx, i);
+            double rc2 = 0.0;
+#pragma unroll
+            for (int ax = 0; ax < DD; ++ax) rc2 = fma(x[ax], x[ax], rc2);
+            rc2max = fmax(rc2max, rc2);
+        }
+        for (int e = tid; e < NR * LL; e += CTA_THREADS) {
+            const int f = e / LL, m = e - f * LL;
+            G[(NN + f) * GP + m] = f < NF ? __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + m], facs[f]) : probe_sign(idx, NN + m);
+        }
+        __syncthreads();
+        r2min = block_reduce_min(r2min, red);
+        rc2max = block_reduce_max(rc2max, red);
+        double anorm = 0.0;
+        for (int r = tid; r < NN + LL; r += CTA_THREADS) {
+            double acc = 0.0;
+            if (r < NN) {
+                for (int j = 0; j < NN; ++j) acc += E[j * EP + r];  // column r == row r, r^3 >= 0
+                for (int m = 0; m < LL; ++m) acc += fabs(G[r * GP + m]);
+            } else {
+                for (int i = 0; i < NN; ++i) acc += fabs(G[i * GP + (r - NN)]);
+            }
+            anorm = fmax(anorm, acc);
+        }
+        anorm = block_reduce_max(anorm, red);
+
+        // ---- Gauss-Jordan column sweep of [Q; g] with node pivoting, register-resident:
+        //      thread (jj = tid % LL, rg = tid / LL) owns rows rg, rg + QG, ... of column jj
+        bool ok = stat == 0;
+        const int qjj = tid % LL, qrg = tid / LL;
+        const bool qact = qrg < QG;
+        double gq[QI];
+#pragma unroll
+        for (int i = 0; i < QI; ++i) {
+            const int r = qrg + QG * i;
+            gq[i] = (qact && r < RG) ? G[r * GP + qjj] : 0.0;
+        }
+        for (int k = 0; k < LL && ok; ++k) {
+            double* pr_buf = prow + (k & 1) * 64;
+            double* ck_buf = colk + (k & 1) * 80;
+            // pivot candidates: the row groups of column k
+            if (qact && qjj == k) {
+                double best = -1.0;
+                int bp = 0x7fffffff;
+#pragma unroll
+                for (int i = 0; i < QI; ++i) {
+                    const int r = qrg + QG * i;
+                    if (r < NN && !isp[r]) {
+                        const double v = fabs(gq[i]);
+                        if (v > best) {
+                            best = v;
+                            bp = r;
+                        }
+                    }
+                }
+                red[qrg] = best;
+                redi[qrg] = bp;
+            }
+            __syncthreads();
+            double best = -1.0;
+            int pr = 0x7fffffff;
+#pragma unroll
+            for (int q = 0; q < QG; ++q) {
+                const double v = red[q];
+                const int p = redi[q];
+                if (v > best || (v == best && p < pr)) {
+                    best = v;
+                    pr = p;
+                }
+            }
+            if (!(best > 0.0) || !isfinite(best) || pr == 0x7fffffff) {
+                ok = false;  // uniform: every thread read the same candidates
+                break;
+            }
+            // stage the pivot row (its owners) and column k (unscaled)
+            if (qact) {
+                if (qrg == pr % QG) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int i = 0; i < QI; ++i)
+                        if (qrg + QG * i == pr) v = gq[i];
+                    pr_buf[qjj] = v;
+                    ops[k * GP + qjj] = v;
+                }
+                if (qjj == k) {
+#pragma unroll
+                    for (int i = 0; i < QI; ++i) {
+                        const int r = qrg + QG * i;
+                        if (r < RG) ck_buf[r] = gq[i];
+                    }
+                }
+            }
+            if (tid == 0) {
+                isp[pr] = 1;
+                piv[k] = pr;
+            }
+            __syncthreads();
+            const double inv = fast_rcp(pr_buf[k]);
+            if (tid == 0) invs[k] = inv;
+            if (qact) {
+                const double pj = pr_buf[qjj];
+#pragma unroll
+                for (int i = 0; i < QI; ++i) {
+                    const int r = qrg + QG * i;
+                    if (r < RG) {
+                        const double cr = ck_buf[r] * inv;
+                        gq[i] = qjj == k ? cr : fma(-pj, cr, gq[i]);
+                    }
+                }
+            }
+        }
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < QI; ++i) {
+                const int r = qrg + QG * i;
+                if (qact && r < RG) G[r * GP + qjj] = gq[i];
+            }
+        }
+        __syncthreads();
+        // free (non-pivot) nodes in node order
+        if (ok && w == 0) {
+            int base = 0;
+            for (int c0 = 0; c0 < NN; c0 += 32) {
+                const int i = c0 + lane;
+                const bool fr = i < NN && !isp[i];
+                const unsigned bal = __ballot_sync(FULL, fr);
+                const int at = base + __popc(bal & ((1u << lane) - 1u));
+                if (fr && at < M) nonpiv[at] = i;
+                base += __popc(bal);
+            }
+            if (lane == 0) redi[CTA_WARPS] = base;
+        }
+        __syncthreads();
+        ok = ok && redi[CTA_WARPS] == M;
+
+        bool definite = true;
+        if (ok) {
+            // ---- Y (l x [M | NR]) on the tensor cores: tiles over the warps
+            for (int tt = w; tt < C::RT * C::CT; tt += CTA_WARPS) {
+                const int lt = tt / C::CT, mt = tt - lt * C::CT;
+                const int kr = lt * 8 + g8;
+                const int pk = piv[kr < LL ? kr : 0];
+                double acc[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = mt * 8 + 2 * t4 + h;
+                    double v = 0.0;
+                    if (kr < LL && c < M) v = E[pk * EP + nonpiv[c]];
+                    else if (kr < LL && c < MR) v = F[pk * NR + (c - M)];
+                    acc[h] = v;
+                }
+                const int cb = mt * 8 + g8;
+                const int grow = cb < M ? nonpiv[cb] : (cb < MR ? NN + (cb - M) : 0);
+#pragma unroll
+                for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
+                    const int k2 = ks * 4 + t4;
+                    const double av = (k2 < LL && kr < LL) ? -E[pk * EP + piv[k2 < LL ? k2 : 0]] : 0.0;
+                    const double bv = (k2 < LL && cb < MR) ? G[grow * GP + k2] : 0.0;
+                    dmma_f64(acc[0], acc[1], av, bv);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = mt * 8 + 2 * t4 + h;
+                    if (kr < LL && c < MR) Y[c * YP + kr] = acc[h];
+                }
+            }
+            __syncthreads();
+            // ---- [K | b] on the tensor cores
+            for (int tt = w; tt < C::MT * C::CT; tt += CTA_WARPS) {
+                const int rt = tt / C::CT, ct = tt - rt * C::CT;
+                const int c = rt * 8 + g8;
+                const int qc = nonpiv[c < M ? c : 0];
+                double acc[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c2 = ct * 8 + 2 * t4 + h;
+                    double v = 0.0;
+                    if (c < M && c2 < M) v = E[qc * EP + nonpiv[c2]];
+                    else if (c < M && c2 < MR) v = F[qc * NR + (c2 - M)];
+                    acc[h] = v;
+                }
+                const int cb = ct * 8 + g8;
+                const int grow = cb < M ? nonpiv[cb] : (cb < MR ? NN + (cb - M) : 0);
+#pragma unroll 6
+                for (int ks = 0; ks < (2 * LL + 3) / 4; ++ks) {
+                    const int kk = ks * 4 + t4;
+                    const bool hp = kk < LL, kv = kk < 2 * LL;
+                    const int kh = hp ? kk : 0, kw = hp ? 0 : (kv ? kk - LL : 0);
+                    double av = 0.0, bv = 0.0;
+                    if (c < M && kv) av = -(hp ? E[qc * EP + piv[kh]] : G[qc * GP + kw]);
+                    if (cb < MR && kv) bv = hp ? G[grow * GP + kh] : Y[cb * YP + kw];
+                    dmma_f64(acc[0], acc[1], av, bv);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c2 = ct * 8 + 2 * t4 + h;
+                    if (c < M && c2 < MR) K[c * KP + c2] = acc[h];
+                }
+            }
+            __syncthreads();
+            // ---- pivot-free Gauss-Jordan on [K | b], register-resident:
+            //      thread (jj = tid % MR, rg = tid / MR) owns rows rg, rg + KG, ...
+            const int kjj = tid % MR, krg = tid / MR;
+            const bool kact = krg < KG;
+            double kv[KI];
+#pragma unroll
+            for (int i = 0; i < KI; ++i) {
+                const int r = krg + KG * i;
+                kv[i] = (kact && r < M) ? K[r * KP + kjj] : 0.0;
+            }
+            const double d0 = K[0];
+            for (int k = 0; k < M; ++k) {
+                double* pr_buf = prow + (k & 1) * 64;
+                double* ck_buf = colk + (k & 1) * 80;
+                if (kact) {
+                    if (krg == k % KG) {
+                        double v = 0.0;
+#pragma unroll
+                        for (int i = 0; i < KI; ++i)
+                            if (krg + KG * i == k) v = kv[i];
+                        pr_buf[kjj] = v;
+                    }
+                    if (kjj == k) {
+#pragma unroll
+                        for (int i = 0; i < KI; ++i) {
+                            const int r = krg + KG * i;
+                            if (r < M) ck_buf[r] = kv[i];
+                        }
+                    }
+                }
+                __syncthreads();
+                const double dk = pr_buf[k];
+                definite = definite && dk * d0 > 0.0;
+                const double inv = fast_rcp(dk);
+                if (kact && kjj > k) {
+                    const double pj = pr_buf[kjj];
+#pragma unroll
+                    for (int i = 0; i < KI; ++i) {
+                        const int r = krg + KG * i;
+                        if (r < M) kv[i] = r == k ? pj * inv : fma(-ck_buf[r] * inv, pj, kv[i]);
+                    }
+                }
+            }
+            // the solution columns
+            if (kact && kjj >= M) {
+#pragma unroll
+                for (int i = 0; i < KI; ++i) {
+                    const int r = krg + KG * i;
+                    if (r < M) V[r * NR + (kjj - M)] = kv[i];
+                }
+            }
+            __syncthreads();
+        }
+        ok = ok && definite;
+
+        // ---- outputs: free weights v, pivot weights w1p - W^T v; estimate
+        bool bad = !ok;
+        double zw = 0.0, xw[NF], la[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) xw[f] = la[f] = 0.0;
+        if (ok) {
+            for (int e = tid; e < M * NR; e += CTA_THREADS) {
+                const int c = e / NR, f = e - c * NR;
+                const double v = V[e];
+                if (f < NF) {
+                    bad |= !isfinite(v);
+                    a.out[((size_t)idx * NF + f) * NN + nonpiv[c]] = v;
+                    xw[f] = fmax(xw[f], fabs(v));
+                } else {
+                    zw = fmax(zw, fabs(v));
+                }
+            }
+            for (int e = tid; e < LL * NR; e += CTA_THREADS) {
+                const int k = e / NR, f = e - k * NR;
+                double wv = G[(NN + f) * GP + k];
+                for (int c = 0; c < M; ++c) wv = fma(-G[nonpiv[c] * GP + k], V[c * NR + f], wv);
+                if (f < NF) {
+                    bad |= !isfinite(wv);
+                    a.out[((size_t)idx * NF + f) * NN + piv[k]] = wv;
+                    xw[f] = fmax(xw[f], fabs(wv));
+                } else {
+                    zw = fmax(zw, fabs(wv));
+                }
+            }
+            // lambda_f = Q1^-1 (r_piv - Y v): the recorded column operations, last first
+            for (int e = tid; e < LL * NF; e += CTA_THREADS) {
+                const int k = e / NF, f = e - k * NF;
+                double sv = Y[(M + f) * YP + k];
+                for (int c = 0; c < M; ++c) sv = fma(-Y[c * YP + k], V[c * NR + f], sv);
+                colk[k * NF + f] = sv;
+            }
+            __syncthreads();
+            for (int f = w; f < NF; f += CTA_WARPS) {
+                for (int k = LL - 1; k >= 0; --k) {
+                    double part = 0.0;
+                    for (int j = lane; j < LL; j += 32)
+                        if (j != k) part = fma(ops[k * GP + j], colk[j * NF + f], part);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+                    if (lane == 0) colk[k * NF + f] = invs[k] * (colk[k * NF + f] - part);
+                    __syncwarp();
+                }
+                double mx = 0.0;
+                for (int j = lane; j < LL; j += 32) mx = fmax(mx, fabs(colk[j * NF + f]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+                la[f] = mx;
+            }
+        }
+        bad = __syncthreads_or(bad) != 0;
+        if (bad && stat == 0) stat = 1;
+        zw = block_reduce_max(zw, red);
+        double ratio = 0.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const double xwf = block_reduce_max(xw[f], red);
+            const double laf = block_reduce_max(la[f], red);
+            ratio = fmax(ratio, fmax(xwf, laf) / xwf);
+        }
+        if (tid == 0) {
+            const double est = anorm * zw * ratio;
+            const bool close = r2min < a.min_sep2 * rc2max;
+            if (stat != 0 || close || !(est <= a.hybrid_thresh)) {
+                const unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+                a.flag_list[slot] = idx;
+            }
+            a.status[idx] = 0;  // failures are re-derived in reference order by the re-solve
+        }
+        __syncthreads();
+    }
+}
+
+template <int NN, int DD, int DEG, int NF>
+int launch_ns_cta2(const PhsArgs& a, cudaStream_t st, int sms) {
+    using C = Cta2Cfg<NN, DD, DEG, NF>;
+    constexpr GradedLex<DD, DEG> gl{};
+    for (int m = 0; m < C::LL; ++m)
+        for (int ax = 0; ax < DD; ++ax)
+            if (a.P.expos[m * DD + ax] != gl.e[m][ax]) return MF_ERR_UNSUPPORTED;
+    const size_t bytes = (size_t)C::TOTAL * sizeof(double);
+    auto kern = phs_ns_cta2<NN, DD, DEG, NF>;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int per_sm = 0;
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CTA_THREADS, bytes));
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = a.m;
+    const int64_t cap = (int64_t)sms * per_sm * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, CTA_THREADS, bytes, st>>>(a);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
 int launch_phs_ns_cta(const PhsArgs& a, cudaStream_t st, int sms) {
     const int n = a.n, l = a.P.l, nf = a.P.nf;
     // HYBRID only (rows that fail or lose definiteness are re-solved); r^3 with
     // degree >= 1 (constant and linear monomials present: l >= d + 1)
     if (!a.flag_list || a.kappa || a.P.k != 3 || a.P.even || l < a.P.d + 1 || n - l < 1) return MF_ERR_UNSUPPORTED;
+    static const bool use_v1 = [] {
+        const char* e = getenv("MF_PHS_KERNEL");
+        return e && strcmp(e, "cta1") == 0;
+    }();
+    if (!use_v1 && n == 70 && l == 35 && a.P.d == 3 && nf == 4) {
+        const int rc = launch_ns_cta2<70, 3, 4, 4>(a, st, sms);
+        if (rc != MF_ERR_UNSUPPORTED) return rc;
+    }
     const NsCtaLayout L = ns_cta_layout(n, a.P.d, l, nf + 1);
     const size_t bytes = L.total * sizeof(double);
     int dev = 0, max_smem = 0;
