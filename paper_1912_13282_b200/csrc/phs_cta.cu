@@ -743,12 +743,15 @@ struct Cta2Cfg {
     static constexpr int RT = (LL + 7) / 8, CT = (MR + 7) / 8, MT = (M + 7) / 8;
     // shared layout (doubles)
     static constexpr int LOC = 0;
+    // Phi packed (upper triangle with the diagonal, row-major): 3 stencils per SM
+    // fit in shared memory; [K | b] reuses the region once Phi is consumed
+    static constexpr int EPK = NN * (NN + 1) / 2;
     static constexpr int E = LOC + ((NN * DD + 1) & ~1);
-    static constexpr int G = E + ((NN * EP + 1) & ~1);
+    static constexpr int G = E + ((EPK + 1) & ~1);
     static constexpr int F = G + ((RG * GP + 1) & ~1);
     static constexpr int Y = F + NN * NR;
-    static constexpr int K = Y + ((MR * YP + 1) & ~1);
-    static constexpr int OPS = K + ((M * KP + 1) & ~1);  // pivot rows per step, then 1 / pivot
+    static constexpr int K = E;
+    static constexpr int OPS = Y + ((MR * YP + 1) & ~1);  // pivot rows per step, then 1 / pivot
     static constexpr int V = OPS + ((LL * GP + LL + 1) & ~1);
     static constexpr int PROW = V + M * NR;              // 2 x 64
     static constexpr int COLK = PROW + 128;              // 2 x 80
@@ -757,12 +760,19 @@ struct Cta2Cfg {
     static constexpr int TOTAL = INTS + (NN + LL + M + 16) / 2 + 2;
     static_assert(QG * LL <= CTA_THREADS && KG * MR <= CTA_THREADS, "sweep layouts");
     static_assert(MR <= 64 && RG <= 80 && M <= 80, "pivot buffers");
+    static_assert(M * KP <= EPK, "[K | b] fits the Phi region");
+    static constexpr int TILES_PER_WARP = (MT * CT + CTA_WARPS - 1) / CTA_WARPS;
+    // packed offset of Phi(i, j)
+    __device__ __forceinline__ static int po(int i, int j) {
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        return lo * (2 * NN - lo + 1) / 2 + (hi - lo);
+    }
 };
 
 template <int NN, int DD, int DEG, int NF>
 __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
     using C = Cta2Cfg<NN, DD, DEG, NF>;
-    constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, EP = C::EP, GP = C::GP, YP = C::YP,
+    constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, GP = C::GP, YP = C::YP,
                   KP = C::KP, QG = C::QG, QI = C::QI, KG = C::KG, KI = C::KI;
     extern __shared__ __align__(16) double sm2[];
     double* loc = sm2 + C::LOC;
@@ -837,8 +847,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                 r2min = r2 < r2min ? r2 : r2min;
                 v = r2 * (r2 * fast_rsqrt(fmax(r2, 1e-300)));
             }
-            E[i * EP + j] = v;
-            E[j * EP + i] = v;
+            E[C::po(i, j)] = v;
         }
         for (int i = tid; i < NN; i += CTA_THREADS) {
             double x[DD], q[LL];
@@ -868,7 +877,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
         for (int r = tid; r < NN + LL; r += CTA_THREADS) {
             double acc = 0.0;
             if (r < NN) {
-                for (int j = 0; j < NN; ++j) acc += E[j * EP + r];  // column r == row r, r^3 >= 0
+                for (int j = 0; j < NN; ++j) acc += E[C::po(j, r)];  // r^3 >= 0
                 for (int m = 0; m < LL; ++m) acc += fabs(G[r * GP + m]);
             } else {
                 for (int i = 0; i < NN; ++i) acc += fabs(G[i * GP + (r - NN)]);
@@ -998,7 +1007,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                 for (int h = 0; h < 2; ++h) {
                     const int c = mt * 8 + 2 * t4 + h;
                     double v = 0.0;
-                    if (kr < LL && c < M) v = E[pk * EP + nonpiv[c]];
+                    if (kr < LL && c < M) v = E[C::po(pk, nonpiv[c])];
                     else if (kr < LL && c < MR) v = F[pk * NR + (c - M)];
                     acc[h] = v;
                 }
@@ -1007,7 +1016,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
 #pragma unroll
                 for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
                     const int k2 = ks * 4 + t4;
-                    const double av = (k2 < LL && kr < LL) ? -E[pk * EP + piv[k2 < LL ? k2 : 0]] : 0.0;
+                    const double av = (k2 < LL && kr < LL) ? -E[C::po(pk, piv[k2 < LL ? k2 : 0])] : 0.0;
                     const double bv = (k2 < LL && cb < MR) ? G[grow * GP + k2] : 0.0;
                     dmma_f64(acc[0], acc[1], av, bv);
                 }
@@ -1018,8 +1027,14 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                 }
             }
             __syncthreads();
-            // ---- [K | b] on the tensor cores
-            for (int tt = w; tt < C::MT * C::CT; tt += CTA_WARPS) {
+            // ---- [K | b] on the tensor cores (accumulated in registers: the tiles land in
+            //      the Phi region once every warp has read Phi)
+            double kacc[C::TILES_PER_WARP][2];
+#pragma unroll
+            for (int ti = 0; ti < C::TILES_PER_WARP; ++ti) {
+                const int tt = w + ti * CTA_WARPS;
+                kacc[ti][0] = kacc[ti][1] = 0.0;
+                if (tt >= C::MT * C::CT) continue;
                 const int rt = tt / C::CT, ct = tt - rt * C::CT;
                 const int c = rt * 8 + g8;
                 const int qc = nonpiv[c < M ? c : 0];
@@ -1028,7 +1043,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                 for (int h = 0; h < 2; ++h) {
                     const int c2 = ct * 8 + 2 * t4 + h;
                     double v = 0.0;
-                    if (c < M && c2 < M) v = E[qc * EP + nonpiv[c2]];
+                    if (c < M && c2 < M) v = E[C::po(qc, nonpiv[c2])];
                     else if (c < M && c2 < MR) v = F[qc * NR + (c2 - M)];
                     acc[h] = v;
                 }
@@ -1040,14 +1055,24 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                     const bool hp = kk < LL, kv = kk < 2 * LL;
                     const int kh = hp ? kk : 0, kw = hp ? 0 : (kv ? kk - LL : 0);
                     double av = 0.0, bv = 0.0;
-                    if (c < M && kv) av = -(hp ? E[qc * EP + piv[kh]] : G[qc * GP + kw]);
+                    if (c < M && kv) av = -(hp ? E[C::po(qc, piv[kh])] : G[qc * GP + kw]);
                     if (cb < MR && kv) bv = hp ? G[grow * GP + kh] : Y[cb * YP + kw];
                     dmma_f64(acc[0], acc[1], av, bv);
                 }
+                kacc[ti][0] = acc[0];
+                kacc[ti][1] = acc[1];
+            }
+            __syncthreads();  // Phi is consumed: [K | b] takes its place
+#pragma unroll
+            for (int ti = 0; ti < C::TILES_PER_WARP; ++ti) {
+                const int tt = w + ti * CTA_WARPS;
+                if (tt >= C::MT * C::CT) continue;
+                const int rt = tt / C::CT, ct = tt - rt * C::CT;
+                const int c = rt * 8 + g8;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int c2 = ct * 8 + 2 * t4 + h;
-                    if (c < M && c2 < MR) K[c * KP + c2] = acc[h];
+                    if (c < M && c2 < MR) K[c * KP + c2] = kacc[ti][h];
                 }
             }
             __syncthreads();
