@@ -115,7 +115,7 @@ struct Ns2Cfg {
 };
 
 template <int NN, int DEG, int DD, int NF>
-__global__ void __launch_bounds__(128, 3) phs_ns2(PhsArgs a) {
+__global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns2(PhsArgs a) {
     using Cfg = Ns2Cfg<NN, DEG, DD, NF>;
     constexpr int LL = Cfg::LL, M = Cfg::M, NR = Cfg::NR, RN = Cfg::RN, XN = Cfg::XN,
                   NP = Cfg::NP, P = Cfg::P, LP = Cfg::LP, NC = Cfg::NC, CS = Cfg::CS;
