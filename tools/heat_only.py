@@ -19,7 +19,7 @@ store = mf.compute_weights(nodes, eng, w.families)
 p = w.positions
 u0 = np.exp(-50 * ((p[:, 0] - 0.5) ** 2 + (p[:, 1] - 0.5) ** 2))
 dt = 4.9739636729043925e-14
-for r in range(3):
+for r in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
