@@ -14,6 +14,7 @@
  *   mf_apply_rows     storage.py:174-184            WeightStore.apply (selected rows)
  *   mf_plan_*         storage.py:186-188            apply_all through a locality-ordered ELL plan
  *   mf_heat_steps     drivers.py:87-110             run_heat_explicit step loop
+ *   mf_heat_pack      (none: packed operator for the heat loop, same results)
  *   mf_neumann_values storage.py:226-250            WeightStore.neumann_value (batched)
  *
  * Conventions
@@ -199,10 +200,23 @@ int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, doub
  * step (NaN sorts above inf); once a step exceeds 1e12 or is non-finite the
  * remaining steps do no work.  Dirichlet values must already be applied to u
  * before the first call (drivers.py:84-85). */
+typedef struct {
+    const int16_t* ell_d16;   /* ELL-32 layout: column - row, or 0 in wide tiles */
+    const uint8_t* meta;      /* N: row length | interior << 5 | dirichlet << 6 */
+    const uint8_t* tile_wide; /* ceil(N/32): 1 where an offset exceeds int16 (ell_idx is read) */
+} mf_heat_pack_t;
+/* Optional packed form of a plan for the heat loop (row length <= 16): per-step
+ * reads drop by the index bytes halved and the row masks folded into one byte.
+ * The result of mf_heat_steps is bitwise the same with or without it. */
+int mf_heat_pack(const int32_t* ell_len, const int32_t* ell_idx, const uint8_t* interior,
+                 const uint8_t* dirichlet, int64_t N, int32_t W, int16_t* ell_d16, uint8_t* meta,
+                 uint8_t* tile_wide, void* stream);
+/* pack: nullable; built by mf_heat_pack from the same plan and masks */
 int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, const double* ell_val, int64_t N,
                   int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
                   const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
-                  int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream);
+                  int64_t steps, double* u, double* scratch, uint64_t* peaks, const mf_heat_pack_t* pack,
+                  void* stream);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,11 @@ class NeumannT(ctypes.Structure):
     ]
 
 
+class HeatPackT(ctypes.Structure):
+    """mf_heat_pack_t (include/meshfree_b200.h)."""
+    _fields_ = [("ell_d16", _P), ("meta", _P), ("tile_wide", _P)]
+
+
 _SIGNATURES = {
     "mf_abi_version": ([], _I32),
     "mf_last_error": ([], ctypes.c_char_p),
@@ -63,8 +68,9 @@ _SIGNATURES = {
     "mf_plan_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "mf_permute": ([_P, _P, _I64, _I32, _P, _P], _I32),
     "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
+    "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
-                       _I64, _P, _P, _P, _P], _I32),
+                       _I64, _P, _P, _P, ctypes.POINTER(HeatPackT), _P], _I32),
 }
 
 EXPORTS = tuple(_SIGNATURES)

@@ -388,6 +388,105 @@ __global__ void __launch_bounds__(256) ell_heat_wide_k(const int32_t* __restrict
     if ((threadIdx.x & 31) == 0 && peak) atomicMax(hs.peak_out, peak);
 }
 
+// Packed heat step (mf_heat_pack): the step-invariant row data folded into one
+// byte per row (length | interior << 5 | dirichlet << 6) and the column
+// indices stored as 16-bit offsets from the row's own plan position -- in the
+// Morton-ordered plan a stencil's columns are near its row.  Tiles with an
+// offset outside int16 keep the 32-bit indices (tile_wide).  C4: 194 -> 161 MB
+// read per step; the sums are the same as ell_heat_wide_k's, term for term.
+constexpr int HEAT_META_LEN = 31, HEAT_META_INTERIOR = 32, HEAT_META_DIRICHLET = 64;
+
+template <int MAXW, int CHUNK, bool WIDE>
+__device__ __forceinline__ double heat_row_sum(const double* __restrict__ ell_val, const int32_t* __restrict__ ell_idx,
+                                               const int16_t* __restrict__ ell_d16, const double* __restrict__ u,
+                                               int64_t base, int32_t r, int len) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j0 = 0; j0 < MAXW; j0 += CHUNK) {
+        double a[CHUNK], g[CHUNK];
+        int32_t c[CHUNK];
+#pragma unroll
+        for (int j = 0; j < CHUNK; ++j) {
+            a[j] = j0 + j < len ? __ldcs(ell_val + base + 32 * (j0 + j)) : 0.0;
+            if (WIDE) c[j] = j0 + j < len ? __ldcs(ell_idx + base + 32 * (j0 + j)) : 0;
+            else c[j] = j0 + j < len ? r + (int32_t)__ldcs(ell_d16 + base + 32 * (j0 + j)) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < CHUNK; ++j) g[j] = j0 + j < len ? __ldg(u + c[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < CHUNK; ++j)
+            if (j0 + j < len) acc = __dadd_rn(acc, __dmul_rn(a[j], g[j]));
+    }
+    return acc;
+}
+
+template <int MAXW, int CHUNK>
+__global__ void __launch_bounds__(256) ell_heat_packed_k(const uint8_t* __restrict__ meta,
+                                                         const int16_t* __restrict__ ell_d16,
+                                                         const uint8_t* __restrict__ tile_wide,
+                                                         const int32_t* __restrict__ ell_idx,
+                                                         const double* __restrict__ ell_val, int64_t N, int W,
+                                                         const double* __restrict__ u, double* __restrict__ y,
+                                                         HeatStep hs) {
+    if (step_blew_up(hs.peak_prev)) return;
+    unsigned long long peak = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ((N + 31) & ~31ll); r += stride) {
+        if (r >= N) continue;
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        const int mt = meta[r];
+        double v = u[r];
+        if (mt & HEAT_META_INTERIOR) {
+            const int len = mt & HEAT_META_LEN;
+            const double acc = tile_wide[r >> 5]
+                                   ? heat_row_sum<MAXW, CHUNK, true>(ell_val, ell_idx, ell_d16, u, base, (int32_t)r, len)
+                                   : heat_row_sum<MAXW, CHUNK, false>(ell_val, ell_idx, ell_d16, u, base, (int32_t)r, len);
+            double f = hs.source ? hs.source[r] : 0.0;
+            // u + dt * (D * lap_u + f)   (drivers.py:93-96)
+            v = __dadd_rn(v, __dmul_rn(hs.dt, __dadd_rn(__dmul_rn(hs.D, acc), f)));
+        }
+        if (mt & HEAT_META_DIRICHLET) v = hs.g_dir[r];
+        y[r] = v;
+        if (!(hs.peak_skip && hs.peak_skip[r])) {
+            unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+            peak = b > peak ? b : peak;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long ob = __shfl_xor_sync(FULL, peak, o);
+        peak = ob > peak ? ob : peak;
+    }
+    if ((threadIdx.x & 31) == 0 && peak) atomicMax(hs.peak_out, peak);
+}
+
+// One thread per ELL entry: the 16-bit offset, and the tile's wide flag when
+// an offset does not fit; slot 0 also writes the row's meta byte.
+__global__ void heat_pack_k(const int32_t* __restrict__ ell_len, const int32_t* __restrict__ ell_idx,
+                            const uint8_t* __restrict__ interior, const uint8_t* __restrict__ dirichlet, int64_t N,
+                            int W, int16_t* __restrict__ d16, uint8_t* __restrict__ meta, uint8_t* __restrict__ tile_wide) {
+    const int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const int64_t tile = e / (32 * (int64_t)W);
+        const int rem = (int)(e - tile * 32 * (int64_t)W);
+        const int j = rem >> 5;
+        const int64_t r = tile * 32 + (rem & 31);
+        int16_t o = 0;
+        if (r < N) {
+            const int len = ell_len[r];
+            if (j < len) {
+                const int64_t dlt = (int64_t)ell_idx[e] - r;
+                if (dlt >= -32768 && dlt <= 32767) o = (int16_t)dlt;
+                else tile_wide[tile] = 1;
+            }
+            if (j == 0)
+                meta[r] = (uint8_t)(len | (interior[r] ? HEAT_META_INTERIOR : 0) | (dirichlet[r] ? HEAT_META_DIRICHLET : 0));
+        }
+        d16[e] = o;
+    }
+}
+
 inline int grid_for(int64_t work, int threads, int per_sm = 16) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -501,11 +600,28 @@ extern "C" int mf_neumann_values(const mf_neumann_t* nm, const double* u, double
     return MF_OK;
 }
 
+extern "C" int mf_heat_pack(const int32_t* ell_len, const int32_t* ell_idx, const uint8_t* interior,
+                            const uint8_t* dirichlet, int64_t N, int32_t W, int16_t* ell_d16, uint8_t* meta,
+                            uint8_t* tile_wide, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0 && W <= HEAT_META_LEN, "mf_heat_pack: bad arguments (W %d)", (int)W);
+    if (N == 0 || W == 0) return MF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    MF_CUDA_CHECK(cudaMemsetAsync(tile_wide, 0, (size_t)((N + 31) / 32), st));
+    const int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
+    heat_pack_k<<<grid_for(total, 256), 256, 0, st>>>(ell_len, ell_idx, interior, dirichlet, N, W, ell_d16, meta,
+                                                       tile_wide);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
 extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, const double* ell_val, int64_t N,
                              int32_t W, const uint8_t* interior, const uint8_t* dirichlet, const double* g_dir,
                              const double* source, double dt, double diffusivity, const mf_neumann_t* nm,
-                             int64_t steps, double* u, double* scratch, uint64_t* peaks, void* stream) {
+                             int64_t steps, double* u, double* scratch, uint64_t* peaks, const mf_heat_pack_t* pack,
+                             void* stream) {
     MF_REQUIRE(N >= 0 && steps >= 0 && W >= 0, "mf_heat_steps: bad arguments");
+    MF_REQUIRE(!pack || (pack->ell_d16 && pack->meta && pack->tile_wide && W <= 16),
+               "mf_heat_steps: a packed plan needs ell_d16, meta and tile_wide, and rows of at most 16 entries");
     if (steps == 0 || N == 0) return MF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     MF_CUDA_CHECK(cudaMemsetAsync(peaks, 0, sizeof(uint64_t) * steps, st));
@@ -518,7 +634,10 @@ extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, con
         HeatStep hs{interior, dirichlet, g_dir, source, has_nm ? nm->mask : nullptr, dt, diffusivity, cur, prev};
         double* u_old = buf[s & 1];
         double* u_new = buf[(s + 1) & 1];
-        if (W <= 16)
+        if (pack)
+            ell_heat_packed_k<16, 8><<<grid, 256, 0, st>>>(pack->meta, pack->ell_d16, pack->tile_wide, ell_idx, ell_val,
+                                                          N, W, u_old, u_new, hs);
+        else if (W <= 16)
             ell_heat_wide_k<16, 8><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
         else
             ell_apply_k<true><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);

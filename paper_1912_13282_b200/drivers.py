@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -153,12 +154,25 @@ def run_heat_explicit(
         _lib.check(lib.mf_permute(u_node.data_ptr(), plan.order.data_ptr(), n, 0, u_d.data_ptr(),
                                   _lib.stream_ptr()), "mf_permute")
 
+    # packed operator (16-bit column offsets, one meta byte per row) for the
+    # loop when the rows fit it; the sums are unchanged
+    pack = None
+    if steps >= 8 and 0 < plan.W <= 16 and os.environ.get("MF_HEAT_PACK", "1") != "0":
+        d16 = torch.empty(max(plan.ell_idx.numel(), 1), dtype=torch.int16, device=dev)
+        meta = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        wide = torch.empty(max((n + 31) // 32, 1), dtype=torch.uint8, device=dev)
+        _lib.check(lib.mf_heat_pack(plan.ell_len.data_ptr(), plan.ell_idx.data_ptr(), interior_d.data_ptr(),
+                                    dmask_d.data_ptr(), n, plan.W, d16.data_ptr(), meta.data_ptr(),
+                                    wide.data_ptr(), _lib.stream_ptr()), "mf_heat_pack")
+        pack = (_lib.HeatPackT(d16.data_ptr(), meta.data_ptr(), wide.data_ptr()), d16, meta, wide)
+
     def launch(k_steps, g_d, src_d, nm_struct, peak_view):
         _lib.check(lib.mf_heat_steps(
             plan.ell_len.data_ptr(), plan.ell_idx.data_ptr(), plan.ell_val.data_ptr(), n, plan.W,
             interior_d.data_ptr(), dmask_d.data_ptr(), g_d.data_ptr(), _lib.ptr(src_d), float(dt),
             float(diffusivity), None if nm_struct is None else ctypes.byref(nm_struct), k_steps,
-            u_d.data_ptr(), scratch.data_ptr(), peak_view.data_ptr(), _lib.stream_ptr()), "mf_heat_steps")
+            u_d.data_ptr(), scratch.data_ptr(), peak_view.data_ptr(),
+            None if pack is None else ctypes.byref(pack[0]), _lib.stream_ptr()), "mf_heat_steps")
 
     if not time_dep:
         g_d = to_plan(dirichlet_vals(dt), torch.float64)
