@@ -11,6 +11,8 @@
 // order from 0.0 with separately rounded multiply and add; the kernels here
 // keep exactly that order (__dmul_rn/__dadd_rn), so the results are bitwise
 // equal to the reference on the same CSR.
+#include <cstdlib>
+
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -420,7 +422,10 @@ __device__ __forceinline__ double heat_row_sum(const double* __restrict__ ell_va
     return acc;
 }
 
-template <int MAXW, int CHUNK>
+// With PDL (programmatic dependent launch) the next step's blocks start as the
+// previous step's drain: they prefetch their first rows' operator entries
+// (which do not depend on u) into L2, then wait for the previous grid.
+template <int MAXW, int CHUNK, bool PDL>
 __global__ void __launch_bounds__(256) ell_heat_packed_k(const uint8_t* __restrict__ meta,
                                                          const int16_t* __restrict__ ell_d16,
                                                          const uint8_t* __restrict__ tile_wide,
@@ -428,9 +433,21 @@ __global__ void __launch_bounds__(256) ell_heat_packed_k(const uint8_t* __restri
                                                          const double* __restrict__ ell_val, int64_t N, int W,
                                                          const double* __restrict__ u, double* __restrict__ y,
                                                          HeatStep hs) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (PDL) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        const int64_t r0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (r0 < N) {
+            const int64_t base = (r0 >> 5) * 32 * (int64_t)W + (r0 & 31);
+            for (int j = 0; j < W; j += 2) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_val + base + 32 * j));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_d16 + base + 32 * j));
+            }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     if (step_blew_up(hs.peak_prev)) return;
     unsigned long long peak = 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < ((N + 31) & ~31ll); r += stride) {
         if (r >= N) continue;
         const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
@@ -625,8 +642,20 @@ extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, con
     if (steps == 0 || N == 0) return MF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     MF_CUDA_CHECK(cudaMemsetAsync(peaks, 0, sizeof(uint64_t) * steps, st));
-    const int grid = ell_grid(N);
+    // blocks per SM: the packed loop runs fastest at 4 x 256 threads (C4: 35 vs
+    // 37-45 ms at 3, 5, 6, 8 or 16; MF_HEAT_BPS overrides, 0 = one row per thread)
+    static const int bps_env = [] {
+        const char* e = getenv("MF_HEAT_BPS");
+        return e ? atoi(e) : -1;
+    }();
+    const int bps = bps_env >= 0 ? bps_env : (pack ? 4 : 8);
+    const int grid = bps > 0 ? grid_for(((N + 31) / 32) * 32, 256, bps) : (int)(((N + 31) / 32 * 32 + 255) / 256);
     const bool has_nm = nm && nm->count > 0;
+    static const bool pdl_env = [] {
+        const char* e = getenv("MF_HEAT_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    const bool pdl = pdl_env && !has_nm;
     double* buf[2] = {u, scratch};
     for (int64_t s = 0; s < steps; ++s) {
         const unsigned long long* prev = s ? (const unsigned long long*)(peaks + s - 1) : nullptr;
@@ -634,9 +663,22 @@ extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, con
         HeatStep hs{interior, dirichlet, g_dir, source, has_nm ? nm->mask : nullptr, dt, diffusivity, cur, prev};
         double* u_old = buf[s & 1];
         double* u_new = buf[(s + 1) & 1];
-        if (pack)
-            ell_heat_packed_k<16, 8><<<grid, 256, 0, st>>>(pack->meta, pack->ell_d16, pack->tile_wide, ell_idx, ell_val,
-                                                          N, W, u_old, u_new, hs);
+        if (pack && pdl && s > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, ell_heat_packed_k<16, 8, true>, pack->meta, pack->ell_d16,
+                                             pack->tile_wide, ell_idx, ell_val, N, W, (const double*)u_old, u_new,
+                                             hs));
+        } else if (pack)
+            ell_heat_packed_k<16, 8, false><<<grid, 256, 0, st>>>(pack->meta, pack->ell_d16, pack->tile_wide, ell_idx,
+                                                                 ell_val, N, W, u_old, u_new, hs);
         else if (W <= 16)
             ell_heat_wide_k<16, 8><<<grid, 256, 0, st>>>(ell_len, ell_idx, ell_val, N, W, u_old, u_new, hs);
         else
