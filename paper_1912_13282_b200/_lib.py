@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmeshfree_b200.so")
+LIB_PATH = os.environ.get("MF_LIB_PATH") or os.path.join(HERE, "libmeshfree_b200.so")  # override: A/B builds
 
 MF_OK = 0
 MF_ERR_UNSUPPORTED = 3

@@ -770,7 +770,7 @@ struct Cta2Cfg {
 };
 
 template <int NN, int DD, int DEG, int NF>
-__global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
+__global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
     using C = Cta2Cfg<NN, DD, DEG, NF>;
     constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, GP = C::GP, YP = C::YP,
                   KP = C::KP, QG = C::QG, QI = C::QI, KG = C::KG, KI = C::KI;
@@ -897,43 +897,40 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
             const int r = qrg + QG * i;
             gq[i] = (qact && r < RG) ? G[r * GP + qjj] : 0.0;
         }
+        // pivot search: one 32-bit key per candidate, the float bits of |v| with
+        // the low 7 bits replaced by 127 - row (largest |v| to 2^-16, then the
+        // lowest row), merged by a shared-memory atomicMax; column k+1's owners
+        // form their keys right after updating it in step k (three key slots).
+        // Pivot rows are a per-thread bit mask of the thread's rows.
+        unsigned* qkey = reinterpret_cast<unsigned*>(red + 40);
+        uint32_t ispm = 0;
+        auto key_of = [](double v, int r) -> unsigned {
+            const float f = __double2float_ru(fabs(v));
+            return (__float_as_uint(f) & ~127u) | (unsigned)(127 - r);
+        };
+        if (tid < 3) qkey[tid] = 0u;
+        __syncthreads();
+        if (ok && qact && qjj == 0) {
+            unsigned kb = 0;
+#pragma unroll
+            for (int i = 0; i < QI; ++i) {
+                const int r = qrg + QG * i;
+                if (r < NN) kb = max(kb, key_of(gq[i], r));
+            }
+            if (kb) atomicMax(&qkey[0], kb);
+        }
+        __syncthreads();
         for (int k = 0; k < LL && ok; ++k) {
             double* pr_buf = prow + (k & 1) * 64;
             double* ck_buf = colk + (k & 1) * 80;
-            // pivot candidates: the row groups of column k
-            if (qact && qjj == k) {
-                double best = -1.0;
-                int bp = 0x7fffffff;
-#pragma unroll
-                for (int i = 0; i < QI; ++i) {
-                    const int r = qrg + QG * i;
-                    if (r < NN && !isp[r]) {
-                        const double v = fabs(gq[i]);
-                        if (v > best) {
-                            best = v;
-                            bp = r;
-                        }
-                    }
-                }
-                red[qrg] = best;
-                redi[qrg] = bp;
-            }
-            __syncthreads();
-            double best = -1.0;
-            int pr = 0x7fffffff;
-#pragma unroll
-            for (int q = 0; q < QG; ++q) {
-                const double v = red[q];
-                const int p = redi[q];
-                if (v > best || (v == best && p < pr)) {
-                    best = v;
-                    pr = p;
-                }
-            }
-            if (!(best > 0.0) || !isfinite(best) || pr == 0x7fffffff) {
-                ok = false;  // uniform: every thread read the same candidates
+            const unsigned key = qkey[k % 3];
+            const int pr = 127 - (int)(key & 127u);
+            const float best = __uint_as_float(key & ~127u);
+            if (key == 0u || !(best > 0.0f) || !isfinite(best) || pr >= NN) {
+                ok = false;  // uniform: every thread read the same key
                 break;
             }
+            if (tid == 0) qkey[(k + 2) % 3] = 0u;  // read in step k - 1, written in step k + 1
             // stage the pivot row (its owners) and column k (unscaled)
             if (qact) {
                 if (qrg == pr % QG) {
@@ -943,6 +940,7 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                         if (qrg + QG * i == pr) v = gq[i];
                     pr_buf[qjj] = v;
                     ops[k * GP + qjj] = v;
+                    ispm |= 1u << (pr / QG);
                 }
                 if (qjj == k) {
 #pragma unroll
@@ -969,7 +967,17 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                         gq[i] = qjj == k ? cr : fma(-pj, cr, gq[i]);
                     }
                 }
+                if (qjj == k + 1) {
+                    unsigned kb = 0;
+#pragma unroll
+                    for (int i = 0; i < QI; ++i) {
+                        const int r = qrg + QG * i;
+                        if (r < NN && !((ispm >> i) & 1u)) kb = max(kb, key_of(gq[i], r));
+                    }
+                    if (kb) atomicMax(&qkey[(k + 1) % 3], kb);
+                }
             }
+            __syncthreads();
         }
         if (ok) {
 #pragma unroll
@@ -1185,17 +1193,46 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta2(PhsArgs a) {
                 la[f] = mx;
             }
         }
-        bad = __syncthreads_or(bad) != 0;
-        if (bad && stat == 0) stat = 1;
-        zw = block_reduce_max(zw, red);
-        double ratio = 0.0;
+        // one fused reduction of the failure flag and the 1 + 2 NF maxima (all
+        // >= 0); only thread 0 consumes them
+        {
+            constexpr int NV = 2 + 2 * NF;
+            double rv[NV];
+            rv[0] = bad ? 1.0 : 0.0;
+            rv[1] = zw;
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            const double xwf = block_reduce_max(xw[f], red);
-            const double laf = block_reduce_max(la[f], red);
-            ratio = fmax(ratio, fmax(xwf, laf) / xwf);
+            for (int f = 0; f < NF; ++f) {
+                rv[2 + f] = xw[f];
+                rv[2 + NF + f] = la[f];
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) rv[v] = fmax(rv[v], __shfl_xor_sync(FULL, rv[v], o));
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) prow[v * CTA_WARPS + w] = rv[v];
+            }
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    double m = prow[v * CTA_WARPS];
+                    for (int q = 1; q < CTA_WARPS; ++q) m = fmax(m, prow[v * CTA_WARPS + q]);
+                    rv[v] = m;
+                }
+                bad = rv[0] != 0.0;
+                zw = rv[1];
+            }
+            if (bad && stat == 0) stat = 1;
+            double ratio = 0.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) ratio = fmax(ratio, fmax(rv[2 + f], rv[2 + NF + f]) / rv[2 + f]);
+            xw[0] = ratio;  // thread 0's
         }
         if (tid == 0) {
+            const double ratio = xw[0];
             const double est = anorm * zw * ratio;
             const bool close = r2min < a.min_sep2 * rc2max;
             if (stat != 0 || close || !(est <= a.hybrid_thresh)) {
