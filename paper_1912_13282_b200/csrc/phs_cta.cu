@@ -1168,7 +1168,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                     zw = fmax(zw, fabs(wv));
                 }
             }
-            // lambda_f = Q1^-1 (r_piv - Y v): the recorded column operations, last first
+            // lambda_f = Q1^-1 (r_piv - Y v): the recorded column operations, last
+            // first.  Step k needs the finished x_j (j > k) and the untouched s_j
+            // (j < k): the j < k part is one parallel product up front, the rest a
+            // column-oriented back substitution (x_k broadcast by one shuffle, the
+            // lanes j < k fold it in) -- a 35-step chain of shuffle + FMA instead
+            // of a warp reduction per step.  Only the estimate uses lambda.
             for (int e = tid; e < LL * NF; e += CTA_THREADS) {
                 const int k = e / NF, f = e - k * NF;
                 double sv = Y[(M + f) * YP + k];
@@ -1176,21 +1181,35 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                 colk[k * NF + f] = sv;
             }
             __syncthreads();
+            constexpr int LS = (LL + 31) / 32;
             for (int f = w; f < NF; f += CTA_WARPS) {
-                for (int k = LL - 1; k >= 0; --k) {
-                    double part = 0.0;
-                    for (int j = lane; j < LL; j += 32)
-                        if (j != k) part = fma(ops[k * GP + j], colk[j * NF + f], part);
+                double acc[LS];
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
-                    if (lane == 0) colk[k * NF + f] = invs[k] * (colk[k * NF + f] - part);
-                    __syncwarp();
+                for (int q = 0; q < LS; ++q) {
+                    const int jr = lane + 32 * q;
+                    double a = 0.0;
+                    if (jr < LL) {
+                        a = colk[jr * NF + f];
+                        for (int i2 = 0; i2 < jr; ++i2) a = fma(-ops[jr * GP + i2], colk[i2 * NF + f], a);
+                    }
+                    acc[q] = a;
                 }
                 double mx = 0.0;
-                for (int j = lane; j < LL; j += 32) mx = fmax(mx, fabs(colk[j * NF + f]));
+                for (int k = LL - 1; k >= 0; --k) {
+                    const int owner = k & 31, qk = k >> 5;
+                    double xk = 0.0;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-                la[f] = mx;
+                    for (int q = 0; q < LS; ++q)
+                        if (q == qk) xk = acc[q];
+                    xk = __shfl_sync(FULL, invs[k] * xk, owner);
+                    mx = fmax(mx, fabs(xk));
+#pragma unroll
+                    for (int q = 0; q < LS; ++q) {
+                        const int jr = lane + 32 * q;
+                        if (jr < k) acc[q] = fma(-ops[jr * GP + k], xk, acc[q]);
+                    }
+                }
+                la[f] = mx;  // uniform over the warp
             }
         }
         // one fused reduction of the failure flag and the 1 + 2 NF maxima (all
