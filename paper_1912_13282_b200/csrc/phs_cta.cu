@@ -958,13 +958,18 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
             const double inv = fast_rcp(pr_buf[k]);
             if (tid == 0) invs[k] = inv;
             if (qact) {
-                const double pj = pr_buf[qjj];
+                if (qjj == k) {
 #pragma unroll
-                for (int i = 0; i < QI; ++i) {
-                    const int r = qrg + QG * i;
-                    if (r < RG) {
-                        const double cr = ck_buf[r] * inv;
-                        gq[i] = qjj == k ? cr : fma(-pj, cr, gq[i]);
+                    for (int i = 0; i < QI; ++i) {
+                        const int r = qrg + QG * i;
+                        if (r < RG) gq[i] = ck_buf[r] * inv;
+                    }
+                } else {
+                    const double pjs = pr_buf[qjj] * inv;
+#pragma unroll
+                    for (int i = 0; i < QI; ++i) {
+                        const int r = qrg + QG * i;
+                        if (r < RG) gq[i] = fma(-ck_buf[r], pjs, gq[i]);
                     }
                 }
                 if (qjj == k + 1) {
@@ -1119,11 +1124,11 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                 definite = definite && dk * d0 > 0.0;
                 const double inv = fast_rcp(dk);
                 if (kact && kjj > k) {
-                    const double pj = pr_buf[kjj];
+                    const double pjs = pr_buf[kjj] * inv;
 #pragma unroll
                     for (int i = 0; i < KI; ++i) {
                         const int r = krg + KG * i;
-                        if (r < M) kv[i] = r == k ? pj * inv : fma(-ck_buf[r] * inv, pj, kv[i]);
+                        if (r < M) kv[i] = r == k ? pjs : fma(-ck_buf[r], pjs, kv[i]);
                     }
                 }
             }
