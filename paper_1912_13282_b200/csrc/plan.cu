@@ -9,6 +9,7 @@
 // contiguous.  Entry order inside each row is unchanged (ascending original
 // column), so every row sum keeps scipy's addend order and results stay
 // bitwise equal to the reference (storage.py:186-188).
+#include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -112,6 +113,42 @@ __global__ void plan_ell_build(const int32_t* __restrict__ indptr, const int32_t
         }
         if (ell_idx) ell_idx[e] = ci;
         if (ell_val) ell_val[e] = v;
+    }
+}
+
+// Block per 32-row tile: the tile's 32 W entries are built by one block, so
+// the rows' CSR segments and the inverse-permutation lookups of their columns
+// (spatial neighbours share columns) are re-read from this SM's L1 instead of
+// being spread over several blocks and SMs; output order and values are the
+// same as plan_ell_build's.
+__global__ void __launch_bounds__(256) plan_ell_build_tile(const int32_t* __restrict__ indptr,
+                                                           const int32_t* __restrict__ indices,
+                                                           const double* __restrict__ data, int64_t N, int W,
+                                                           const int32_t* __restrict__ order,
+                                                           const int32_t* __restrict__ inv, int32_t* __restrict__ ell_idx,
+                                                           double* __restrict__ ell_val, int32_t* __restrict__ ell_len) {
+    const int64_t tiles = (N + 31) / 32;
+    const int per = 32 * W;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t base = tile * per;
+        for (int rem = threadIdx.x; rem < per; rem += blockDim.x) {
+            const int j = rem >> 5, lane = rem & 31;
+            const int64_t rn = tile * 32 + lane;
+            int32_t ci = 0;
+            double v = 0.0;
+            if (rn < N) {
+                const int64_t ro = order ? order[rn] : rn;
+                const int32_t lo = indptr[ro], len = indptr[ro + 1] - lo;
+                if (j == 0 && ell_len) ell_len[rn] = len;
+                if (j < len) {
+                    const int32_t c = indices[lo + j];
+                    ci = inv ? inv[c] : c;
+                    if (data) v = data[lo + j];
+                }
+            }
+            if (ell_idx) ell_idx[base + rem] = ci;
+            if (ell_val) ell_val[base + rem] = v;
+        }
     }
 }
 
@@ -224,8 +261,20 @@ extern "C" int mf_plan_build(const int32_t* indptr, const int32_t* indices, cons
     int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
     if (total == 0 && N == 0) return MF_OK;
     int64_t work = total > N ? total : N;
-    plan_ell_build<<<grid_of(work, 256, 16), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, N, W, order, inv,
-                                                                              ell_idx, ell_val, ell_len);
+    // blocks per SM for the tile build (C3 plan, order + ELL: 444 us element-wise;
+    // tile build 570 / 429 / 361 / 338 / 355 / 600 us at 2 / 3 / 4 / 5 / 6 / 8
+    // blocks per SM -- the L1 reuse collapses beyond that); 0 = element-wise
+    static const int variant = [] {
+        const char* e = getenv("MF_PLAN_BUILD");
+        return e ? atoi(e) : 5;
+    }();
+    if (variant >= 1 && W > 0)
+        plan_ell_build_tile<<<grid_of((N + 31) / 32 * 256, 256, variant), 256, 0,
+                              (cudaStream_t)stream>>>(indptr, indices, data, N, W, order, inv, ell_idx, ell_val,
+                                                      ell_len);
+    else
+        plan_ell_build<<<grid_of(work, 256, 16), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, N, W, order,
+                                                                                  inv, ell_idx, ell_val, ell_len);
     MF_LAUNCH_CHECK();
     return MF_OK;
 }
