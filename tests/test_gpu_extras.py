@@ -73,23 +73,25 @@ def test_neumann_value_and_heat_with_neumann():
         u2 = u.copy()
         u2[i] = got
         assert abs(c @ u2[store.stencil(i)] - 0.3) <= 1e-9 * np.abs(c).sum()
-    # heat with Dirichlet on the outer circle and Neumann on the hole
-    dt, steps = 1e-6, 4
-    out = m.run_heat_explicit(nodes, store, dt=dt, steps=steps, dirichlet={-1: 0.0}, neumann={-2: 0.0},
-                              initial=u)
-    lap = store.matrix("laplacian")
-    cur = u.copy()
-    cur[nodes.select(-1)] = 0.0
-    for _ in range(steps):
-        lap_u = oracle.apply(lap.indptr, lap.indices, lap.data, cur)
-        new = cur.copy()
-        it = nodes.interior_indices()
-        new[it] = cur[it] + dt * (1.0 * lap_u[it] + 0.0)
-        new[nodes.select(-1)] = 0.0
-        for i in nodes.select(-2):
-            new[int(i)] = neumann_ref(store, cur, int(i), nodes.normal(int(i)), 0.0)
-        cur = new
-    assert np.max(np.abs(out - cur)) <= 1e-12 * np.max(np.abs(cur))
+    # heat with Dirichlet on the outer circle and Neumann on the hole; 10 steps
+    # run the packed operator (mf_heat_pack) on the node-ordered plan
+    dt = 1e-6
+    for steps in (4, 10):
+        out = m.run_heat_explicit(nodes, store, dt=dt, steps=steps, dirichlet={-1: 0.0}, neumann={-2: 0.0},
+                                  initial=u)
+        lap = store.matrix("laplacian")
+        cur = u.copy()
+        cur[nodes.select(-1)] = 0.0
+        for _ in range(steps):
+            lap_u = oracle.apply(lap.indptr, lap.indices, lap.data, cur)
+            new = cur.copy()
+            it = nodes.interior_indices()
+            new[it] = cur[it] + dt * (1.0 * lap_u[it] + 0.0)
+            new[nodes.select(-1)] = 0.0
+            for i in nodes.select(-2):
+                new[int(i)] = neumann_ref(store, cur, int(i), nodes.normal(int(i)), 0.0)
+            cur = new
+        assert np.max(np.abs(out - cur)) <= 1e-12 * np.max(np.abs(cur))
 
 
 def test_vector_helpers_exact_on_linear_fields():

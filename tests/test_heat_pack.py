@@ -50,3 +50,24 @@ def test_packed_heat_bitwise_both_tile_kinds(monkeypatch):
                                     steps=steps)
     assert bad == 0
     assert np.array_equal(u_pack.view(np.int64), ref.view(np.int64))
+
+
+def test_packed_heat_time_dependent_matches_plain(monkeypatch):
+    """Time-dependent Dirichlet data: one launch per step over the packed plan."""
+    import paper_1912_13282_b200 as m
+
+    rng = np.random.default_rng(9)
+    N = 3001  # not a multiple of 32: a partial last tile
+    pts = rng.uniform(0, 1, (N, 2))
+    types = np.where(np.min(np.minimum(pts, 1 - pts), axis=1) < 0.02, -1, 1).astype(np.int64)
+    nodes = m.find_closest_stencils(m.NodeSet(pts, types), 9)
+    store = m.compute_weights(nodes, m.RbfFd(m.Polyharmonic(3), degree=1, scale="support", solver="lu"),
+                              ["laplacian"])
+    fn = lambda p, t: t * p[:, 0] + 0.5  # noqa: E731
+    args = dict(dt=1e-7, steps=11, dirichlet={-1: fn}, initial=np.cos(pts[:, 1]))
+    u_pack = m.run_heat_explicit(nodes, store, **args)
+    monkeypatch.setenv("MF_HEAT_PACK", "0")
+    u_plain = m.run_heat_explicit(nodes, store, **args)
+    assert np.array_equal(u_pack.view(np.int64), u_plain.view(np.int64))
+    idx = nodes.boundary_indices()
+    assert np.array_equal(u_pack[idx], fn(pts[idx], 11 * 1e-7))
