@@ -112,20 +112,22 @@ __global__ void __launch_bounds__(256) csr_fill_smem(const int64_t* __restrict__
 // order is the stable (column, slot) lexsort of csr_fill.
 template <int NR>
 struct SortNet {
-    int c[700][2];
+    static constexpr int P = NR <= 64 ? 64 : 128;  // network width (power of two >= NR)
+    static constexpr int CAP = P == 64 ? 700 : 1600;
+    int c[CAP][2];
     int nc;
-    int out[64];
+    int out[P];
     constexpr SortNet() : c{}, nc(0), out{} {
-        int map[64] = {};
-        bool inf[64] = {};
-        for (int i = 0; i < 64; ++i) {
+        int map[P] = {};
+        bool inf[P] = {};
+        for (int i = 0; i < P; ++i) {
             map[i] = i;
             inf[i] = i >= NR;
         }
-        for (int p = 1; p < 64; p <<= 1)
+        for (int p = 1; p < P; p <<= 1)
             for (int k = p; k >= 1; k >>= 1)
-                for (int j = k % p; j + k < 64; j += 2 * k)
-                    for (int i = 0; i < k && i + j + k < 64; ++i)
+                for (int j = k % p; j + k < P; j += 2 * k)
+                    for (int i = 0; i < k && i + j + k < P; ++i)
                         if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
                             const int a = i + j, b = i + j + k;
                             if (inf[b]) continue;  // (both inf, or only the high one: no-op)
@@ -141,25 +143,33 @@ struct SortNet {
                             c[nc][1] = map[b];
                             ++nc;
                         }
-        for (int i = 0; i < 64; ++i) out[i] = map[i];
+        for (int i = 0; i < P; ++i) out[i] = map[i];
     }
 };
 
+// warps per block of csr_fill_net (the staged tiles must fit 48 KB of static shared memory)
 template <int NR>
-__global__ void __launch_bounds__(256, 4) csr_fill_net(const int64_t* __restrict__ rows, const int32_t* __restrict__ st,
-                                                       int64_t m, const int32_t* __restrict__ indptr,
-                                                       int32_t* __restrict__ indices, int32_t* __restrict__ perm) {
+constexpr int csr_net_warps() {
+    return NR <= 40 ? 8 : 4;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(csr_net_warps<NR>() * 32, NR <= 40 ? 4 : 2)
+    csr_fill_net(const int64_t* __restrict__ rows, const int32_t* __restrict__ st, int64_t m,
+                 const int32_t* __restrict__ indptr, int32_t* __restrict__ indices, int32_t* __restrict__ perm) {
     constexpr int PITCH = NR | 1;  // odd: lane-per-row accesses hit distinct banks
+    constexpr int WPB = csr_net_warps<NR>();
+    constexpr int SH = NR <= 64 ? 6 : 7;  // key = column << SH | slot
     constexpr SortNet<NR> net{};
-    __shared__ int32_t sk[8][32 * PITCH];
+    __shared__ int32_t sk[WPB][32 * PITCH];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int32_t* k = sk[wib];
-    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + wib) * 32; r0 < m; r0 += (int64_t)gridDim.x * 8 * 32) {
+    for (int64_t r0 = ((int64_t)blockIdx.x * WPB + wib) * 32; r0 < m; r0 += (int64_t)gridDim.x * WPB * 32) {
         const int nr = (int)(m - r0 < 32 ? m - r0 : 32);
         // coalesced staging of the tile's keys (rows are contiguous in `st`)
         for (int e = lane; e < nr * NR; e += 32) {
             const int rr = e / NR, j = e - rr * NR;
-            k[rr * PITCH + j] = (st[r0 * NR + e] << 6) | j;
+            k[rr * PITCH + j] = (st[r0 * NR + e] << SH) | j;
         }
         __syncwarp();
         if (lane < nr) {
@@ -182,8 +192,8 @@ __global__ void __launch_bounds__(256, 4) csr_fill_net(const int64_t* __restrict
             const int64_t base = indptr[rows[r]];
             for (int q = lane; q < NR; q += 32) {
                 const int kk = k[rr * PITCH + q];
-                indices[base + q] = kk >> 6;
-                perm[base + q] = (int32_t)(r * NR + (kk & 63));
+                indices[base + q] = kk >> SH;
+                perm[base + q] = (int32_t)(r * NR + (kk & ((1 << SH) - 1)));
             }
         }
         __syncwarp();
@@ -564,6 +574,9 @@ extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_
         if (N < (1 << 25) && (n == 15 || n == 25 || n == 35)) {
             auto k = n == 15 ? csr_fill_net<15> : (n == 25 ? csr_fill_net<25> : csr_fill_net<35>);
             k<<<grid_for((m + 255) / 256 * 256, 256, 16), 256, 0, st>>>(rows, stencils, m, indptr, indices, perm);
+        } else if (N < (1 << 24) && n == 70) {
+            csr_fill_net<70><<<grid_for((m + 127) / 128 * 128, 128, 16), 128, 0, st>>>(rows, stencils, m, indptr,
+                                                                                    indices, perm);
         } else if (N < (1 << 25) && n <= 64) {
             const int smem = CSR_ROWS * ((n + 3) & ~3) * (int)sizeof(int32_t);
             csr_fill_smem<<<grid_for((m + CSR_ROWS - 1) / CSR_ROWS, 1, 8), 256, smem, st>>>(rows, stencils, m, n,
