@@ -44,7 +44,7 @@ def check(pts, n, for_which=None, search_among=None):
     assert bad.size == 0, f"{bad.size} rows differ, first target {targets[bad[0]]}"
 
 
-@pytest.mark.parametrize("d,n", [(3, 35), (2, 15), (2, 25), (3, 20)])
+@pytest.mark.parametrize("d,n", [(3, 35), (2, 15), (2, 25), (3, 20), (3, 70)])
 def test_clustered_bitwise(d, n):
     check(clustered(40_000, d, seed=d * 100 + n), n)
 
@@ -69,3 +69,13 @@ def test_target_and_pool_subsets_bitwise():
     targets = rng.choice(30_000, 5000, replace=False)
     pool = np.sort(rng.choice(30_000, 20_000, replace=False))
     check(pts, 35, for_which=targets, search_among=pool)
+
+
+def test_wide_k_uniform_and_subsets_bitwise():
+    """K = n + 8 = 78 (C5's stencil size): the general kernel's path."""
+    rng = np.random.default_rng(13)
+    pts = rng.uniform(-1, 1, (40_000, 3))
+    check(pts, 70)
+    targets = rng.choice(40_000, 3000, replace=False)
+    pool = np.sort(rng.choice(40_000, 30_000, replace=False))
+    check(pts, 70, for_which=targets, search_among=pool)
