@@ -80,6 +80,41 @@ __device__ __forceinline__ double from_ordered_bits(unsigned long long u) {
     return __longlong_as_double((long long)u);
 }
 
+// Bounding-box reduction of a block (blockDim.x a multiple of 32, <= 1024): warp
+// shuffles, then one warp over the per-warp partials, then one atomic per
+// value and block on bb[0..d) (min) / bb[3..3+d) (max) as ordered bits --
+// per-warp atomics on six addresses serialise at the L2.
+__device__ __forceinline__ void block_bbox_commit(double mn[3], double mx[3], int d, unsigned long long* bb) {
+    __shared__ double smn[3][32], smx[3][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int a = 0; a < d; ++a) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(FULL, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(FULL, mx[a], o));
+        }
+        if (lane == 0) {
+            smn[a][w] = mn[a];
+            smx[a][w] = mx[a];
+        }
+    }
+    __syncthreads();
+    if (w == 0) {
+        for (int a = 0; a < d; ++a) {
+            double vn = lane < nw ? smn[a][lane] : INFINITY, vx = lane < nw ? smx[a][lane] : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                vn = fmin(vn, __shfl_xor_sync(FULL, vn, o));
+                vx = fmax(vx, __shfl_xor_sync(FULL, vx, o));
+            }
+            if (lane == 0) {
+                atomicMin(&bb[a], ordered_bits(vn));
+                atomicMax(&bb[3 + a], ordered_bits(vx));
+            }
+        }
+    }
+}
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

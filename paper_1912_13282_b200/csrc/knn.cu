@@ -792,17 +792,7 @@ __global__ void knn_bbox(const double* __restrict__ pos, int d, const int64_t* _
             mx[a] = fmax(mx[a], x);
         }
     }
-    for (int a = 0; a < d; ++a) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn[a] = fmin(mn[a], __shfl_xor_sync(FULL, mn[a], o));
-            mx[a] = fmax(mx[a], __shfl_xor_sync(FULL, mx[a], o));
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&bb[a], ordered_bits(mn[a]));
-            atomicMax(&bb[3 + a], ordered_bits(mx[a]));
-        }
-    }
+    block_bbox_commit(mn, mx, d, bb);
 }
 
 __global__ void knn_params(const unsigned long long* bb, int d, int64_t P, GridParams* gp) {
@@ -988,7 +978,7 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cudaMemsetAsync(L.fb_count, 0, 2 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.cnt, 0, sizeof(int32_t) * (nc + 1), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.in_pool, 0, (size_t)N, st));
-    knn_bbox<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.bb);
+    knn_bbox<<<grid_for(P, 256, 4), 256, 0, st>>>(pos, d, pool, P, L.bb);
     MF_LAUNCH_CHECK();
     knn_params<<<1, 1, 0, st>>>(L.bb, d, P, L.gp);
     MF_LAUNCH_CHECK();

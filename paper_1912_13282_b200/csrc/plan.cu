@@ -44,17 +44,7 @@ __global__ void plan_bbox(const double* __restrict__ pos, int64_t N, int d, unsi
             mn[a] = fmin(mn[a], x);
             mx[a] = fmax(mx[a], x);
         }
-    for (int a = 0; a < d; ++a) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn[a] = fmin(mn[a], __shfl_xor_sync(FULL, mn[a], o));
-            mx[a] = fmax(mx[a], __shfl_xor_sync(FULL, mx[a], o));
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(&bb[a], ordered_bits(mn[a]));
-            atomicMax(&bb[3 + a], ordered_bits(mx[a]));
-        }
-    }
+    block_bbox_commit(mn, mx, d, bb);
 }
 
 __global__ void plan_keys(const double* __restrict__ pos, int64_t N, int d, const unsigned long long* __restrict__ bb,
@@ -238,7 +228,7 @@ extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_
     }
     MF_CUDA_CHECK(cudaMemsetAsync(bb, 0xff, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(bb + 3, 0, 3 * sizeof(unsigned long long), st));
-    plan_bbox<<<grid_of(N, 256), 256, 0, st>>>(pos, N, d, bb);
+    plan_bbox<<<grid_of(N, 256, 4), 256, 0, st>>>(pos, N, d, bb);
     MF_LAUNCH_CHECK();
     plan_keys<<<grid_of(N, 256), 256, 0, st>>>(pos, N, d, bb, k0, v0);
     MF_LAUNCH_CHECK();
