@@ -50,7 +50,9 @@ __global__ void plan_bbox(const double* __restrict__ pos, int64_t N, int d, unsi
 __global__ void plan_keys(const double* __restrict__ pos, int64_t N, int d, const unsigned long long* __restrict__ bb,
                           unsigned* __restrict__ key, int32_t* __restrict__ val) {
     double lo[3], sc[3];
-    const int bits = d == 1 ? 32 : (d == 2 ? 16 : 10);
+    // 24-bit keys (three radix passes): 2^24 Morton cells is ~16 per node at
+    // N = 1M, enough for the gather locality the plan is for
+    const int bits = d == 1 ? 24 : (d == 2 ? 12 : 8);
     const double span = (double)((1ull << bits) - 1);
     for (int a = 0; a < d; ++a) {
         lo[a] = from_ordered_bits(bb[a]);
@@ -234,7 +236,7 @@ extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_
     MF_LAUNCH_CHECK();
     cub::DoubleBuffer<unsigned> kb(k0, k1);
     cub::DoubleBuffer<int32_t> vb(v0, order);
-    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, kb, vb, (int)N, 0, d == 3 ? 30 : 32, st));
+    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, kb, vb, (int)N, 0, 24, st));
     if (vb.Current() != order)
         MF_CUDA_CHECK(cudaMemcpyAsync(order, vb.Current(), sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
     if (inv) {
