@@ -24,6 +24,7 @@ no collective on the data path; value = all stencils / max-over-ranks time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -350,33 +351,65 @@ def main():
     torch.cuda.synchronize()
     fp64_peak = fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
 
-    # timed region: per-step events, L2 flushed between steps (outside the events)
+    # ---- stage breakdown: eager steps, events between the stages (host enqueue
+    # times recorded alongside; a stage whose host side stalls longer than the
+    # device work queued ahead of it would show the stall here)
+    gc.collect()
+    gc.disable()
     timers = []
+    for _ in range(args.steps):
+        flush.zero_()
+        y, ff, n_rep = step(timers)
+    torch.cuda.synchronize()
+    stage = np.array([[a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])] for ev in timers])  # ms
+    host_ms = np.array(host_marks[-args.steps:])
+
+    # ---- timed region: the same step captured once as a CUDA graph and replayed
+    # K times (no host work between kernels, so host stalls cannot leak into the
+    # device time); events around each replay, L2 flushed between replays
+    # (outside the events)
     launches0 = lib.mf_launch_count()
+    graph = torch.cuda.CUDAGraph()
+    cap_stream = torch.cuda.Stream()
+    cap_stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap_stream):
+        with torch.cuda.graph(graph, stream=cap_stream):
+            g_out = step()
+    torch.cuda.current_stream().wait_stream(cap_stream)
+    launches = lib.mf_launch_count() - launches0  # our kernels per step (captured once)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert int(g_out[1].item()) == _lib.SENTINEL_OK, "shape solve reported a failing stencil (graph)"
+    assert torch.equal(g_out[0], y), "graph replay differs from the eager step"
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
+        for e0, e1 in ev_pairs:
             flush.zero_()
-            y, ff, n_rep = step(timers)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = (lib.mf_launch_count() - launches0) // args.steps
-    stage = np.array([[a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])] for ev in timers])  # ms
+    gc.enable()
+    step_list = [a.elapsed_time(b) for a, b in ev_pairs]
     if os.environ.get("MF_BENCH_DEBUG"):
         print("[debug] per-step stage ms (knn, shape, csr+plan, apply):\n" + np.array2string(stage, precision=2),
               file=sys.stderr)
-        print("[debug] per-step host ms to enqueue each stage:\n" + np.array2string(np.array(host_marks), precision=2),
+        print("[debug] per-step host ms to enqueue each stage:\n" + np.array2string(host_ms, precision=2),
               file=sys.stderr)
-    step_ms = float(stage.sum(axis=1).mean())
+        print("[debug] graph steps ms: " + " ".join(f"{t:.3f}" for t in step_list), file=sys.stderr)
+    step_ms = float(np.mean(step_list))
     t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     step_ms_max = float(t_local.item())
     value = world * N / (step_ms_max * 1e-3)
-    n_replayed = int(n_rep.item())
+    n_replayed = int(g_out[2].item())
 
     knn_ms, phs_ms, csr_ms, apply_ms = (float(x) for x in stage.mean(axis=0))
     F = flops_per_stencil(n, l, 1)
@@ -405,15 +438,19 @@ def main():
             return store_h.apply_all("laplacian", u_pin)
 
         e2e_step()
+        e2e_step()
         torch.cuda.synchronize()
+        gc.collect()
+        gc.disable()
         ts = []
-        for _ in range(max(3, min(args.steps, 5))):
+        for _ in range(max(5, min(args.steps, 10))):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             y_h = e2e_step()
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
+        gc.enable()
         # median step: host-side hiccups (allocator, GC) hit single wall-clock steps
         e2e_t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -465,6 +502,14 @@ def main():
                                      "loads and issue, not by these bytes"},
             "replayed_stencils": n_replayed,
             "gpu_launches": int(launches),
+            "timing": {"value_from": f"{args.steps} replays of the step captured as one CUDA graph "
+                                     "(device events around each replay, L2 flushed between)",
+                       "steps_ms": [round(t, 4) for t in step_list],
+                       "spread": (max(step_list) - min(step_list)) / float(np.median(step_list)),
+                       "eager_ms_per_step": float(stage.sum(axis=1).mean()),
+                       "eager_steps_ms": [round(float(t), 4) for t in stage.sum(axis=1)],
+                       "eager_host_enqueue_ms": [round(float(t), 3) for t in host_ms.sum(axis=1)],
+                       "stage_ms_from": "eager steps, events between stages"},
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -145,8 +145,35 @@ def ptr(t) -> int | None:
     raise TypeError(type(t))
 
 
+_WORKSPACES: dict = {}
+
+
 def workspace(nbytes: int) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device())
+    """Scratch bytes for one C-ABI call, reused across calls on the same stream.
+
+    Every entry point uses its workspace only for work it enqueues on the
+    caller's stream, so the next call on that stream may take the same buffer;
+    the buffer grows to the largest request and is kept (release_workspaces()
+    drops them).  No call's outputs live in it.
+    """
+    dev = device()
+    stream = torch.cuda.current_stream(dev)
+    key = (dev.index, stream.cuda_stream)
+    buf = _WORKSPACES.get(key)
+    need = max(int(nbytes), 1)
+    if buf is None or buf.numel() < need:
+        if buf is not None:
+            del _WORKSPACES[key]
+            buf = None
+        # round up (1 MiB) so small growth does not reallocate every call
+        buf = torch.empty(((need + (1 << 20) - 1) >> 20) << 20, dtype=torch.uint8, device=dev)
+        _WORKSPACES[key] = buf
+    return buf[:need]
+
+
+def release_workspaces() -> None:
+    """Free the cached per-stream workspaces."""
+    _WORKSPACES.clear()
 
 
 _COPY_STREAM = None

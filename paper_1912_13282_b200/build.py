@@ -16,7 +16,7 @@ REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmeshfree_b200.so")
 SOURCES = ["api.cu", "knn.cu", "phs.cu", "phs_reg.cu", "phs_reg_c3.cu", "phs_reg_c14.cu", "phs_reg_c2.cu", "sparse.cu", "plan.cu", "phs_cta.cu"]
-HEADERS = ["common.cuh", "phs_params.cuh", "phs_reg.cuh", "phs_mma.cuh", "phs_split.cuh", "phs_ns.cuh", "phs_ns2.cuh"]
+HEADERS = ["common.cuh", "phs_params.cuh", "phs_reg.cuh", "phs_nullspace.cuh", "phs_ns2.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

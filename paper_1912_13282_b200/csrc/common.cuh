@@ -28,6 +28,27 @@ void set_error(const char* fmt, ...);
     } while (0)
 
 void count_launch();
+
+// Per-device properties, queried once per device (launchers size grids from them
+// on every call; the runtime queries are not free on the enqueue path).
+int dev_sms();            // multiprocessor count of the current device
+int dev_max_smem_optin(); // opt-in dynamic shared memory per block
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device) and
+// size; returns cudaSuccess or the error of the first call.
+cudaError_t ensure_smem_attr(const void* kernel, int bytes);
+template <class K>
+inline cudaError_t ensure_smem(K* kernel, int bytes) { return ensure_smem_attr((const void*)kernel, bytes); }
+// resident blocks per SM of (kernel, block size, dynamic smem), queried once
+int occupancy_attr(const void* kernel, int threads, size_t smem);
+template <class K>
+inline int occupancy(K* kernel, int threads, size_t smem) { return occupancy_attr((const void*)kernel, threads, smem); }
+// grid for a grid-stride kernel: ceil(work / threads) blocks, capped at per_sm per SM
+inline int grid_cap(int64_t work, int threads, int per_sm) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)dev_sms() * per_sm;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
 #define MF_LAUNCH_CHECK()             \
     do {                              \
         ::mf::count_launch();         \

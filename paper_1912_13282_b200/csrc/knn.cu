@@ -872,15 +872,7 @@ __global__ void knn_target_gather(const double* __restrict__ pos, int d, const i
         for (int a = 0; a < d; ++a) tpos[w * d + a] = pos[node * d + a];
     }
 }
-inline int grid_for(int64_t work, int threads, int per_sm = 8) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t g = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)sms * per_sm;
-    if (g > cap) g = cap;
-    return g < 1 ? 1 : (int)g;
-}
+inline int grid_for(int64_t work, int threads, int per_sm = 8) { return grid_cap(work, threads, per_sm); }
 
 struct KnnLayout {
     GridParams* gp;
@@ -1007,38 +999,30 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     auto strd_k = big ? (d == 1 ? knn_kernel<true, 1, 32> : (d == 2 ? knn_kernel<true, 2, 32> : knn_kernel<true, 3, 32>))
                       : (d == 1 ? knn_kernel<true, 1, 16> : (d == 2 ? knn_kernel<true, 2, 16> : knn_kernel<true, 3, 16>));
     constexpr int smem_bytes = KNN_WARPS * (int)sizeof(WarpSmem);
-    MF_CUDA_CHECK(cudaFuncSetAttribute(main_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-    MF_CUDA_CHECK(cudaFuncSetAttribute(strd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    MF_CUDA_CHECK(ensure_smem(main_k, smem_bytes));
+    MF_CUDA_CHECK(ensure_smem(strd_k, smem_bytes));
     // fast passes where they apply: a cube that usually proves the K-th key
     // (2D: rho0 + 1; 3D: rho0), then the rows it hands back with one more cell of
     // half-width, then the general kernel for whatever is left
     const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
     int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
-    static const bool no_fast = [] {
-        const char* e = getenv("MF_KNN_FAST");
-        return e && e[0] == '0';
-    }();
     auto fits = [&](int rho, int slots) {
         return KNN_OCC * pow(2.0 * rho + 1.0, (double)d) <= 0.8 * 32 * slots;
     };
     const int rho1 = d == 2 ? rho0 + 1 : rho0, rho2 = rho1 + 1;
-    const bool fast = !no_fast && K <= 56 &&
+    const bool fast = K <= 56 &&
                       ((d == 3 && fits(rho1, 10) && fits(rho2, 28)) || (d == 2 && fits(rho1, 5) && fits(rho2, 8)));
     // (the first pass keeps only the cells that reach the proof's ball: ~0.7 of the
     // cube, so 8 slots hold it in 3D)
-    static const int kf_win = [] {
-        const char* e = getenv("MF_KNN_WIN");
-        const int v = e ? atoi(e) : 16;
-        return v < 4 ? 4 : (v > 32 ? 32 : v);
-    }();
+    constexpr int kf_win = 16;  // first-pass survivor window (bisection stops at K..K+16)
     if (fast) {
         auto f1 = d == 3 ? knn_fast<3, 8, true> : knn_fast<2, 5, true>;
         auto f2 = d == 3 ? knn_fast<3, 28, false> : knn_fast<2, 8, false>;
         const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<8>) : (int)sizeof(FastSmem<5>));
         const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
-        MF_CUDA_CHECK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
-        MF_CUDA_CHECK(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2));
+        MF_CUDA_CHECK(ensure_smem(f1, sm1));
+        MF_CUDA_CHECK(ensure_smem(f2, sm2));
         knn_target_gather<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, order, T, L.tpos);
         MF_LAUNCH_CHECK();
         f1<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, sm1, st>>>(a, order, T, nullptr, K, rho1, L.fb_list[0],
@@ -1049,13 +1033,6 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
         MF_LAUNCH_CHECK();
         main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list[1], T, L.fb_count + 1, K);
         MF_LAUNCH_CHECK();
-        if (getenv("MF_KNN_DEBUG")) {
-            unsigned long long nfb[2] = {0, 0};
-            MF_CUDA_CHECK(cudaMemcpyAsync(nfb, L.fb_count, sizeof(nfb), cudaMemcpyDeviceToHost, st));
-            MF_CUDA_CHECK(cudaStreamSynchronize(st));
-            fprintf(stderr, "[mf_knn] rows handed on: %llu (rho %d -> %d), %llu (-> general) of %lld\n", nfb[0], rho1,
-                    rho2, nfb[1], (long long)T);
-        }
     } else {
         main_k<<<grid_for(T, KNN_WARPS, 64), KNN_WARPS * 32, smem_bytes, st>>>(a, order, T, nullptr, K);
         MF_LAUNCH_CHECK();

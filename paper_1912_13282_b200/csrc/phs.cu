@@ -304,34 +304,21 @@ using namespace mf;
 
 namespace {
 
-int sm_count() {
-    static int cached = 0;
-    if (!cached) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-        if (!cached) cached = 148;
-    }
-    return cached;
-}
+int sm_count() { return dev_sms(); }
 
 template <bool REPLAY>
 int launch_generic(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
                    cudaStream_t st) {
     const int s = a.n + a.P.l;
     size_t per_warp = generic_warp_doubles(a.n, a.P.d, s, a.P.nf, !REPLAY) * sizeof(double);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int max_smem = 0;
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int max_smem = dev_max_smem_optin();
     int wpb = (int)((size_t)(max_smem / 2) / per_warp);
     if (wpb > 4) wpb = 4;
     if (wpb < 1) wpb = per_warp <= (size_t)max_smem ? 1 : 0;
     MF_REQUIRE(wpb >= 1, "stencil system of size %d needs %zu bytes of shared memory (max %d)", s,
                per_warp, max_smem);
     size_t bytes = per_warp * wpb;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(phs_generic<REPLAY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bytes));
+    MF_CUDA_CHECK(ensure_smem(phs_generic<REPLAY>, (int)bytes));
     int64_t blocks = (max_count + wpb - 1) / wpb;
     int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;

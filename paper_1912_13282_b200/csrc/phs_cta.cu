@@ -15,7 +15,7 @@
 #include "common.cuh"
 #include "phs_params.cuh"
 #include "phs_reg.cuh"  // fast_rcp, fast_rsqrt
-#include "phs_ns.cuh"   // dmma_f64, monomials_reg
+#include "phs_nullspace.cuh"  // dmma_f64, monomials_reg
 
 namespace mf {
 
@@ -338,13 +338,9 @@ int launch_cta_t(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     const int nrhs = a.P.nf + (REPLAY ? 0 : 1);
     if (s + nrhs > CTA_MAXCOLS) return MF_ERR_UNSUPPORTED;
     const size_t bytes = cta_doubles(a.n, a.P.d, s, nrhs) * sizeof(double);
-    int dev = 0, max_smem = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (bytes > (size_t)max_smem) return MF_ERR_UNSUPPORTED;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(phs_cta<REPLAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    int per_sm = 0;
-    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, phs_cta<REPLAY>, CTA_THREADS, bytes));
+    if (bytes > (size_t)dev_max_smem_optin()) return MF_ERR_UNSUPPORTED;
+    MF_CUDA_CHECK(ensure_smem(phs_cta<REPLAY>, (int)bytes));
+    int per_sm = occupancy(phs_cta<REPLAY>, CTA_THREADS, bytes);
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = max_count;
     int64_t cap = (int64_t)sms * per_sm * 8;
@@ -1278,9 +1274,8 @@ int launch_ns_cta2(const PhsArgs& a, cudaStream_t st, int sms) {
             if (a.P.expos[m * DD + ax] != gl.e[m][ax]) return MF_ERR_UNSUPPORTED;
     const size_t bytes = (size_t)C::TOTAL * sizeof(double);
     auto kern = phs_ns_cta2<NN, DD, DEG, NF>;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    int per_sm = 0;
-    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CTA_THREADS, bytes));
+    MF_CUDA_CHECK(ensure_smem(kern, (int)bytes));
+    int per_sm = occupancy(kern, CTA_THREADS, bytes);
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = a.m;
     const int64_t cap = (int64_t)sms * per_sm * 8;
@@ -1296,25 +1291,16 @@ int launch_phs_ns_cta(const PhsArgs& a, cudaStream_t st, int sms) {
     // HYBRID only (rows that fail or lose definiteness are re-solved); r^3 with
     // degree >= 1 (constant and linear monomials present: l >= d + 1)
     if (!a.flag_list || a.kappa || a.P.k != 3 || a.P.even || l < a.P.d + 1 || n - l < 1) return MF_ERR_UNSUPPORTED;
-    static const bool use_v1 = [] {
-        const char* e = getenv("MF_PHS_KERNEL");
-        return e && strcmp(e, "cta1") == 0;
-    }();
-    if (!use_v1 && n == 70 && l == 35 && a.P.d == 3 && nf == 4) {
+    if (n == 70 && l == 35 && a.P.d == 3 && nf == 4) {
         const int rc = launch_ns_cta2<70, 3, 4, 4>(a, st, sms);
         if (rc != MF_ERR_UNSUPPORTED) return rc;
     }
     const NsCtaLayout L = ns_cta_layout(n, a.P.d, l, nf + 1);
     const size_t bytes = L.total * sizeof(double);
-    int dev = 0, max_smem = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (bytes > (size_t)max_smem) return MF_ERR_UNSUPPORTED;
-    // the C5 shape (n = 70, degree 4 in 3D, four families) with compile-time sizes
-    auto kern = (n == 70 && l == 35 && a.P.d == 3 && nf == 4) ? phs_ns_cta<70, 3, 35, 4> : phs_ns_cta<0, 0, 0, 0>;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    int per_sm = 0;
-    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CTA_THREADS, bytes));
+    if (bytes > (size_t)dev_max_smem_optin()) return MF_ERR_UNSUPPORTED;
+    auto kern = phs_ns_cta<0, 0, 0, 0>;
+    MF_CUDA_CHECK(ensure_smem(kern, (int)bytes));
+    int per_sm = occupancy(kern, CTA_THREADS, bytes);
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = a.m;
     const int64_t cap = (int64_t)sms * per_sm * 8;

@@ -1,8 +1,8 @@
 // Nullspace shape solve, pivots-first layout: the HYBRID first pass for the hot
-// stencil shapes (sm_100a).  Same mathematics as phs_ns.cuh (nullspace of Q^T,
-// pivot-free Gauss-Jordan on the reduced definite system); the work is ordered
-// so that every phase has instruction-level parallelism and regular shared
-// memory addressing:
+// stencil shapes (sm_100a).  Mathematics in phs_nullspace.cuh (nullspace of
+// Q^T, pivot-free Gauss-Jordan on the reduced definite system); one warp per
+// stencil, and the work is ordered so that every phase has instruction-level
+// parallelism and regular shared memory addressing:
 //
 //   0. the next stencil's node positions are staged with cp.async while the
 //      current one is solved (the index -> position gather is two dependent
@@ -22,12 +22,11 @@
 //   5. W^T v and Y v (pivot weights and the estimate's multipliers) are one
 //      small tensor-core product instead of a shared-memory reduction.
 //
-// Rounding differs from the reference's LU exactly as phs_ns.cuh does; the
-// HYBRID flags (near-coincident nodes, sensitivity estimate, failed or
+// Rounding differs from the reference's LU (phs_nullspace.cuh); the HYBRID flags (near-coincident nodes, sensitivity estimate, failed or
 // indefinite reduction, non-finite weights) are the same.
 #pragma once
 
-#include "phs_ns.cuh"
+#include "phs_nullspace.cuh"
 
 namespace mf {
 
@@ -771,9 +770,8 @@ int launch_ns2(const PhsArgs& a, cudaStream_t st, int sms) {
             if (a.P.expos[m * DD + ax] != g.e[m][ax]) return MF_ERR_UNSUPPORTED;
     if (a.P.k != 3 || a.P.even || DEG < 1) return MF_ERR_UNSUPPORTED;
     auto kern = phs_ns2<NN, DEG, DD, NF>;
-    MF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
-    int per_sm = 0;
-    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::WARPS * 32, Cfg::SMEM));
+    MF_CUDA_CHECK(ensure_smem(kern, (int)Cfg::SMEM));
+    int per_sm = occupancy(kern, Cfg::WARPS * 32, Cfg::SMEM);
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = (a.m + Cfg::WARPS - 1) / Cfg::WARPS;
     const int64_t cap = (int64_t)sms * per_sm * 4;

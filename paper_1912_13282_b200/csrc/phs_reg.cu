@@ -1,9 +1,6 @@
 // Dispatch of the register-resident shape solve (kernel template in phs_reg.cuh;
 // each hot shape is instantiated in its own translation unit, phs_reg_<shape>.cu,
 // so nvcc builds them in parallel).
-#include <cstdlib>
-#include <cstring>
-
 #include "common.cuh"
 #include "phs_params.cuh"
 
@@ -12,15 +9,6 @@ namespace mf {
 template <int NN, int DEG, int DD, int NF, bool REPLAY>
 int launch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_count, int64_t max_count,
                cudaStream_t st, int sms);
-
-template <int NN, int DEG, int DD, int NF>
-int launch_mma(const PhsArgs& a, cudaStream_t st, int sms);
-
-template <int NN, int DEG, int DD, int NF>
-int launch_split(const PhsArgs& a, cudaStream_t st, int sms);
-
-template <int NN, int DEG, int DD, int NF>
-int launch_ns(const PhsArgs& a, cudaStream_t st, int sms);
 
 template <int NN, int DEG, int DD, int NF>
 int launch_ns2(const PhsArgs& a, cudaStream_t st, int sms);
@@ -37,51 +25,16 @@ int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     return MF_ERR_UNSUPPORTED;
 }
 
-// FAST/HYBRID first pass.  Default: HYBRID runs the nullspace kernel
-// (phs_ns2.cuh; MF_PHS_KERNEL=ns1 the first version, phs_ns.cuh) where it applies, FAST (and every other shape) the register
-// rank-1 LU (phs_reg.cuh).  MF_PHS_KERNEL=lu forces the LU kernel,
-// =split the split-row LU (phs_split.cuh), =mma the tensor-core blocked LU
-// (phs_mma.cuh).
+// FAST/HYBRID first pass: HYBRID runs the nullspace kernel (phs_ns2.cuh) on the
+// shapes it is instantiated for; FAST, and HYBRID on every other shape, the
+// register rank-1 LU (phs_reg.cuh).
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms) {
-    static const int which = [] {
-        const char* e = getenv("MF_PHS_KERNEL");
-        if (e && strcmp(e, "mma") == 0) return 2;
-        if (e && strcmp(e, "split") == 0) return 3;
-        if (e && strcmp(e, "lu") == 0) return 4;
-        if (e && strcmp(e, "ns1") == 0) return 5;
-        return 1;
-    }();
-    if (which == 1) {
-        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
-        int rc = MF_ERR_UNSUPPORTED;
-        if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_ns2<35, 2, 3, 1>(a, st, sms);
-        else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_ns2<15, 2, 2, 1>(a, st, sms);
-        else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_ns2<25, 2, 2, 3>(a, st, sms);
-        if (rc != MF_ERR_UNSUPPORTED) return rc;
-    }
-    if (which == 5) {
-        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
-        int rc = MF_ERR_UNSUPPORTED;
-        if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_ns<35, 2, 3, 1>(a, st, sms);
-        else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_ns<15, 2, 2, 1>(a, st, sms);
-        else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_ns<25, 2, 2, 3>(a, st, sms);
-        if (rc != MF_ERR_UNSUPPORTED) return rc;
-    }
-    if (which == 3) {
-        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
-        if (d == 3 && n == 35 && l == 10 && nf == 1) {
-            int rc = launch_split<35, 2, 3, 1>(a, st, sms);
-            if (rc != MF_ERR_UNSUPPORTED) return rc;
-        }
-    }
-    if (which == 2) {
-        const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
-        int rc = MF_ERR_UNSUPPORTED;
-        if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_mma<35, 2, 3, 1>(a, st, sms);
-        else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_mma<15, 2, 2, 1>(a, st, sms);
-        else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_mma<25, 2, 2, 3>(a, st, sms);
-        if (rc != MF_ERR_UNSUPPORTED) return rc;
-    }
+    const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
+    int rc = MF_ERR_UNSUPPORTED;
+    if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_ns2<35, 2, 3, 1>(a, st, sms);
+    else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_ns2<15, 2, 2, 1>(a, st, sms);
+    else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_ns2<25, 2, 2, 3>(a, st, sms);
+    if (rc != MF_ERR_UNSUPPORTED) return rc;
     return dispatch_reg<false>(a, nullptr, nullptr, a.m, st, sms);
 }
 

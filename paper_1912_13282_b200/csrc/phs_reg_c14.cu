@@ -1,11 +1,8 @@
-// Register and tensor-core shape solves instantiated for n=15, degree 2, d=2, 1 family.
-#include "phs_mma.cuh"
-
+// Shape-solve kernels instantiated for n=15, degree 2, d=2, 1 family (configs C1, C4): the register LU
+// (FAST / REPLAY, phs_reg.cuh) and the nullspace HYBRID first pass (phs_ns2.cuh).
 #include "phs_ns2.cuh"
 
 namespace mf {
 MF_INSTANTIATE_REG(15, 2, 2, 1)
-MF_INSTANTIATE_MMA(15, 2, 2, 1)
-MF_INSTANTIATE_NS(15, 2, 2, 1)
 MF_INSTANTIATE_NS2(15, 2, 2, 1)
 }  // namespace mf

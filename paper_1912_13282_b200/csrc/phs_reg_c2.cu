@@ -1,11 +1,8 @@
-// Register and tensor-core shape solves instantiated for n=25, degree 2, d=2, 3 families.
-#include "phs_mma.cuh"
-
+// Shape-solve kernels instantiated for n=25, degree 2, d=2, 3 families (config C2): the register LU
+// (FAST / REPLAY, phs_reg.cuh) and the nullspace HYBRID first pass (phs_ns2.cuh).
 #include "phs_ns2.cuh"
 
 namespace mf {
 MF_INSTANTIATE_REG(25, 2, 2, 3)
-MF_INSTANTIATE_MMA(25, 2, 2, 3)
-MF_INSTANTIATE_NS(25, 2, 2, 3)
 MF_INSTANTIATE_NS2(25, 2, 2, 3)
 }  // namespace mf

@@ -176,15 +176,7 @@ __global__ void __launch_bounds__(256) plan_apply_k(const int32_t* __restrict__ 
     }
 }
 
-inline int grid_of(int64_t work, int threads, int per_sm = 8) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t g = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)sms * per_sm;
-    if (g > cap) g = cap;
-    return g < 1 ? 1 : (int)g;
-}
+inline int grid_of(int64_t work, int threads, int per_sm = 8) { return grid_cap(work, threads, per_sm); }
 
 }  // namespace mf
 
@@ -253,15 +245,11 @@ extern "C" int mf_plan_build(const int32_t* indptr, const int32_t* indices, cons
     int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
     if (total == 0 && N == 0) return MF_OK;
     int64_t work = total > N ? total : N;
-    // blocks per SM for the tile build (C3 plan, order + ELL: 444 us element-wise;
-    // tile build 570 / 429 / 361 / 338 / 355 / 600 us at 2 / 3 / 4 / 5 / 6 / 8
-    // blocks per SM -- the L1 reuse collapses beyond that); 0 = element-wise
-    static const int variant = [] {
-        const char* e = getenv("MF_PLAN_BUILD");
-        return e ? atoi(e) : 5;
-    }();
-    if (variant >= 1 && W > 0)
-        plan_ell_build_tile<<<grid_of((N + 31) / 32 * 256, 256, variant), 256, 0,
+    // the tile build at 5 blocks per SM (C3 plan, order + ELL: 570 / 429 / 361 / 338
+    // / 355 / 600 us at 2 / 3 / 4 / 5 / 6 / 8 blocks per SM, 444 us element-wise);
+    // rows without a width (W = 0) only need their lengths
+    if (W > 0)
+        plan_ell_build_tile<<<grid_of((N + 31) / 32 * 256, 256, 5), 256, 0,
                               (cudaStream_t)stream>>>(indptr, indices, data, N, W, order, inv, ell_idx, ell_val,
                                                       ell_len);
     else

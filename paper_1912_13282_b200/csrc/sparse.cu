@@ -514,15 +514,7 @@ __global__ void heat_pack_k(const int32_t* __restrict__ ell_len, const int32_t* 
     }
 }
 
-inline int grid_for(int64_t work, int threads, int per_sm = 16) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t g = (work + threads - 1) / threads;
-    int64_t cap = (int64_t)sms * per_sm;
-    if (g > cap) g = cap;
-    return g < 1 ? 1 : (int)g;
-}
+inline int grid_for(int64_t work, int threads, int per_sm = 16) { return grid_cap(work, threads, per_sm); }
 
 }  // namespace mf
 
@@ -656,19 +648,11 @@ extern "C" int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, con
     cudaStream_t st = (cudaStream_t)stream;
     MF_CUDA_CHECK(cudaMemsetAsync(peaks, 0, sizeof(uint64_t) * steps, st));
     // blocks per SM: the packed loop runs fastest at 4 x 256 threads (C4: 35 vs
-    // 37-45 ms at 3, 5, 6, 8 or 16; MF_HEAT_BPS overrides, 0 = one row per thread)
-    static const int bps_env = [] {
-        const char* e = getenv("MF_HEAT_BPS");
-        return e ? atoi(e) : -1;
-    }();
-    const int bps = bps_env >= 0 ? bps_env : (pack ? 4 : 8);
-    const int grid = bps > 0 ? grid_for(((N + 31) / 32) * 32, 256, bps) : (int)(((N + 31) / 32 * 32 + 255) / 256);
+    // 37-45 ms at 3, 5, 6, 8 or 16); the unpacked ones at 8
+    const int grid = grid_for(((N + 31) / 32) * 32, 256, pack ? 4 : 8);
     const bool has_nm = nm && nm->count > 0;
-    static const bool pdl_env = [] {
-        const char* e = getenv("MF_HEAT_PDL");
-        return !(e && atoi(e) == 0);
-    }();
-    const bool pdl = pdl_env && !has_nm;
+    // programmatic dependent launch chains the packed steps (not with the Neumann pass in between)
+    const bool pdl = !has_nm;
     double* buf[2] = {u, scratch};
     for (int64_t s = 0; s < steps; ++s) {
         const unsigned long long* prev = s ? (const unsigned long long*)(peaks + s - 1) : nullptr;

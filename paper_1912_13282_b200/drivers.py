@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 
 import numpy as np
 import torch
@@ -24,6 +23,9 @@ from .errors import ConfigError, InstabilityError, NumericalError
 from .storage import _to_host
 
 BLOWUP_LIMIT = 1e12
+# the loop runs over the packed operator (16-bit column offsets) when rows fit it;
+# tests switch it off to compare against the unpacked plan (the sums are identical)
+PACK_OPERATOR = True
 
 
 def _bc_values(value, points, t):
@@ -157,7 +159,7 @@ def run_heat_explicit(
     # packed operator (16-bit column offsets, one meta byte per row) for the
     # loop when the rows fit it; the sums are unchanged
     pack = None
-    if steps >= 8 and 0 < plan.W <= 16 and os.environ.get("MF_HEAT_PACK", "1") != "0":
+    if steps >= 8 and 0 < plan.W <= 16 and PACK_OPERATOR:
         d16 = torch.empty(max(plan.ell_idx.numel(), 1), dtype=torch.int16, device=dev)
         meta = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
         wide = torch.empty(max((n + 31) // 32, 1), dtype=torch.uint8, device=dev)

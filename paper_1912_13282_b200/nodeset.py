@@ -202,18 +202,26 @@ class NodeSet:
                 all_sizes |= {len(blkobj.row(int(k))) for k in rows}
             if len(all_sizes) != 1:
                 raise StencilError(f"stencil sizes differ: {sorted(all_sizes)}")
-        if used.size == 1:
-            mat = self._blocks[int(used[0])].device_matrix()
-            rows = self._row[idx]
-            if rows.shape[0] == mat.shape[0] and np.array_equal(rows, np.arange(rows.shape[0])):
+        n = len(self._blocks[int(blk[0])].row(int(self._row[idx[0]])))
+
+        def rows_of(b, sel_rows):
+            """Device (k, n) int32 stencils of block b's rows sel_rows: blocks held as
+            host rows upload only the selected rows (they may mix stencil sizes)."""
+            blkobj = self._blocks[int(b)]
+            if blkobj.mat is None:
+                host = np.stack([blkobj.row(int(k)) for k in sel_rows]).astype(np.int32)
+                return _lib.to_device(host, torch.int32)
+            mat = blkobj.mat
+            if sel_rows.shape[0] == mat.shape[0] and np.array_equal(sel_rows, np.arange(sel_rows.shape[0])):
                 return mat
-            return mat.index_select(0, _lib.to_device(rows, torch.int64))
-        n = sizes[0]
+            return mat.index_select(0, _lib.to_device(sel_rows, torch.int64))
+
+        if used.size == 1:
+            return rows_of(used[0], self._row[idx])
         out = torch.empty((idx.shape[0], n), dtype=torch.int32, device=_lib.device())
         for b in used:
             sel = np.flatnonzero(blk == b)
-            src = self._blocks[int(b)].device_matrix().index_select(0, _lib.to_device(self._row[idx[sel]], torch.int64))
-            out.index_copy_(0, _lib.to_device(sel, torch.int64), src)
+            out.index_copy_(0, _lib.to_device(sel, torch.int64), rows_of(b, self._row[idx[sel]]))
         return out
 
     # -- basic queries ---------------------------------------------------

@@ -22,6 +22,7 @@ ConfigError: there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+from collections.abc import Mapping
 
 import numpy as np
 import torch
@@ -143,12 +144,24 @@ def _result_to_host(y: torch.Tensor, structure) -> np.ndarray:
 
 
 def _to_field(field, N):
-    """Field argument -> (device f64 tensor, was_numpy)."""
+    """Field argument -> (device f64 tensor, was_numpy).
+
+    The kernels index the field by node number without bounds checks, so a
+    device field must be a length-N vector on the current device (a shorter
+    one would be read out of bounds); host fields broadcast like numpy.
+    """
     if isinstance(field, torch.Tensor) and field.is_cuda:
+        if field.ndim != 1 or field.shape[0] != N:
+            raise ValueError(f"field of shape {tuple(field.shape)} does not match the {N} nodes")
+        if field.device != _lib.device():
+            raise ValueError(f"field on {field.device}, weights on {_lib.device()}")
         return field.to(torch.float64).contiguous(), False
     arr = np.asarray(field, dtype=float)
     if arr.shape != (N,):
-        arr = np.broadcast_to(arr, (N,))
+        try:
+            arr = np.broadcast_to(arr, (N,))
+        except ValueError:
+            raise ValueError(f"field of shape {arr.shape} does not match the {N} nodes") from None
     return _lib.to_device(arr, torch.float64), True
 
 
@@ -357,24 +370,20 @@ class DeviceCSR:
 # weight store
 # ---------------------------------------------------------------------------
 
-class _LazyValues(dict):
-    """{family: flat f64 host array aligned with cols}, copied from the device on first access."""
+class _LazyValues(Mapping):
+    """{family: flat f64 host array aligned with cols}, copied from the device on
+    first access.  A read-only Mapping: get(), items(), ==, dict(...) all go
+    through __getitem__ (the reference's ``values`` is a plain dict)."""
 
     def __init__(self, store):
-        super().__init__()
         self._store = store
+        self._host = {}
 
     def __getitem__(self, key):
-        if not dict.__contains__(self, key):
-            t = self._store._values_d[key]
-            dict.__setitem__(self, key, t.reshape(-1).cpu().numpy())
-        return dict.__getitem__(self, key)
-
-    def __contains__(self, key):
-        return key in self._store._values_d
-
-    def keys(self):
-        return self._store._values_d.keys()
+        if key not in self._host:
+            t = self._store._values_d[key]  # KeyError for unknown families, as a dict
+            self._host[key] = t.reshape(-1).cpu().numpy()
+        return self._host[key]
 
     def __iter__(self):
         return iter(self._store._values_d)
@@ -382,11 +391,11 @@ class _LazyValues(dict):
     def __len__(self):
         return len(self._store._values_d)
 
-    def items(self):
-        return [(k, self[k]) for k in self._store._values_d]
+    def copy(self):
+        return {k: self[k] for k in self}
 
-    def values(self):
-        return [self[k] for k in self._store._values_d]
+    def __repr__(self):
+        return f"{{{', '.join(repr(k) for k in self)}}} (device-backed)"
 
 
 class WeightStore:
@@ -520,7 +529,10 @@ class WeightStore:
             return self.matrix(key) @ field
         arr = np.asarray(field, dtype=float)
         if arr.shape != (self.n_nodes,):
-            arr = np.broadcast_to(arr, (self.n_nodes,))
+            try:
+                arr = np.broadcast_to(arr, (self.n_nodes,))
+            except ValueError:
+                raise ValueError(f"field of shape {arr.shape} does not match the {self.n_nodes} nodes") from None
         # the field's host-to-device copy overlaps the CSR and apply-plan builds
         u_d, ready = _lib.to_device_async(arr, torch.float64)
         mat = self.matrix(key)
@@ -653,6 +665,10 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
             raise StencilError("no node has a stencil; run find_closest_stencils first")
     else:
         rows = nodes.select(for_which).astype(np.int64)
+        if rows.size > 1 and np.unique(rows).size != rows.size:
+            # the canonical CSR keeps one row per node; the reference would store the
+            # duplicated row twice and let scipy sum both copies (a caller error)
+            raise StorageError("stored rows must be distinct node indices")
 
     fams = expand_families(families, nodes.dim)
     if isinstance(engine, dict):
@@ -678,6 +694,15 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
         groups = [(engine, fams)]
     for eng, _ in groups:
         _check_batchable(eng)
+    if rows.size == 0:
+        # nothing selected (e.g. "boundary" on a set without boundary nodes): an
+        # empty store, as the reference returns
+        dev = _lib.device()
+        empty = torch.empty((0, 0), dtype=torch.int32, device=dev)
+        return WeightStore(len(nodes), rows, empty, {k: torch.empty((0, 0), dtype=torch.float64, device=dev)
+                                                     for k in fams}, 0,
+                           rows_d=torch.empty(0, dtype=torch.int64, device=dev),
+                           positions_d=nodes.positions_device())
     if full is not None:
         stencils_d = full
         rows_d = _lib.device_arange(len(nodes))

@@ -7,7 +7,6 @@ drivers.py:99-102 applied to the same stored weights (test infrastructure).
 """
 
 import os
-import subprocess
 import sys
 
 import numpy as np
@@ -108,30 +107,6 @@ def test_vector_helpers_exact_on_linear_fields():
     assert store.divergence(vec, i) == pytest.approx(5.0, abs=1e-8)
     assert np.allclose(store.vector_laplacian(vec, i), [0.0, 0.0], atol=1e-6)
     assert np.allclose(store.grad_div(vec, i), [0.0, 0.0], atol=1e-6)
-
-
-@pytest.mark.parametrize("kernel", ["mma", "split"])
-def test_opt_in_shape_kernels(kernel):
-    """The tensor-core and split-row FAST kernels meet the same parity bar (subprocess: env is read once)."""
-    script = r"""
-import sys, numpy as np
-sys.path.insert(0, %r); sys.path.insert(0, %r)
-import paper_1912_13282_b200 as m
-from paper_1912_13282_b200 import workloads
-g = np.load(%r)
-w = workloads.make("C3")
-nodes = m.find_closest_stencils(m.NodeSet(w.positions, w.types), 35, for_which=g["targets"])
-for mode in ("fast", "hybrid"):
-    store = m.compute_weights(nodes, m.RbfFd(m.Polyharmonic(3), 2, "support", "lu", mode=mode), ["laplacian"],
-                              for_which=g["targets"])
-    ref = g["w_laplacian"]
-    err = np.max(np.abs(store.values["laplacian"].reshape(ref.shape) - ref), 1) / np.max(np.abs(ref), 1)
-    assert err.max() <= 1e-9, (mode, err.max())
-print("ok")
-""" % (REPO, os.path.join(REPO, "oracle"), os.path.join(REPO, "tests", "golden", "config_C3.npz"))
-    env = dict(os.environ, MF_PHS_KERNEL=kernel)
-    res = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
 
 
 def test_replay_mode_agreement_statistics():

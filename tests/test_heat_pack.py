@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 def test_packed_heat_bitwise_both_tile_kinds(monkeypatch):
     import paper_1912_13282_b200 as m
+    from paper_1912_13282_b200 import drivers
 
     rng = np.random.default_rng(5)
     N = 120_000
@@ -38,7 +39,7 @@ def test_packed_heat_bitwise_both_tile_kinds(monkeypatch):
     dt = 1e-12
     steps = 12
     u_pack = m.run_heat_explicit(nodes, store, dt=dt, steps=steps, dirichlet={-1: 0.25}, initial=u0)
-    monkeypatch.setenv("MF_HEAT_PACK", "0")
+    monkeypatch.setattr(drivers, "PACK_OPERATOR", False)
     u_plain = m.run_heat_explicit(nodes, store, dt=dt, steps=steps, dirichlet={-1: 0.25}, initial=u0)
     assert np.array_equal(u_pack.view(np.int64), u_plain.view(np.int64))
 
@@ -55,6 +56,7 @@ def test_packed_heat_bitwise_both_tile_kinds(monkeypatch):
 def test_packed_heat_time_dependent_matches_plain(monkeypatch):
     """Time-dependent Dirichlet data: one launch per step over the packed plan."""
     import paper_1912_13282_b200 as m
+    from paper_1912_13282_b200 import drivers
 
     rng = np.random.default_rng(9)
     N = 3001  # not a multiple of 32: a partial last tile
@@ -66,7 +68,7 @@ def test_packed_heat_time_dependent_matches_plain(monkeypatch):
     fn = lambda p, t: t * p[:, 0] + 0.5  # noqa: E731
     args = dict(dt=1e-7, steps=11, dirichlet={-1: fn}, initial=np.cos(pts[:, 1]))
     u_pack = m.run_heat_explicit(nodes, store, **args)
-    monkeypatch.setenv("MF_HEAT_PACK", "0")
+    monkeypatch.setattr(drivers, "PACK_OPERATOR", False)
     u_plain = m.run_heat_explicit(nodes, store, **args)
     assert np.array_equal(u_pack.view(np.int64), u_plain.view(np.int64))
     idx = nodes.boundary_indices()
