@@ -13,6 +13,8 @@
  *   mf_apply          storage.py:186-188            WeightStore.apply_all (scipy csr_matvec)
  *   mf_apply_rows     storage.py:174-184            WeightStore.apply (selected rows)
  *   mf_plan_*         storage.py:186-188            apply_all through a locality-ordered ELL plan
+ *   mf_*_terms        storage.py:174-222            apply / gradient / divergence / vector_laplacian /
+ *                                                   grad_div (several families and fields, one pass)
  *   mf_heat_steps     drivers.py:87-110             run_heat_explicit step loop
  *   mf_heat_pack      (none: packed operator for the heat loop, same results)
  *   mf_neumann_values storage.py:226-250            WeightStore.neumann_value (batched)
@@ -159,6 +161,32 @@ int mf_plan_build(const int32_t* indptr, const int32_t* indices, const double* d
 int mf_plan_apply(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
                   int32_t W, const int32_t* order, const double* u, double* y, double* scratch_u,
                   double* scratch_y, void* stream);
+/* ---- operator combinations over one stencil structure ----------------------------
+ * Every family of a WeightStore shares one CSR structure (and one plan).  A
+ * "terms" descriptor lists row sums s_t = (A_{fam[t]} u_{fld[t]})_i, each in
+ * the CSR's addend order from 0.0 (WeightStore.apply, storage.py:174-184), and
+ * outputs out[o]_i = ((0.0 + s_{t0[o]}) + s_{t0[o]+1}) + ... over the terms
+ * t0[o] .. t0[o+1]-1, the accumulation of gradient / divergence /
+ * vector_laplacian / grad_div (storage.py:190-222).  Pointer tables are HOST
+ * arrays copied at the call; the arrays they point to are device arrays. */
+#define MF_MAX_TERMS 16
+typedef struct {
+    int32_t nterm;                      /* <= MF_MAX_TERMS */
+    int32_t nout;                       /* <= MF_MAX_TERMS */
+    const double* val[MF_MAX_TERMS];    /* per term: the family's values (plan layout or CSR data) */
+    const double* fld[MF_MAX_TERMS];    /* per term: its field (plan order or node order) */
+    int32_t out_t0[MF_MAX_TERMS + 1];   /* output o sums terms out_t0[o] .. out_t0[o+1]-1 */
+    double* out[MF_MAX_TERMS];          /* per output: N values (plan) or count values (rows) */
+} mf_terms_t;
+/* Whole field over an apply plan: fields in plan order; outputs in node order
+ * when order is given (scattered through it), else in plan order. */
+int mf_plan_apply_terms(const int32_t* ell_idx, const int32_t* ell_len, int64_t N, int32_t W,
+                        const int32_t* order, const mf_terms_t* terms, void* stream);
+/* Selected rows sel[0..count) over the CSR (values = CSR data, fields in node
+ * order); output o gets count values. */
+int mf_apply_terms_rows(const int32_t* indptr, const int32_t* indices, const int64_t* sel, int64_t count,
+                        const mf_terms_t* terms, void* stream);
+
 /* dst[i] = src[order[i]] (scatter = 0) or dst[order[i]] = src[i] (scatter = 1) */
 int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatter, double* dst,
                void* stream);

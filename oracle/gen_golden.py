@@ -280,9 +280,75 @@ def dump_heat():
     save("heat.npz", **arrs)
 
 
+# -- vector operators and the explicit Neumann closure -----------
+
+def square_set(m=48, seed=61):
+    """Jittered grid on the unit square (jitter 0.2 h inside): interior +1;
+    left edge x = 0 tagged -2 with outward normal (-1, 0), the other three
+    edges -1 with their outward normals."""
+    rng = np.random.default_rng(seed)
+    h = 1.0 / (m - 1)
+    g = np.arange(m) * h
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    pts = np.stack([X.ravel(), Y.ravel()], 1)
+    on_b = (pts[:, 0] == 0) | (pts[:, 0] == g[-1]) | (pts[:, 1] == 0) | (pts[:, 1] == g[-1])
+    pts[~on_b] += rng.uniform(-0.2 * h, 0.2 * h, (int((~on_b).sum()), 2))
+    types = np.where(on_b, -1, 1).astype(np.int64)
+    left = pts[:, 0] == 0
+    types[left] = -2
+    normals = np.full(pts.shape, np.nan)
+    normals[left] = (-1.0, 0.0)
+    normals[(pts[:, 0] == g[-1]) & ~left] = (1.0, 0.0)
+    normals[(pts[:, 1] == 0) & (types == -1) & (pts[:, 0] != g[-1])] = (0.0, -1.0)
+    normals[(pts[:, 1] == g[-1]) & (types == -1) & (pts[:, 0] != g[-1])] = (0.0, 1.0)
+    return pts, types, normals
+
+
+def dump_vector_ops():
+    arrs = {}
+    pts, types, normals = square_set()
+    N = pts.shape[0]
+    nodes = find_closest_stencils(NodeSet(pts, types, normals), 15)
+    eng = RbfFd(Polyharmonic(3), degree=2, scale="support", solver="lu")
+    store = compute_weights(nodes, eng, ["laplacian", "gradient", "hessian"])
+    rng = np.random.default_rng(62)
+    u = rng.standard_normal(N)
+    vec = rng.standard_normal((N, 2))
+    sample = np.sort(rng.choice(N, 300, replace=False))
+    arrs.update(pts=pts, types=types, normals=normals, u=u, vec=vec, sample=sample,
+                stencils=nodes.stencil_matrix().astype(np.int32))
+    for f in store.families:
+        arrs[f"w_{f}"] = store.values[f].reshape(N, 15)
+        arrs[f"y_{f}"] = store.apply_all(f, u)
+    arrs["apply_lap"] = np.array([store.apply("laplacian", u, int(i)) for i in sample])
+    arrs["gradient"] = np.stack([store.gradient(u, int(i)) for i in sample])
+    arrs["divergence"] = np.array([store.divergence(vec, int(i)) for i in sample])
+    arrs["vector_laplacian"] = np.stack([store.vector_laplacian(vec, int(i)) for i in sample])
+    arrs["grad_div"] = np.stack([store.grad_div(vec, int(i)) for i in sample])
+    bnd = np.flatnonzero(types < 0)
+    gn = np.linspace(-0.5, 0.5, bnd.size)
+    arrs["neumann_nodes"] = bnd
+    arrs["neumann_gn"] = gn
+    arrs["neumann_values"] = np.array([store.neumann_value(u, int(i), normals[i], g) for i, g in zip(bnd, gn)])
+    arrs["normal_comb"] = np.stack([store.normal_combination(int(i), normals[i]) for i in bnd[:40]])
+    # heat with Neumann on the hole and Dirichlet on the outer circle (drivers.py:99-102)
+    from scipy.spatial import cKDTree
+    hmin = float(cKDTree(pts).query(pts, k=2)[0][:, 1].min())
+    dt = 0.1 * hmin * hmin
+    u0 = np.exp(-4.0 * np.sum((pts - 0.3) ** 2, axis=1))
+    arrs["heat_dt"] = np.array(dt)
+    arrs["heat_u0"] = u0
+    arrs["heat_neumann"] = run_heat_explicit(nodes, store, dt=dt, steps=30, dirichlet={-1: 0.0},
+                                             neumann={-2: 0.3}, initial=u0)
+    arrs["heat_neumann_fn"] = run_heat_explicit(nodes, store, dt=dt, steps=20, diffusivity=0.5,
+                                                dirichlet={-1: lambda p, t: p[:, 0] * (1.0 + t)},
+                                                neumann={-2: lambda p, t: p[:, 1] + t}, initial=u0)
+    save("vector_ops.npz", **arrs)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat"]
+    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector"]
     if "knn" in which:
         dump_knn()
     if "variants" in which:
@@ -293,5 +359,7 @@ if __name__ == "__main__":
         dump_csr_apply()
     if "heat" in which:
         dump_heat()
+    if "vector" in which:
+        dump_vector_ops()
     if "configs" in which:
         dump_configs()

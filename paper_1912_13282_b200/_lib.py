@@ -41,6 +41,15 @@ class NeumannT(ctypes.Structure):
     ]
 
 
+MF_MAX_TERMS = 16
+
+
+class TermsT(ctypes.Structure):
+    """mf_terms_t (include/meshfree_b200.h): row sums of (family, field) terms, summed per output."""
+    _fields_ = [("nterm", _I32), ("nout", _I32), ("val", _P * MF_MAX_TERMS), ("fld", _P * MF_MAX_TERMS),
+                ("out_t0", _I32 * (MF_MAX_TERMS + 1)), ("out", _P * MF_MAX_TERMS)]
+
+
 class HeatPackT(ctypes.Structure):
     """mf_heat_pack_t (include/meshfree_b200.h)."""
     _fields_ = [("ell_d16", _P), ("meta", _P), ("tile_wide", _P)]
@@ -67,6 +76,8 @@ _SIGNATURES = {
     "mf_plan_build": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "mf_plan_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "mf_permute": ([_P, _P, _I64, _I32, _P, _P], _I32),
+    "mf_plan_apply_terms": ([_P, _P, _I64, _I32, _P, ctypes.POINTER(TermsT), _P], _I32),
+    "mf_apply_terms_rows": ([_P, _P, _P, _I64, ctypes.POINTER(TermsT), _P], _I32),
     "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
     "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),

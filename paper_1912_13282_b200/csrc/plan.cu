@@ -178,6 +178,72 @@ __global__ void __launch_bounds__(256) plan_apply_k(const int32_t* __restrict__ 
 
 inline int grid_of(int64_t work, int threads, int per_sm = 8) { return grid_cap(work, threads, per_sm); }
 
+// ---- operator combinations (storage.py:174-222) ------------------------------
+// One pass over the shared index stream: per entry one column index, then per
+// term one value and one field load; each term's sum runs in the row's addend
+// order from 0.0 (separately rounded multiply and add), outputs add their terms
+// in order onto 0.0.  NT = number of terms (compile time: the sums stay in
+// registers); the plan variant scatters outputs to node order through `order`.
+struct TermsDev {
+    const double* val[MF_MAX_TERMS];
+    const double* fld[MF_MAX_TERMS];
+    double* out[MF_MAX_TERMS];
+    int t0[MF_MAX_TERMS + 1];
+    int nout;
+};
+
+template <int NT>
+__device__ __forceinline__ void terms_finish(const TermsDev& T, const double (&s)[NT], int64_t dst) {
+    for (int o = 0; o < T.nout; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if (t >= T.t0[o] && t < T.t0[o + 1]) acc = __dadd_rn(acc, s[t]);
+        T.out[o][dst] = acc;
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) plan_terms_k(const int32_t* __restrict__ ell_idx,
+                                                    const int32_t* __restrict__ ell_len, int64_t N, int W,
+                                                    const int32_t* __restrict__ order, const TermsDev T) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        const int len = ell_len[r];
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double s[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) s[t] = 0.0;
+        for (int j = 0; j < len; ++j) {
+            const int64_t e = base + 32 * j;
+            const int32_t c = __ldcs(ell_idx + e);
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                s[t] = __dadd_rn(s[t], __dmul_rn(__ldcs(T.val[t] + e), __ldg(T.fld[t] + c)));
+        }
+        terms_finish<NT>(T, s, order ? (int64_t)order[r] : r);
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(128) rows_terms_k(const int32_t* __restrict__ indptr,
+                                                    const int32_t* __restrict__ indices,
+                                                    const int64_t* __restrict__ sel, int64_t count, const TermsDev T) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride) {
+        const int64_t i = sel[k];
+        double s[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) s[t] = 0.0;
+        for (int32_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            const int32_t c = indices[p];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) s[t] = __dadd_rn(s[t], __dmul_rn(T.val[t][p], T.fld[t][c]));
+        }
+        terms_finish<NT>(T, s, k);
+    }
+}
+
 }  // namespace mf
 
 using namespace mf;
@@ -278,6 +344,81 @@ extern "C" int mf_plan_apply(const int32_t* ell_idx, const double* ell_val, cons
     plan_scatter<<<grid_of(N, 256), 256, 0, st>>>(scratch_y, order, N, y);
     MF_LAUNCH_CHECK();
     return MF_OK;
+}
+
+namespace {
+int terms_dev(const mf_terms_t* t, TermsDev& T) {
+    MF_REQUIRE(t && t->nterm >= 1 && t->nterm <= MF_MAX_TERMS && t->nout >= 1 && t->nout <= MF_MAX_TERMS,
+               "mf_*_terms: bad term / output counts");
+    MF_REQUIRE(t->out_t0[0] == 0 && t->out_t0[t->nout] == t->nterm, "mf_*_terms: outputs must cover the terms in order");
+    for (int o = 0; o < t->nout; ++o) {
+        MF_REQUIRE(t->out_t0[o] <= t->out_t0[o + 1] && t->out[o], "mf_*_terms: bad output %d", o);
+        T.out[o] = t->out[o];
+        T.t0[o] = t->out_t0[o];
+    }
+    T.t0[t->nout] = t->out_t0[t->nout];
+    for (int k = 0; k < t->nterm; ++k) {
+        MF_REQUIRE(t->val[k] && t->fld[k], "mf_*_terms: term %d has no values or field", k);
+        T.val[k] = t->val[k];
+        T.fld[k] = t->fld[k];
+    }
+    for (int k = t->nterm; k < MF_MAX_TERMS; ++k) T.val[k] = T.val[0], T.fld[k] = T.fld[0];
+    T.nout = t->nout;
+    return MF_OK;
+}
+
+template <template <int> class L, class... A>
+int dispatch_nt(int nt, A... a) {
+    switch (nt) {
+        case 1: return L<1>::go(a...);
+        case 2: return L<2>::go(a...);
+        case 3: return L<3>::go(a...);
+        case 4: return L<4>::go(a...);
+        case 5: case 6: return L<6>::go(a...);
+        case 7: case 8: case 9: return L<9>::go(a...);
+        default: return L<16>::go(a...);
+    }
+}
+
+template <int NT>
+struct PlanTermsL {
+    static int go(const int32_t* idx, const int32_t* len, int64_t N, int W, const int32_t* order, const TermsDev* T,
+                  cudaStream_t st) {
+        plan_terms_k<NT><<<grid_of(N, 256), 256, 0, st>>>(idx, len, N, W, order, *T);
+        MF_LAUNCH_CHECK();
+        return MF_OK;
+    }
+};
+template <int NT>
+struct RowsTermsL {
+    static int go(const int32_t* ip, const int32_t* ix, const int64_t* sel, int64_t count, const TermsDev* T,
+                  cudaStream_t st) {
+        rows_terms_k<NT><<<grid_of(count, 128), 128, 0, st>>>(ip, ix, sel, count, *T);
+        MF_LAUNCH_CHECK();
+        return MF_OK;
+    }
+};
+}  // namespace
+
+extern "C" int mf_plan_apply_terms(const int32_t* ell_idx, const int32_t* ell_len, int64_t N, int32_t W,
+                                   const int32_t* order, const mf_terms_t* terms, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0, "mf_plan_apply_terms: bad arguments");
+    TermsDev T{};
+    int rc = terms_dev(terms, T);
+    if (rc != MF_OK || N == 0) return rc;
+    // unused term slots (NT rounded up) add 0 * field to a sum nobody reads
+    return dispatch_nt<PlanTermsL>(terms->nterm, ell_idx, ell_len, N, (int)W, order, (const TermsDev*)&T,
+                                   (cudaStream_t)stream);
+}
+
+extern "C" int mf_apply_terms_rows(const int32_t* indptr, const int32_t* indices, const int64_t* sel, int64_t count,
+                                   const mf_terms_t* terms, void* stream) {
+    MF_REQUIRE(count >= 0, "mf_apply_terms_rows: bad count");
+    TermsDev T{};
+    int rc = terms_dev(terms, T);
+    if (rc != MF_OK || count == 0) return rc;
+    return dispatch_nt<RowsTermsL>(terms->nterm, indptr, indices, sel, count, (const TermsDev*)&T,
+                                   (cudaStream_t)stream);
 }
 
 extern "C" int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatter, double* dst,

@@ -538,7 +538,7 @@ extern "C" int mf_csr_workspace_size(int64_t N, size_t* bytes) {
 extern "C" int mf_csr_build(const int64_t* rows, const int32_t* stencils, int64_t m, int32_t n, int64_t N,
                             int32_t* indptr, int32_t* indices, int32_t* perm, int32_t* dup_flag, void* ws,
                             size_t ws_bytes, void* stream) {
-    MF_REQUIRE(n >= 1 && m >= 0 && N >= 0, "mf_csr_build: bad shape");
+    MF_REQUIRE((n >= 1 || m == 0) && m >= 0 && N >= 0, "mf_csr_build: bad shape");
     MF_REQUIRE((double)m * n < 2147483647.0, "mf_csr_build: nnz %lld exceeds int32 indexing", (long long)(m * n));
     cudaStream_t st = (cudaStream_t)stream;
     MF_REQUIRE(N < 2147483647, "mf_csr_build: N exceeds int32 indexing");

@@ -510,18 +510,14 @@ class WeightStore:
 
     # -- explicit application ---------------------------------------------
 
-    def apply(self, key: str, field, i: int) -> float:
-        """(L u)(p_i) from stored weights; matches the assembled matrix row bitwise."""
-        mat = self.matrix(key)
-        if self.node_row[i] < 0:
-            raise StorageError(f"no weights stored for node {i}")
-        u_d, _ = _to_field(field, self.n_nodes)
-        sel = torch.tensor([int(i)], dtype=torch.int64, device=u_d.device)
-        y = torch.empty(1, dtype=torch.float64, device=u_d.device)
-        _lib.check(_lib.load().mf_apply_rows(mat.indptr_device.data_ptr(), mat.indices_device.data_ptr(),
-                                             mat.data_device.data_ptr(), u_d.data_ptr(), sel.data_ptr(), 1,
-                                             y.data_ptr(), _lib.stream_ptr()), "mf_apply_rows")
-        return float(y.item())
+    def apply(self, key: str, field, i):
+        """(L u)(p_i) from stored weights; matches the assembled matrix row bitwise.
+
+        ``i`` an int gives a float (the reference's call); an index array gives
+        the values at those nodes from one launch."""
+        scalar = np.ndim(i) == 0
+        out = self._combine([[(key, 0)]], [field], i)
+        return float(out[0][0]) if scalar else out[0]
 
     def apply_all(self, key: str, field):
         """(L u) at every stored node as a length-N vector (zeros elsewhere)."""
@@ -541,33 +537,122 @@ class WeightStore:
         y = mat.apply_device(u_d)
         return _result_to_host(y, mat._s)
 
-    def gradient(self, field, i: int):
-        d = self._dim()
-        return np.array([self.apply(f"d1_{a}", field, i) for a in range(d)])
+    def apply_families(self, keys, field):
+        """{key: L_key u} at every stored node for several families in ONE pass
+        over the shared stencil structure (index stream and field gathers read
+        once); each result is bitwise apply_all(key, field)."""
+        keys = list(keys)
+        out = self._combine([[(k, 0)] for k in keys], [field], None)
+        return dict(zip(keys, out))
 
-    def divergence(self, vec_field, i: int) -> float:
-        vec_field = np.asarray(vec_field, dtype=float)
-        d = self._dim()
-        acc = 0.0
-        for a in range(d):
-            acc += self.apply(f"d1_{a}", vec_field[:, a], i)
-        return acc
+    # -- vector calculus (storage.py:190-222).  ``i`` an int: the reference's
+    # per-node result; an index array: those nodes; None: the whole field
+    # (zeros at nodes without weights), each from one launch.
 
-    def vector_laplacian(self, vec_field, i: int):
-        vec_field = np.asarray(vec_field, dtype=float)
-        d = vec_field.shape[1]
-        return np.array([self.apply("laplacian", vec_field[:, a], i) for a in range(d)])
-
-    def grad_div(self, vec_field, i: int):
-        """grad(div u) at node i; needs the hessian families."""
-        vec_field = np.asarray(vec_field, dtype=float)
+    def gradient(self, field, i=None):
         d = self._dim()
-        out = np.zeros(d)
-        for a in range(d):
-            for b in range(d):
-                key = f"d2_{min(a, b)}_{max(a, b)}"
-                out[a] += self.apply(key, vec_field[:, b], i)
-        return out
+        out = self._combine([[(f"d1_{a}", 0)] for a in range(d)], [field], i)
+        return self._shape_out(out, i)
+
+    def divergence(self, vec_field, i=None):
+        d = self._dim()
+        cols = self._components(vec_field, d)
+        out = self._combine([[(f"d1_{a}", a) for a in range(d)]], cols, i)
+        return float(out[0][0]) if np.ndim(i) == 0 and i is not None else out[0]
+
+    def vector_laplacian(self, vec_field, i=None):
+        vec = vec_field if isinstance(vec_field, torch.Tensor) else np.asarray(vec_field, dtype=float)
+        d = int(vec.shape[1])
+        cols = self._components(vec, d)
+        out = self._combine([[("laplacian", a)] for a in range(d)], cols, i)
+        return self._shape_out(out, i)
+
+    def grad_div(self, vec_field, i=None):
+        """grad(div u); needs the hessian families."""
+        d = self._dim()
+        cols = self._components(vec_field, d)
+        spec = [[(f"d2_{min(a, b)}_{max(a, b)}", b) for b in range(d)] for a in range(d)]
+        out = self._combine(spec, cols, i)
+        return self._shape_out(out, i)
+
+    @staticmethod
+    def _shape_out(out, i):
+        if i is not None and np.ndim(i) == 0:
+            return np.array([float(o[0]) for o in out])
+        return np.stack(out, axis=-1) if isinstance(out[0], np.ndarray) else torch.stack(out, dim=-1)
+
+    def _components(self, vec_field, d):
+        if isinstance(vec_field, torch.Tensor) and vec_field.is_cuda:
+            if vec_field.ndim != 2 or vec_field.shape[1] < d:
+                raise ValueError(f"vector field of shape {tuple(vec_field.shape)} has fewer than {d} components")
+            return [vec_field[:, a] for a in range(d)]
+        vec = np.asarray(vec_field, dtype=float)
+        if vec.ndim != 2 or vec.shape[1] < d:
+            raise ValueError(f"vector field of shape {vec.shape} has fewer than {d} components")
+        return [np.ascontiguousarray(vec[:, a]) for a in range(d)]
+
+    def _combine(self, spec, fields, i):
+        """Outputs o = ((0.0 + s_o0) + s_o1) + ... with s = row sums of (family,
+        field index) terms (spec: list of outputs, each a list of terms), at node
+        i / nodes i / every node (i None).  Returns host arrays for host fields,
+        device tensors for device fields."""
+        terms = [t for o in spec for t in o]
+        if len(terms) > _lib.MF_MAX_TERMS or len(spec) > _lib.MF_MAX_TERMS:
+            raise ConfigError(f"at most {_lib.MF_MAX_TERMS} terms per combination")
+        for key, _ in terms:
+            self._family(key)
+        device_in = all(isinstance(f, torch.Tensor) and f.is_cuda for f in fields)
+        flds = [_to_field(f, self.n_nodes)[0] for f in fields]
+        lib = _lib.load()
+        mats = {key: self.matrix(key) for key, _ in terms}
+        s = self._structure
+        tt = _lib.TermsT()
+        tt.nterm, tt.nout = len(terms), len(spec)
+        t0 = 0
+        for o, out_terms in enumerate(spec):
+            tt.out_t0[o] = t0
+            t0 += len(out_terms)
+        tt.out_t0[len(spec)] = t0
+        dev = flds[0].device
+        if i is None:
+            order, _, ell_idx, ell_len = s.plan(True)
+            n = self.n_nodes
+            if order is not None:
+                plan_f = []
+                for f in flds:
+                    g = torch.empty(n, dtype=torch.float64, device=dev)
+                    _lib.check(lib.mf_permute(f.data_ptr(), order.data_ptr(), n, 0, g.data_ptr(),
+                                              _lib.stream_ptr()), "mf_permute")
+                    plan_f.append(g)
+            else:
+                plan_f = flds
+            outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in spec]
+            for k, (key, fi) in enumerate(terms):
+                tt.val[k] = mats[key].plan(True).ell_val.data_ptr()
+                tt.fld[k] = plan_f[fi].data_ptr()
+            for o, y in enumerate(outs):
+                tt.out[o] = y.data_ptr()
+            _lib.check(lib.mf_plan_apply_terms(ell_idx.data_ptr(), ell_len.data_ptr(), n, s.n,
+                                               _lib.ptr(order), ctypes.byref(tt), _lib.stream_ptr()),
+                       "mf_plan_apply_terms")
+        else:
+            sel = np.atleast_1d(np.asarray(i, dtype=np.int64))
+            for node in sel:
+                self._row(int(node))  # StorageError for nodes without weights, as the reference
+            sel_d = _lib.to_device(sel, torch.int64)
+            outs = [torch.empty(max(sel.size, 1), dtype=torch.float64, device=dev)[: sel.size] for _ in spec]
+            for k, (key, fi) in enumerate(terms):
+                tt.val[k] = mats[key].data_device.data_ptr()
+                tt.fld[k] = flds[fi].data_ptr()
+            for o, y in enumerate(outs):
+                tt.out[o] = y.data_ptr()
+            _lib.check(lib.mf_apply_terms_rows(s.indptr.data_ptr(), s.indices.data_ptr(), sel_d.data_ptr(),
+                                               sel.size, ctypes.byref(tt), _lib.stream_ptr()),
+                       "mf_apply_terms_rows")
+        if device_in:
+            return outs
+        host = _result_to_host(torch.stack(outs) if outs else outs, s)
+        return [host[o] for o in range(len(spec))]
 
     def _dim(self) -> int:
         axes = [int(k[3:]) for k in self._values_d if k.startswith("d1_")]
