@@ -246,6 +246,63 @@ int mf_heat_steps(const int32_t* ell_len, const int32_t* ell_idx, const double* 
                   int64_t steps, double* u, double* scratch, uint64_t* peaks, const mf_heat_pack_t* pack,
                   void* stream);
 
+/* ---- general weight engines (the reference's per-node loop) ---------------------
+ * Replaces the per-node engine loop _run_loop (storage.py:325-339) over
+ * RbfFd.weights (approx/engines.py:147-201) and WeightedLeastSquares.weights
+ * (approx/engines.py:102-145): every configuration batch_phs_weights does not
+ * take -- the qr / svd solvers (the reference's default is qr), Gaussian /
+ * multiquadric / inverse multiquadric / r^k (k <= 2) kernels, weighted least
+ * squares, composite operators (ScaledOperator / OperatorSum / Directional).
+ * One warp per stencil; every family is solved from one factorisation.
+ * out is m x nf x n f64 in stencil order; status is m x nf int8:
+ *   0 ok, 1 non-finite weights, 2 degenerate scale (all nodes on the centre),
+ *   3 polyharmonic derivative singular at the centre (k <= 2, basis.py:180-186),
+ *   4 least-squares weight function not positive (engines.py:131-132);
+ * first_fail (device int64) receives the lowest failing row, or
+ * 0x7f7f7f7f7f7f7f7f. */
+#define MF_ENGINE_RBFFD 0
+#define MF_ENGINE_WLS 1
+#define MF_RBF_PHS 0
+#define MF_RBF_GAUSSIAN 1
+#define MF_RBF_MQ 2
+#define MF_RBF_IMQ 3
+#define MF_WEIGHT_CONSTANT 0
+#define MF_WEIGHT_GAUSSIAN 1
+#define MF_SOLVER_LU 0
+#define MF_SOLVER_QR 1
+#define MF_SOLVER_SVD 2
+#define MF_TERM_IDENTITY 0
+#define MF_TERM_D1 1
+#define MF_TERM_D2 2
+#define MF_TERM_LAPLACIAN 3
+#define MF_TERM_DIRECTIONAL 4
+#define MF_MAX_ENGINE_TERMS 32
+typedef struct {
+    int32_t engine;       /* MF_ENGINE_* */
+    int32_t rbf;          /* MF_RBF_* (RbfFd) */
+    int32_t k;            /* polyharmonic exponent (odd: r^k, even: r^k log r) */
+    int32_t solver;       /* MF_SOLVER_* */
+    int32_t scale_code;   /* MF_SCALE_* */
+    int32_t weight;       /* MF_WEIGHT_* (WLS) */
+    double sigma;         /* kernel shape parameter (Gaussian / MQ / IMQ) */
+    double weight_sigma;  /* Gaussian weight shape parameter (WLS) */
+    int32_t d;            /* dimension */
+    int32_t l;            /* monomials: RbfFd augmentation (0 = none), WLS basis size */
+    int32_t expos[MF_MAX_MONOMIALS * MF_MAX_DIM]; /* exponent of monomial j on axis a at j*MF_MAX_DIM + a */
+    int32_t nf;           /* families */
+    int32_t term0[MF_MAX_FAMILIES + 1];  /* family f = elementary terms term0[f] .. term0[f+1]-1 */
+    int32_t term_kind[MF_MAX_ENGINE_TERMS];
+    int32_t term_a[MF_MAX_ENGINE_TERMS];
+    int32_t term_b[MF_MAX_ENGINE_TERMS];
+    int32_t term_order[MF_MAX_ENGINE_TERMS];
+    double term_coeff[MF_MAX_ENGINE_TERMS];
+    double term_vec[MF_MAX_ENGINE_TERMS * MF_MAX_DIM]; /* Directional vectors */
+} mf_engine_t;
+/* eng is a HOST struct (copied at the call) */
+int mf_engine_weights(const double* pos, int64_t N, const int64_t* rows, const int32_t* stencils,
+                      int64_t m, int32_t n, const mf_engine_t* eng, double* out, int8_t* status,
+                      int64_t* first_fail, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

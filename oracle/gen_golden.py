@@ -26,6 +26,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
 
 import meshfree  # noqa: E402  (the reference, from PYTHONPATH)
 import numba  # noqa: E402
@@ -346,9 +347,44 @@ def dump_vector_ops():
     save("vector_ops.npz", **arrs)
 
 
+# -- general engines (the reference's per-node loop, storage.py:325-339) --------
+
+from gen_golden_specs import ENGINE_ERRORS, ENGINE_VARIANTS, family_specs  # noqa: E402
+
+
+def dump_engines():
+    arrs = {}
+    arrs["names"] = np.array([v[0] for v in ENGINE_VARIANTS])
+    for vi, (name, d, N, n, eng_expr, fams) in enumerate(ENGINE_VARIANTS):
+        pts = cloud(N, d, 700 + vi, 0.0, 1.0)
+        nodes = find_closest_stencils(NodeSet(pts, np.ones(N, dtype=np.int64)), n)
+        eng = eval(eng_expr, vars(meshfree))
+        store = compute_weights(nodes, eng, family_specs(meshfree, fams))
+        arrs[f"{name}_pts"] = pts
+        arrs[f"{name}_stencils"] = nodes.stencil_matrix().astype(np.int32)
+        arrs[f"{name}_keys"] = np.array(store.families)
+        for f in store.families:
+            arrs[f"{name}_w_{f}"] = store.values[f].reshape(N, n)
+    arrs["errors"] = np.array([v[0] for v in ENGINE_ERRORS])
+    for vi, (name, d, N, n, eng_expr, fams, mutate) in enumerate(ENGINE_ERRORS):
+        pts = cloud(N, d, 800 + vi, 0.0, 1.0)
+        if mutate == "coincide":
+            pts[[17, 40, 41, 42, 43, 44]] = pts[17]
+        nodes = find_closest_stencils(NodeSet(pts, np.ones(N, dtype=np.int64)), n)
+        try:
+            compute_weights(nodes, eval(eng_expr, vars(meshfree)), family_specs(meshfree, fams))
+            msg = ""
+        except WeightError as exc:
+            msg = str(exc)
+        arrs[f"err_{name}_pts"] = pts
+        arrs[f"err_{name}_msg"] = np.array(msg)
+        print(name, "->", msg)
+    save("engines.npz", **arrs)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector"]
+    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector", "engines"]
     if "knn" in which:
         dump_knn()
     if "variants" in which:
@@ -361,5 +397,7 @@ if __name__ == "__main__":
         dump_heat()
     if "vector" in which:
         dump_vector_ops()
+    if "engines" in which:
+        dump_engines()
     if "configs" in which:
         dump_configs()

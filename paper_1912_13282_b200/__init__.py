@@ -3,7 +3,8 @@
 Public API mirrors the reference:
 
     NodeSet, find_closest_stencils          stencil selection  (csrc/knn.cu)
-    RbfFd, Polyharmonic, compute_weights    batched shape solve (csrc/phs.cu)
+    RbfFd, Polyharmonic, compute_weights    batched shape solve (csrc/phs*.cu)
+    WeightedLeastSquares, Gaussian, ...      general engines, batched (csrc/engines.cu)
     WeightStore.matrix / apply / apply_all  canonical CSR + explicit apply (csrc/sparse.cu)
     run_heat_explicit                       fused forward-Euler stepping (csrc/sparse.cu)
 
@@ -12,14 +13,23 @@ include/meshfree_b200.h; there is no CPU fallback.
 """
 
 from .approx import (
+    ConstantWeight,
+    Directional,
     FirstDerivative,
+    Gaussian,
+    GaussianWeight,
     Identity,
+    InverseMultiquadric,
     Laplacian,
     MonomialBasis,
+    Multiquadric,
     Operator,
+    OperatorSum,
     Polyharmonic,
     RbfFd,
+    ScaledOperator,
     SecondDerivative,
+    WeightedLeastSquares,
     graded_lex_exponents,
     monomial_count,
 )
@@ -40,6 +50,15 @@ from .storage import DeviceCSR, WeightStore, compute_weights, expand_families
 
 __all__ = [
     "ConfigError",
+    "ConstantWeight",
+    "Directional",
+    "Gaussian",
+    "GaussianWeight",
+    "InverseMultiquadric",
+    "Multiquadric",
+    "OperatorSum",
+    "ScaledOperator",
+    "WeightedLeastSquares",
     "DeviceCSR",
     "FirstDerivative",
     "GeometryError",

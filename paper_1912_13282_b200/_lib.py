@@ -55,6 +55,28 @@ class HeatPackT(ctypes.Structure):
     _fields_ = [("ell_d16", _P), ("meta", _P), ("tile_wide", _P)]
 
 
+MF_MAX_DIM = 3
+MF_MAX_ENGINE_TERMS = 32
+MF_ENGINE_RBFFD, MF_ENGINE_WLS = 0, 1
+MF_RBF_PHS, MF_RBF_GAUSSIAN, MF_RBF_MQ, MF_RBF_IMQ = 0, 1, 2, 3
+MF_WEIGHT_CONSTANT, MF_WEIGHT_GAUSSIAN = 0, 1
+MF_SOLVER_LU, MF_SOLVER_QR, MF_SOLVER_SVD = 0, 1, 2
+MF_TERM_IDENTITY, MF_TERM_D1, MF_TERM_D2, MF_TERM_LAPLACIAN, MF_TERM_DIRECTIONAL = 0, 1, 2, 3, 4
+
+
+class EngineT(ctypes.Structure):
+    """mf_engine_t (include/meshfree_b200.h): a general weight engine and its families."""
+    _fields_ = [
+        ("engine", _I32), ("rbf", _I32), ("k", _I32), ("solver", _I32), ("scale_code", _I32),
+        ("weight", _I32), ("sigma", _D), ("weight_sigma", _D), ("d", _I32), ("l", _I32),
+        ("expos", _I32 * (MF_MAX_MONOMIALS * MF_MAX_DIM)), ("nf", _I32),
+        ("term0", _I32 * (MF_MAX_FAMILIES + 1)),
+        ("term_kind", _I32 * MF_MAX_ENGINE_TERMS), ("term_a", _I32 * MF_MAX_ENGINE_TERMS),
+        ("term_b", _I32 * MF_MAX_ENGINE_TERMS), ("term_order", _I32 * MF_MAX_ENGINE_TERMS),
+        ("term_coeff", _D * MF_MAX_ENGINE_TERMS), ("term_vec", _D * (MF_MAX_ENGINE_TERMS * MF_MAX_DIM)),
+    ]
+
+
 _SIGNATURES = {
     "mf_abi_version": ([], _I32),
     "mf_last_error": ([], ctypes.c_char_p),
@@ -79,6 +101,7 @@ _SIGNATURES = {
     "mf_plan_apply_terms": ([_P, _P, _I64, _I32, _P, ctypes.POINTER(TermsT), _P], _I32),
     "mf_apply_terms_rows": ([_P, _P, _P, _I64, ctypes.POINTER(TermsT), _P], _I32),
     "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
+    "mf_engine_weights": ([_P, _I64, _P, _P, _I64, _I32, ctypes.POINTER(EngineT), _P, _P, _P, _P], _I32),
     "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
                        _I64, _P, _P, _P, ctypes.POINTER(HeatPackT), _P], _I32),

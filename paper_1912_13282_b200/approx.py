@@ -1,12 +1,15 @@
-"""Approximation primitives needed by the batched shape path (host side).
+"""Approximation primitives of the shape path (host side).
 
-Restates the pieces of the reference's approx package that feed the batched
-kernel: graded-lex exponents (approx/basis.py:25-33),
-monomial counts (basis.py:88-90), the polyharmonic kernel (basis.py:172-228),
-the elementary operators and their derivative orders (operators.py:80-155),
-and the RbfFd engine descriptor (engines.py:147-158).  The per-point operator
-algebra of the reference (apply_rbf/apply_monomial on arbitrary points) is not
-needed on the GPU path; only the constraint right-hand side at the origin is.
+Restates the pieces of the reference's approx package that parameterise the
+GPU weight kernels: graded-lex exponents
+(approx/basis.py:25-33), monomial counts (basis.py:88-90), the radial kernels
+(basis.py:93-228: polyharmonic, Gaussian, multiquadric, inverse
+multiquadric), the elementary operators, their derivative orders and the
+operator algebra (operators.py:18-244), the least-squares weight functions
+(approx/weights.py) and the engine descriptors RbfFd / WeightedLeastSquares
+(engines.py:102-209).  The per-point evaluation itself (apply_rbf /
+apply_monomial) runs inside the kernels; only the constraint right-hand side at
+the origin is evaluated here.
 """
 
 from __future__ import annotations
@@ -35,7 +38,13 @@ def monomial_count(degree: int, dim: int) -> int:
 
 
 class Operator:
-    """Elementary linear differential operator evaluated at a point."""
+    """Linear differential operator evaluated at a point (operators.py:18-52).
+
+    ``terms()`` flattens sums and scalar multiples into (coefficient,
+    elementary) pairs; ``2 * Laplacian() + FirstDerivative(0)`` builds an
+    OperatorSum.  User subclasses with their own point evaluation cannot run
+    on the GPU (ConfigError at compute_weights).
+    """
 
     order: int = 0
 
@@ -45,6 +54,20 @@ class Operator:
     def origin_monomial(self, expo) -> float:
         """(L x^expo)(0)."""
         raise NotImplementedError
+
+    def __mul__(self, c):
+        return ScaledOperator(float(c), self)
+
+    __rmul__ = __mul__
+
+    def __neg__(self):
+        return ScaledOperator(-1.0, self)
+
+    def __add__(self, other):
+        return OperatorSum([self, other])
+
+    def __sub__(self, other):
+        return OperatorSum([self, ScaledOperator(-1.0, other)])
 
 
 class Identity(Operator):
@@ -97,6 +120,133 @@ class Laplacian(Operator):
         return "Laplacian()"
 
 
+class Directional(Operator):
+    """First derivative along a fixed vector, (v . grad) (operators.py:178-202)."""
+
+    order = 1
+
+    def __init__(self, vector):
+        self.vector = np.atleast_1d(np.asarray(vector, dtype=float))
+
+    def origin_monomial(self, expo):
+        if sum(expo) != 1:
+            return 0.0
+        a = list(expo).index(1)
+        return float(self.vector[a]) if a < self.vector.shape[0] else 0.0
+
+    def __repr__(self):
+        return f"Directional({self.vector.tolist()})"
+
+
+class ScaledOperator(Operator):
+    def __init__(self, coeff: float, inner: Operator):
+        self.coeff = float(coeff)
+        self.inner = inner
+
+    @property
+    def order(self):
+        return self.inner.order
+
+    def terms(self):
+        return [(self.coeff * c, op) for c, op in self.inner.terms()]
+
+    def origin_monomial(self, expo):
+        return self.coeff * self.inner.origin_monomial(expo)
+
+    def __mul__(self, c):
+        return ScaledOperator(self.coeff * float(c), self.inner)
+
+    __rmul__ = __mul__
+
+    def __repr__(self):
+        return f"{self.coeff} * {self.inner!r}"
+
+
+class OperatorSum(Operator):
+    def __init__(self, parts):
+        flat = []
+        for p in parts:
+            if isinstance(p, OperatorSum):
+                flat.extend(p.parts)
+            else:
+                flat.append(p)
+        self.parts = flat
+
+    @property
+    def order(self):
+        return max(p.order for p in self.parts)
+
+    def terms(self):
+        out = []
+        for p in self.parts:
+            out.extend(p.terms())
+        return out
+
+    def origin_monomial(self, expo):
+        acc = self.parts[0].origin_monomial(expo)
+        for p in self.parts[1:]:
+            acc = acc + p.origin_monomial(expo)
+        return acc
+
+    def __repr__(self):
+        return " + ".join(repr(p) for p in self.parts)
+
+
+class Gaussian:
+    """phi(r) = exp(-(r / sigma)^2) (basis.py:93-113)."""
+
+    def __init__(self, sigma: float):
+        self.sigma = float(sigma)
+        if self.sigma <= 0:
+            raise ConfigError("gaussian shape parameter must be positive")
+
+    def __repr__(self):
+        return f"Gaussian({self.sigma})"
+
+
+class Multiquadric:
+    """phi(r) = sqrt(1 + (r / sigma)^2) (basis.py:116-140)."""
+
+    def __init__(self, sigma: float):
+        self.sigma = float(sigma)
+        if self.sigma <= 0:
+            raise ConfigError("multiquadric shape parameter must be positive")
+
+    def __repr__(self):
+        return f"Multiquadric({self.sigma})"
+
+
+class InverseMultiquadric:
+    """phi(r) = 1 / sqrt(1 + (r / sigma)^2) (basis.py:143-167)."""
+
+    def __init__(self, sigma: float):
+        self.sigma = float(sigma)
+        if self.sigma <= 0:
+            raise ConfigError("inverse multiquadric shape parameter must be positive")
+
+    def __repr__(self):
+        return f"InverseMultiquadric({self.sigma})"
+
+
+class ConstantWeight:
+    """w(x) = 1 (approx/weights.py:15-20)."""
+
+    def __repr__(self):
+        return "ConstantWeight()"
+
+
+class GaussianWeight:
+    """w(x) = exp(-(|x| / sigma)^2) (approx/weights.py:23-37)."""
+
+    def __init__(self, sigma: float):
+        self.sigma = float(sigma)
+        if self.sigma <= 0:
+            raise ConfigError("weight shape parameter must be positive")
+
+    def __repr__(self):
+        return f"GaussianWeight({self.sigma})"
+
+
 class Polyharmonic:
     """phi(r) = r^k for odd k, r^k log(r) for even k, with phi(0) = 0."""
 
@@ -120,6 +270,20 @@ class MonomialBasis:
         self.degree = int(degree)
         self.exponents = graded_lex_exponents(self.dim, self.degree)
 
+    @classmethod
+    def from_exponents(cls, dim: int, exponents):
+        """Explicit exponent list (basis.py:50-62)."""
+        self = cls.__new__(cls)
+        self.dim = int(dim)
+        self.exponents = [tuple(int(x) for x in e) for e in exponents]
+        if not self.exponents:
+            raise ConfigError("empty monomial basis")
+        for e in self.exponents:
+            if len(e) != dim or any(x < 0 for x in e):
+                raise ConfigError(f"bad exponent tuple {e} for dimension {dim}")
+        self.degree = max(sum(e) for e in self.exponents)
+        return self
+
     @property
     def size(self) -> int:
         return len(self.exponents)
@@ -132,15 +296,47 @@ class MonomialBasis:
         return f"MonomialBasis(dim={self.dim}, size={self.size})"
 
 
-class RbfFd:
-    """RBF collocation with optional monomial augmentation (engines.py:147-158).
+class WeightedLeastSquares:
+    """Weighted least squares fit over a monomial basis (engines.py:102-145).
 
-    The GPU path implements the reference's batched configuration: a
-    Polyharmonic kernel with exponent >= 3, ``solver="lu"``, scale rule
-    ``none``/``nearest``/``support``.  ``mode`` selects the shape-solve variant
-    (``"hybrid"``: FMA solve, conditioning-flagged stencils re-solved in the
-    reference's op order; ``"replay"``: reference op order everywhere;
-    ``"fast"``: FMA only).
+    ``basis`` is a MonomialBasis or an int degree (the full basis of that
+    degree once the dimension is known).  Runs in the general engine kernel
+    (csrc/engines.cu): minimum-norm (qr / svd) or square (lu) solves of
+    (W B)^T y = L b(0), w = W y.
+    """
+
+    def __init__(self, basis, weight=None, scale="nearest", solver="qr"):
+        self.basis = basis
+        self.weight = weight if weight is not None else ConstantWeight()
+        self.scale = scale
+        self.solver = solver
+
+    def _resolve_basis(self, dim):
+        if isinstance(self.basis, int):
+            self.basis = MonomialBasis(dim, self.basis)
+        if self.basis.dim != dim:
+            raise ConfigError(
+                f"basis dimension {self.basis.dim} does not match points ({dim})"
+            )
+        return self.basis
+
+    def __repr__(self):
+        return (
+            f"WeightedLeastSquares({self.basis!r}, weight={self.weight!r}, "
+            f"scale={self.scale!r}, solver={self.solver!r})"
+        )
+
+
+class RbfFd:
+    """RBF collocation with optional monomial augmentation (engines.py:147-209).
+
+    The reference's batched configuration (Polyharmonic exponent >= 3,
+    ``solver="lu"``, uniform stencils) runs in the hot shape kernels, where
+    ``mode`` selects the variant (``"hybrid"``: FMA solve, conditioning-flagged
+    stencils re-solved in the reference's op order; ``"replay"``: reference op
+    order everywhere; ``"fast"``: FMA only).  Every other configuration (qr /
+    svd solvers, Gaussian / multiquadric / inverse multiquadric kernels, r^k
+    with k <= 2, composite operators) runs in the general engine kernel.
     """
 
     def __init__(self, rbf, degree: int = 2, scale="nearest", solver="qr", mode="hybrid"):

@@ -12,11 +12,16 @@ canonical layout (rows ascending, columns ascending, int32 indices, rows only
 for stored nodes -- storage.py:156-170); ``@`` and ``apply_all`` run on the GPU
 and are bitwise equal to scipy's ``csr_matvec`` on the same matrix.
 
-Only the batched configuration of the reference is implemented
-(storage.py:310-322: uniform stencil size, RbfFd + Polyharmonic(k >= 3),
-``solver="lu"``, scale none/nearest/support, elementary operator families).
-Everything else -- the per-node engine loop (storage.py:325-339) -- raises
-ConfigError: there is no CPU fallback.
+The reference's batched configuration (storage.py:310-322: RbfFd +
+Polyharmonic(k >= 3), ``solver="lu"``, scale none/nearest/support,
+elementary operator families) runs in the hot shape kernels
+(``mf_phs_weights``); every other engine configuration the reference sends
+through its per-node loop (storage.py:325-339) -- qr / svd solvers,
+Gaussian / multiquadric / inverse multiquadric kernels, r^k with k <= 2,
+WeightedLeastSquares, composite operators -- runs batched in the general
+engine kernel (``mf_engine_weights``).  Stencils must have one size (the
+device store is dense); user-defined operator or weight classes, whose point
+evaluation is Python code, raise ConfigError: there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -29,15 +34,25 @@ import torch
 
 from . import _lib
 from .approx import (
+    ConstantWeight,
+    Directional,
     FirstDerivative,
+    Gaussian,
+    GaussianWeight,
     Identity,
+    InverseMultiquadric,
     Laplacian,
     MonomialBasis,
+    Multiquadric,
     Operator,
+    OperatorSum,
     Polyharmonic,
     RbfFd,
+    ScaledOperator,
     SecondDerivative,
+    WeightedLeastSquares,
     graded_lex_exponents,
+    monomial_count,
 )
 from .errors import ConfigError, NumericalError, StencilError, StorageError, WeightError
 
@@ -777,8 +792,8 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
                 groups.append((eng, sub))
     else:
         groups = [(engine, fams)]
-    for eng, _ in groups:
-        _check_batchable(eng)
+    for eng, sub in groups:
+        _check_engine(eng, sub)
     if rows.size == 0:
         # nothing selected (e.g. "boundary" on a set without boundary nodes): an
         # empty store, as the reference returns
@@ -800,10 +815,46 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
     n = int(stencils_d.shape[1]) if rows.size else 0
     values = {}
     for eng, sub in groups:
-        values.update(_run_batch(nodes, eng, sub, rows, rows_d, stencils_d, n))
+        if _batchable(eng, sub):
+            values.update(_run_batch(nodes, eng, sub, rows, rows_d, stencils_d, n))
+        else:
+            values.update(_run_general(nodes, eng, sub, rows, rows_d, stencils_d, n))
     values = {k: values[k] for k in fams}
     return WeightStore(len(nodes), rows, stencils_d, values, n, rows_d=rows_d,
                        positions_d=nodes.positions_device())
+
+
+_ELEMENTARY = (Identity, FirstDerivative, SecondDerivative, Laplacian)
+_GENERAL_TERMS = _ELEMENTARY + (Directional,)
+_RBF_CODES = {Polyharmonic: _lib.MF_RBF_PHS, Gaussian: _lib.MF_RBF_GAUSSIAN,
+              Multiquadric: _lib.MF_RBF_MQ, InverseMultiquadric: _lib.MF_RBF_IMQ}
+
+
+def _batchable(engine, fams) -> bool:
+    """The reference's own batch criterion (storage.py:310-322)."""
+    return (isinstance(engine, RbfFd) and isinstance(engine.rbf, Polyharmonic)
+            and engine.solver == "lu" and engine.rbf.exponent >= 3
+            and engine.scale in SCALE_CODES
+            and all(isinstance(op, _ELEMENTARY) for op in fams.values()))
+
+
+def _check_engine(engine, fams):
+    """ConfigError for what cannot run on the GPU at all (Python-defined
+    kernels, weights or operators); everything else is batched or general."""
+    if isinstance(engine, RbfFd):
+        if type(engine.rbf) not in _RBF_CODES:
+            raise ConfigError(f"{engine!r}: kernel {engine.rbf!r} has no GPU implementation")
+    elif isinstance(engine, WeightedLeastSquares):
+        if not isinstance(engine.weight, (ConstantWeight, GaussianWeight)):
+            raise ConfigError(f"{engine!r}: weight function {engine.weight!r} has no GPU implementation")
+    else:
+        raise ConfigError(f"{engine!r}: unknown weight engine")
+    for key, op in fams.items():
+        for _, elem in op.terms():
+            if not isinstance(elem, _GENERAL_TERMS):
+                raise ConfigError(f"family {key!r}: operator {elem!r} has no GPU implementation")
+    if _batchable(engine, fams):
+        _check_batchable(engine)
 
 
 def _check_batchable(engine):
@@ -901,4 +952,139 @@ def _run_batch(nodes, engine, fams, rows, rows_d, stencils_d, n):
             raise WeightError(node, "all stencil nodes coincide with the center")
         raise WeightError(node, "singular local collocation system; try a larger stencil")
     # (m, nf, n) -> per family (m, n)
+    return {key: out[:, f, :].contiguous() for f, key in enumerate(fams)}
+
+
+_ENGINE_MESSAGES = {
+    2: "all stencil nodes coincide with the center",
+    4: "weight function must be positive on the stencil",
+}
+_NONFINITE = {
+    True: "least squares fit produced non-finite weights (singular local system); use the qr or svd solver",
+    False: "local collocation produced non-finite weights (degenerate stencil geometry?); try a larger stencil",
+}
+
+
+def encode_engine(engine, fams: dict, dim: int, n: int):
+    """mf_engine_t for the general kernel, or raise the reference's per-node error
+    text for the first family (rows are checked by the caller)."""
+    e = _lib.EngineT()
+    wls = isinstance(engine, WeightedLeastSquares)
+    e.engine = _lib.MF_ENGINE_WLS if wls else _lib.MF_ENGINE_RBFFD
+    e.d = dim
+    first = next(iter(fams))
+    if engine.scale not in SCALE_CODES:
+        raise _EngineSetupError(first, f"unknown scale rule {engine.scale!r}; use none, nearest or support")
+    e.scale_code = SCALE_CODES[engine.scale]
+    solvers = {"lu": _lib.MF_SOLVER_LU, "qr": _lib.MF_SOLVER_QR, "svd": _lib.MF_SOLVER_SVD}
+    if wls:
+        try:
+            basis = engine._resolve_basis(dim)
+        except ConfigError as exc:
+            raise _EngineSetupError(first, str(exc)) from None
+        expos = [tuple(x) for x in basis.exponents]
+        if isinstance(engine.weight, GaussianWeight):
+            e.weight, e.weight_sigma = _lib.MF_WEIGHT_GAUSSIAN, engine.weight.sigma
+        else:
+            e.weight = _lib.MF_WEIGHT_CONSTANT
+        if engine.solver == "lu" and len(expos) != n:
+            raise _EngineSetupError(
+                first, f"lu needs a square local system, got {(len(expos), n)}; use qr or svd")
+    else:
+        rbf = engine.rbf
+        e.rbf = _RBF_CODES[type(rbf)]
+        if isinstance(rbf, Polyharmonic):
+            e.k = rbf.exponent
+        else:
+            e.sigma = rbf.sigma
+        expos = graded_lex_exponents(dim, engine.degree) if engine.degree >= 0 else []
+        if len(expos) > n:
+            raise _EngineSetupError(
+                first, f"augmentation of degree {engine.degree} needs at least {len(expos)} stencil nodes, got {n}")
+    if engine.solver not in solvers:
+        raise _EngineSetupError(first, f"unknown dense solver {engine.solver!r}; use lu, qr or svd")
+    e.solver = solvers[engine.solver]
+    if len(expos) > _lib.MF_MAX_MONOMIALS or len(fams) > _lib.MF_MAX_FAMILIES:
+        raise ConfigError("too many families or monomials for the general engine kernel")
+    unknowns = (min(len(expos), n) if wls else n + len(expos))
+    if (engine.solver == "svd" and unknowns > 128) or (engine.solver == "qr" and unknowns > 256):
+        raise ConfigError("local system too large for the GPU svd (128 unknowns) / qr (256) solver")
+    e.l = len(expos)
+    for j, ex in enumerate(expos):
+        for a in range(dim):
+            e.expos[j * _lib.MF_MAX_DIM + a] = int(ex[a])
+    e.nf = len(fams)
+    t = 0
+    e.term0[0] = 0
+    for f, (key, op) in enumerate(fams.items()):
+        for coeff, elem in op.terms():
+            if t >= _lib.MF_MAX_ENGINE_TERMS:
+                raise ConfigError(f"more than {_lib.MF_MAX_ENGINE_TERMS} operator terms in one call")
+            e.term_coeff[t] = float(coeff)
+            e.term_order[t] = int(elem.order)
+            if isinstance(elem, Identity):
+                e.term_kind[t] = _lib.MF_TERM_IDENTITY
+            elif isinstance(elem, FirstDerivative):
+                e.term_kind[t], e.term_a[t] = _lib.MF_TERM_D1, elem.axis
+            elif isinstance(elem, SecondDerivative):
+                e.term_kind[t], e.term_a[t], e.term_b[t] = _lib.MF_TERM_D2, elem.a, elem.b
+            elif isinstance(elem, Laplacian):
+                e.term_kind[t] = _lib.MF_TERM_LAPLACIAN
+            else:
+                e.term_kind[t] = _lib.MF_TERM_DIRECTIONAL
+                for a, v in enumerate(np.asarray(elem.vector, dtype=float)[:dim]):
+                    e.term_vec[t * _lib.MF_MAX_DIM + a] = float(v)
+            axes = [e.term_a[t], e.term_b[t]]
+            if max(axes) >= dim:
+                raise _EngineSetupError(key, f"axis out of range for dimension {dim}")
+            t += 1
+        e.term0[f + 1] = t
+    return e
+
+
+class _EngineSetupError(Exception):
+    def __init__(self, key, msg):
+        self.key, self.msg = key, msg
+
+
+def engine_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int):
+    """Run mf_engine_weights -> ((m, nf, n) f64 weights, (m, nf) status, first_fail)."""
+    lib = _lib.load()
+    m, n = int(stencils_d.shape[0]), int(stencils_d.shape[1])
+    e = encode_engine(engine, fams, dim, n)
+    dev = pos_d.device
+    out = torch.empty((m, len(fams), n), dtype=torch.float64, device=dev)
+    status = torch.empty((max(m, 1), len(fams)), dtype=torch.int8, device=dev)
+    first_fail = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.check(lib.mf_engine_weights(pos_d.data_ptr(), int(pos_d.shape[0]), rows_d.data_ptr(),
+                                     stencils_d.data_ptr(), m, n, ctypes.byref(e), out.data_ptr(),
+                                     status.data_ptr(), first_fail.data_ptr(), _lib.stream_ptr()),
+               "mf_engine_weights")
+    return out, status, first_fail
+
+
+def _run_general(nodes, engine, fams, rows, rows_d, stencils_d, n):
+    """The per-node loop of the reference (storage.py:325-339), batched on the
+    GPU: same weights up to rounding, same WeightError (lowest failing node,
+    first failing family, the engine's message)."""
+    dim = nodes.dim
+    pos_d = nodes.positions_device()
+    try:
+        out, status, first_fail = engine_weights_device(pos_d, rows_d, stencils_d, engine, fams, dim)
+    except _EngineSetupError as exc:
+        raise WeightError(int(rows[0]), f"family {exc.key!r}: {exc.msg}") from None
+    bad = int(first_fail.item())
+    if bad != _lib.SENTINEL_OK:
+        codes = status[bad].cpu().numpy()
+        f = int(np.flatnonzero(codes)[0])
+        code = int(codes[f])
+        key = list(fams)[f]
+        if code == 1:
+            msg = _NONFINITE[isinstance(engine, WeightedLeastSquares)]
+        elif code == 3:
+            msg = (f"derivatives of polyharmonic r^{engine.rbf.exponent} are singular "
+                   "at the stencil center; use an exponent of 3 or more")
+        else:
+            msg = _ENGINE_MESSAGES[code]
+        raise WeightError(int(rows[bad]), f"family {key!r}: {msg}")
     return {key: out[:, f, :].contiguous() for f, key in enumerate(fams)}

@@ -151,8 +151,11 @@ def test_unsupported_engine_raises_config_error():
     m = mf()
     nodes = m.find_closest_stencils(m.NodeSet(np.random.default_rng(0).uniform(0, 1, (50, 2)),
                                               np.ones(50, dtype=np.int64)), 9)
-    with pytest.raises(m.ConfigError):
-        m.compute_weights(nodes, m.RbfFd(m.Polyharmonic(3), degree=1), ["laplacian"])  # solver qr
+    # the reference default (solver qr) runs in the general engine kernel
+    store = m.compute_weights(nodes, m.RbfFd(m.Polyharmonic(3), degree=1), ["laplacian"])
+    assert np.all(np.isfinite(store.values["laplacian"]))
+    with pytest.raises(m.ConfigError):  # a kernel class without a GPU implementation
+        m.compute_weights(nodes, m.RbfFd(object(), degree=1), ["laplacian"])
     with pytest.raises(m.WeightError, match="augmentation of degree 3"):
         m.compute_weights(nodes, m.RbfFd(m.Polyharmonic(3), degree=3, solver="lu"), ["laplacian"])
 

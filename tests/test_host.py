@@ -126,12 +126,15 @@ def test_compute_weights_preconditions_without_gpu():
     ns = ns.with_stencils([0, 1], [np.array([0, 1, 2]), np.array([1, 0, 2])])
     with pytest.raises(StencilError, match="node 2 has no stencil"):
         compute_weights(ns, eng, ["laplacian"], for_which=np.array([0, 2]))
+    # qr / svd, r^1, unknown scale rules run in the general engine kernel (GPU);
+    # Python-defined kernels / weights / engines cannot run there at all
     with pytest.raises(ConfigError):
-        compute_weights(ns, RbfFd(Polyharmonic(3), degree=1), ["laplacian"])
+        compute_weights(ns, RbfFd(object(), degree=1), ["laplacian"])
     with pytest.raises(ConfigError):
-        compute_weights(ns, RbfFd(Polyharmonic(1), degree=1, solver="lu"), ["laplacian"])
+        from paper_1912_13282_b200 import WeightedLeastSquares
+        compute_weights(ns, WeightedLeastSquares(1, weight=lambda x: 1.0), ["laplacian"])
     with pytest.raises(ConfigError):
-        compute_weights(ns, RbfFd(Polyharmonic(3), degree=1, solver="lu", scale="wide"), ["laplacian"])
+        compute_weights(ns, object(), ["laplacian"])
     with pytest.raises(StorageError, match="no engine given"):
         compute_weights(ns, {"laplacian": eng}, ["laplacian", "gradient"])
     with pytest.raises(StorageError, match="two engines"):
