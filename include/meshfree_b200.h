@@ -303,6 +303,66 @@ int mf_engine_weights(const double* pos, int64_t N, const int64_t* rows, const i
                       int64_t m, int32_t n, const mf_engine_t* eng, double* out, int8_t* status,
                       int64_t* first_fail, void* stream);
 
+/* ---- implicit consumer: assembly, ILU(0), BiCGStab ---------------------------------
+ * SparseSystem.finalize (assembly.py:91-108): committed rows given as COO in
+ * commit order (rows, cols int32, vals f64; columns distinct within a row) ->
+ * canonical CSR (rows ascending, columns ascending).  indptr N+1, indices /
+ * data nnz. */
+int mf_coo_workspace_size(int64_t N, size_t* bytes);
+int mf_coo_to_csr(const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz, int64_t N,
+                  int32_t* indptr, int32_t* indices, double* data, void* ws, size_t ws_bytes, void* stream);
+/* The row loop of solve_poisson_implicit (drivers.py:138-154) over a weight
+ * store's canonical structure (s_indptr / s_indices / s_perm from
+ * mf_csr_build, node space): kind[i] = 1 interior (values v_interior, the
+ * store's m x n stencil-order term combination), 2 Dirichlet (1 on the
+ * diagonal), 3 Neumann (values v_neumann[neumann_row[i]] x n, stencil order),
+ * 0 never committed.  mf_assemble_rows writes indptr and *nnz_out (host, the
+ * call synchronises) and the lowest node that is uncommitted or lacks a stored
+ * row into missing (device int64, 0x7f.. if none); mf_assemble_fill then
+ * writes indices / data. */
+int mf_assemble_workspace_size(int64_t N, size_t* bytes);
+int mf_assemble_rows(const int32_t* s_indptr, const int8_t* kind, int64_t N, int32_t* indptr, int64_t* missing,
+                     int64_t* nnz_out, void* ws, size_t ws_bytes, void* stream);
+int mf_assemble_fill(const int32_t* s_indptr, const int32_t* s_indices, const int32_t* s_perm, int32_t n,
+                     const double* v_interior, const double* v_neumann, const int64_t* neumann_row,
+                     const int8_t* kind, int64_t N, const int32_t* indptr, int32_t* indices, double* data,
+                     void* stream);
+/* ILU(0) preconditioner in multicolour order (replaces spilu's ILUT,
+ * solve.py:49-62): the symmetrised pattern is coloured (Jones-Plassmann, at
+ * most 128 colours), rows of one colour never couple, so the factorisation and
+ * both substitutions run colour by colour.  The struct is filled by
+ * mf_ilu0_build (host), its arrays are caller-owned device buffers. */
+#define MF_MAX_COLORS 128
+typedef struct {
+    const int32_t* indptr;
+    const int32_t* indices;
+    const int8_t* part;   /* nnz: -1 L, 0 diagonal, +1 U */
+    const int32_t* diag;  /* N: position of the diagonal entry */
+    const double* lu;     /* nnz: unit-L below / U on and above, CSR order */
+    const int32_t* order; /* N: rows colour by colour */
+    int32_t ncolors;
+    int32_t rounds;       /* colouring rounds taken */
+    int32_t color_off[MF_MAX_COLORS + 1];
+} mf_ilu0_t;
+int mf_ilu0_workspace_size(int64_t N, size_t* bytes);
+/* color, order, diag: N int32; part: nnz int8; lu: nnz f64.  zero_pivot_row
+ * (device int64) receives the lowest row without a diagonal entry or
+ * 0x7f7f7f7f7f7f7f7f.  Synchronises (colouring rounds). */
+int mf_ilu0_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, int64_t nnz,
+                  int32_t* color, int32_t* order, int8_t* part, int32_t* diag, double* lu, mf_ilu0_t* M,
+                  int64_t* zero_pivot_row, void* ws, size_t ws_bytes, void* stream);
+/* y = M^-1 x */
+int mf_ilu0_apply(const mf_ilu0_t* M, const double* x, double* y, void* stream);
+/* scipy's bicgstab recurrence (solve.py:96-99) on the device, preconditioned
+ * by M (nullable: none), x0 = x on entry, stop at ||r|| < max(atol, rtol ||b||).
+ * info: 0 converged, -10 / -11 breakdown, maxiter when exhausted; iterations =
+ * completed iterations (the reference's callback count); residual_norm = the
+ * last ||r|| the recurrence evaluated.  Synchronises every iteration. */
+int mf_bicgstab_workspace_size(int64_t N, size_t* bytes);
+int mf_bicgstab(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, const mf_ilu0_t* M,
+                const double* b, double* x, double rtol, double atol, int64_t maxiter, int64_t* iterations,
+                int32_t* info, double* residual_norm, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

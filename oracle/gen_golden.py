@@ -382,9 +382,130 @@ def dump_engines():
     save("engines.npz", **arrs)
 
 
+# -- implicit consumer (SparseSystem, solve_sparse, solve_poisson_implicit) -------
+
+def jittered(m, d, seed):
+    """m^d jittered grid nodes in the unit cube; the band within h of x = 0/1 is
+    Dirichlet (-1), the band within h of the other faces Neumann (-2, outward
+    axis normals), everything else interior (+1)."""
+    rng = np.random.default_rng(seed)
+    h = 1.0 / m
+    g = np.arange(h / 2, 1, h)
+    P = np.stack(np.meshgrid(*([g] * d), indexing="ij"), -1).reshape(-1, d)
+    P = P + rng.uniform(-0.3 * h, 0.3 * h, P.shape)
+    types = np.ones(P.shape[0], dtype=np.int64)
+    normals = np.full(P.shape, np.nan)
+    for a in range(1, d):
+        lo, hi = P[:, a] < h, P[:, a] > 1 - h
+        types[lo | hi] = -2
+        normals[lo] = 0.0
+        normals[hi] = 0.0
+        normals[lo, a] = -1.0
+        normals[hi, a] = 1.0
+    xb = (P[:, 0] < h) | (P[:, 0] > 1 - h)
+    types[xb] = -1
+    return P, types, normals
+
+
+def dump_implicit():
+    from meshfree import SparseSystem
+    from meshfree.drivers import solve_poisson_implicit
+    from meshfree.solve import SolverConfig, solve_sparse
+
+    arrs = {}
+    cases = [
+        # name, m, d, n, families, terms, neumann?
+        ("dir2d", 64, 2, 15, ["laplacian"], [(-1.0, "laplacian")], False),
+        ("neu2d", 56, 2, 15, ["laplacian", "gradient", "identity"], [(1.0, "laplacian"), (-0.5, "identity")], True),
+        ("dir3d", 15, 3, 35, ["laplacian"], [(-1.0, "laplacian")], False),
+    ]
+    arrs["names"] = np.array([c[0] for c in cases])
+    for ci, (name, m, d, n, fams, terms, neu) in enumerate(cases):
+        pts, types, normals = jittered(m, d, 900 + ci)
+        if not neu:
+            types[types == -2] = -1
+        nodes = find_closest_stencils(NodeSet(pts, types, normals), n)
+        store = compute_weights(nodes, RbfFd(Polyharmonic(3), degree=2, scale="support", solver="lu"), fams)
+        out = []
+        f = lambda p: np.sin(3 * p[:, 0]) + p[:, 1] ** 2
+        res = solve_poisson_implicit(nodes, store, terms=terms, rhs=f,
+                                     dirichlet={-1: lambda p: p[:, 0] * p[:, 1]},
+                                     neumann={-2: 0.25} if neu else None, system_out=out)
+        mat, rhs = out[0]
+        arrs[f"{name}_pts"] = pts
+        arrs[f"{name}_types"] = types
+        arrs[f"{name}_normals"] = normals
+        arrs[f"{name}_stencils"] = nodes.stencil_matrix().astype(np.int32)
+        for k in store.families:
+            arrs[f"{name}_w_{k}"] = store.values[k].reshape(-1, n)
+        arrs[f"{name}_indptr"] = mat.indptr
+        arrs[f"{name}_indices"] = mat.indices
+        arrs[f"{name}_data"] = mat.data
+        arrs[f"{name}_rhs"] = rhs
+        arrs[f"{name}_u"] = res.u
+        arrs[f"{name}_iters"] = np.array(res.iterations)
+        arrs[f"{name}_residual"] = np.array(res.residual)
+        print(name, len(nodes), "iters", res.iterations, "residual", res.residual)
+    # per-row SparseSystem: rows committed out of order, then finalize
+    rng = np.random.default_rng(950)
+    sysm = SparseSystem(6)
+    order = [3, 0, 5, 1, 4, 2]
+    for i in order:
+        cols = rng.permutation(6)[: 3]
+        if i not in cols:
+            cols[0] = i
+        sysm.add_row(i, cols, rng.standard_normal(3) + 4.0 * (cols == i), float(i))
+    mat, rhs = sysm.finalize()
+    arrs["rows_indptr"], arrs["rows_indices"], arrs["rows_data"], arrs["rows_rhs"] = (
+        mat.indptr, mat.indices, mat.data, rhs)
+    res = solve_sparse(mat, rhs)
+    arrs["rows_u"] = res.u
+    # errors
+    msgs = {}
+    def err(key, fn):
+        try:
+            fn()
+            msgs[key] = ""
+        except Exception as exc:  # noqa: BLE001
+            msgs[key] = f"{type(exc).__name__}: {exc}"
+    s2 = SparseSystem(4)
+    s2.add_row(1, [1, 2], [1.0, 0.5], 0.0)
+    err("double", lambda: s2.add_row(1, [1], [1.0], 0.0))
+    err("range", lambda: s2.add_row(2, [2, 4], [1.0, 1.0], 0.0))
+    err("dupcol", lambda: s2.add_row(2, [2, 2], [1.0, 1.0], 0.0))
+    err("shape", lambda: s2.add_row(2, [2, 3], [1.0], 0.0))
+    err("outside", lambda: s2.add_row(7, [1], [1.0], 0.0))
+    err("missing", lambda: s2.finalize())
+    pts, types, normals = jittered(20, 2, 960)
+    nodes = find_closest_stencils(NodeSet(pts, types, normals), 12)
+    store = compute_weights(nodes, RbfFd(Polyharmonic(3), degree=2, scale="support", solver="lu"),
+                            ["laplacian", "gradient"])
+    err("neu_interior", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                       dirichlet={-1: 0.0, -2: 0.0}, neumann={1: 0.0}))
+    err("no_tag", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                 dirichlet={-1: 0.0, -7: 0.0}))
+    err("uncovered", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                    dirichlet={-1: 0.0}))
+    err("double_bc", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                    dirichlet={-1: 0.0, -2: 0.0}, neumann={-2: 0.0}))
+    err("family", lambda: solve_poisson_implicit(nodes, store, terms="d2_0_0", rhs=1.0,
+                                                 dirichlet={-1: 0.0, -2: 0.0}))
+    err("config", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                 dirichlet={-1: 0.0, -2: 0.0},
+                                                 config=SolverConfig(preconditioner="jacobi")))
+    err("maxiter", lambda: solve_poisson_implicit(nodes, store, terms="laplacian", rhs=1.0,
+                                                  dirichlet={-1: 0.0, -2: 0.0}, config=SolverConfig(max_iter=1)))
+    arrs["err_pts"], arrs["err_types"], arrs["err_normals"] = pts, types, normals
+    arrs["err_keys"] = np.array(list(msgs))
+    arrs["err_msgs"] = np.array([msgs[k] for k in msgs])
+    for k, v in msgs.items():
+        print(k, "->", v)
+    save("implicit.npz", **arrs)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector", "engines"]
+    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector", "engines", "implicit"]
     if "knn" in which:
         dump_knn()
     if "variants" in which:
@@ -399,5 +520,7 @@ if __name__ == "__main__":
         dump_vector_ops()
     if "engines" in which:
         dump_engines()
+    if "implicit" in which:
+        dump_implicit()
     if "configs" in which:
         dump_configs()

@@ -7,6 +7,8 @@ Public API mirrors the reference:
     WeightedLeastSquares, Gaussian, ...      general engines, batched (csrc/engines.cu)
     WeightStore.matrix / apply / apply_all  canonical CSR + explicit apply (csrc/sparse.cu)
     run_heat_explicit                       fused forward-Euler stepping (csrc/sparse.cu)
+    SparseSystem, solve_sparse,             implicit assembly + multicolour ILU(0) BiCGStab
+    solve_poisson_implicit                  (csrc/solve.cu)
 
 All compute runs in hand-written sm_100a kernels behind the C ABI declared in
 include/meshfree_b200.h; there is no CPU fallback.
@@ -33,7 +35,8 @@ from .approx import (
     graded_lex_exponents,
     monomial_count,
 )
-from .drivers import run_heat_explicit
+from .assembly import SparseSystem
+from .drivers import run_heat_explicit, solve_poisson_implicit
 from .errors import (
     ConfigError,
     GeometryError,
@@ -45,6 +48,7 @@ from .errors import (
     WeightError,
 )
 from .nodeset import NodeSet
+from .solve import SolverConfig, SolveResult, SystemMatrix, make_preconditioner, solve_sparse
 from .stencils import find_closest_stencils
 from .storage import DeviceCSR, WeightStore, compute_weights, expand_families
 
@@ -78,6 +82,13 @@ __all__ = [
     "WeightError",
     "WeightStore",
     "compute_weights",
+    "make_preconditioner",
+    "solve_poisson_implicit",
+    "solve_sparse",
+    "SolveResult",
+    "SolverConfig",
+    "SparseSystem",
+    "SystemMatrix",
     "expand_families",
     "find_closest_stencils",
     "graded_lex_exponents",

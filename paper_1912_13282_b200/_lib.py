@@ -77,6 +77,15 @@ class EngineT(ctypes.Structure):
     ]
 
 
+MF_MAX_COLORS = 128
+
+
+class Ilu0T(ctypes.Structure):
+    """mf_ilu0_t (include/meshfree_b200.h): a multicolour ILU(0) factorisation."""
+    _fields_ = [("indptr", _P), ("indices", _P), ("part", _P), ("diag", _P), ("lu", _P), ("order", _P),
+                ("ncolors", _I32), ("rounds", _I32), ("color_off", _I32 * (MF_MAX_COLORS + 1))]
+
+
 _SIGNATURES = {
     "mf_abi_version": ([], _I32),
     "mf_last_error": ([], ctypes.c_char_p),
@@ -102,6 +111,18 @@ _SIGNATURES = {
     "mf_apply_terms_rows": ([_P, _P, _P, _I64, ctypes.POINTER(TermsT), _P], _I32),
     "mf_neumann_values": ([ctypes.POINTER(NeumannT), _P, _P, _P, _P, _P, _P], _I32),
     "mf_engine_weights": ([_P, _I64, _P, _P, _I64, _I32, ctypes.POINTER(EngineT), _P, _P, _P, _P], _I32),
+    "mf_coo_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_coo_to_csr": ([_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P], _I32),
+    "mf_assemble_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_assemble_rows": ([_P, _P, _I64, _P, _P, ctypes.POINTER(_I64), _P, _SZ, _P], _I32),
+    "mf_assemble_fill": ([_P, _P, _P, _I32, _P, _P, _P, _P, _I64, _P, _P, _P, _P], _I32),
+    "mf_ilu0_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_ilu0_build": ([_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, ctypes.POINTER(Ilu0T), _P, _P, _SZ, _P],
+                      _I32),
+    "mf_ilu0_apply": ([ctypes.POINTER(Ilu0T), _P, _P, _P], _I32),
+    "mf_bicgstab_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_bicgstab": ([_P, _P, _P, _I64, ctypes.POINTER(Ilu0T), _P, _P, _D, _D, _I64, ctypes.POINTER(_I64),
+                     ctypes.POINTER(_I32), ctypes.POINTER(_D), _P, _SZ, _P], _I32),
     "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
                        _I64, _P, _P, _P, ctypes.POINTER(HeatPackT), _P], _I32),

@@ -1,4 +1,4 @@
-"""Explicit forward-Euler heat stepping on the GPU.
+"""Explicit forward-Euler heat stepping and the implicit steady solve on the GPU.
 
 Drop-in for the reference's run_heat_explicit (drivers.py:48-111): same
 arguments, checks, boundary handling order (interior Euler update, Dirichlet
@@ -8,6 +8,12 @@ finite.  Step-invariant data (constant Dirichlet/Neumann values and source)
 runs as one ``mf_heat_steps`` call over the ELL-32 plan of the laplacian;
 time-dependent callables are evaluated on the host at the reference's times
 and the device steps one at a time.
+
+``solve_poisson_implicit`` (drivers.py:114-157) assembles the whole
+collocation system in one device pass over the weight store's canonical
+structure (``mf_assemble_*``: the same canonical CSR the reference's row loop
+and ``SparseSystem.finalize`` produce, bitwise) and solves it with the GPU
+BiCGStab of solve.py.
 """
 
 from __future__ import annotations
@@ -19,7 +25,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigError, InstabilityError, NumericalError
+from .errors import ConfigError, GeometryError, InstabilityError, NumericalError, StorageError
+from .solve import SolverConfig, SystemMatrix, solve_sparse
 from .storage import _to_host
 
 BLOWUP_LIMIT = 1e12
@@ -220,3 +227,149 @@ def _first_bad(peaks: torch.Tensor):
     if math.isnan(peak):
         peak = float("nan")
     return s + 1, peak
+
+
+def _steady_values(value, points):
+    if callable(value):
+        out = value(points)
+        return np.broadcast_to(np.asarray(out, dtype=float), (points.shape[0],))
+    arr = np.asarray(value, dtype=float)
+    if arr.ndim == 0:
+        return np.full(points.shape[0], float(arr))
+    return np.broadcast_to(arr, (points.shape[0],))
+
+
+def assemble_poisson_system(nodes, store, *, terms, rhs, dirichlet=None, neumann=None):
+    """The assembly half of solve_poisson_implicit (drivers.py:135-154): the
+    canonical system matrix (SystemMatrix) and right-hand side.  Errors are the
+    reference's, raised for the node its row loop would reach first."""
+    lib = _lib.load()
+    n = len(nodes)
+    pts = nodes.positions
+    kind = np.zeros(n, dtype=np.int8)
+    rhs_vec = np.zeros(n)
+    node_row = store.node_row
+
+    interior = nodes.interior_indices()
+    f = _steady_values(rhs, pts[interior])
+    if isinstance(terms, str):
+        terms = [(1.0, terms)]
+    if interior.size:
+        lacking = interior[node_row[interior] < 0]
+        if lacking.size:
+            raise StorageError(f"no weights stored for node {int(lacking[0])}")
+        for _, key in terms:
+            store._family(key)
+    kind[interior] = 1
+    rhs_vec[interior] = f
+
+    def claim(idx):
+        taken = kind[idx] != 0
+        if taken.any():
+            raise StorageError(f"row {int(idx[np.argmax(taken)])} is already committed")
+
+    for idx, value in _tag_indices(nodes, dirichlet).values():
+        g = _steady_values(value, pts[idx])
+        claim(idx)
+        kind[idx] = 2
+        rhs_vec[idx] = g
+    neu_nodes, neu_normals = [], []
+    for idx, value in _tag_indices(nodes, neumann).values():
+        g = _steady_values(value, pts[idx])
+        # per row, in order: nodes.normal(i), store.stencil(i), the d1 families of
+        # normal_combination, then the claim (drivers.py:149-152, assembly.py:85-88)
+        e_geom = nodes.types[idx] >= 0
+        e_store = node_row[idx] < 0
+        fam_missing = any(f"d1_{a}" not in store.families for a in range(nodes.dim))
+        e_claim = kind[idx] != 0
+        bad = e_geom | e_store | e_claim | fam_missing
+        if bad.any():
+            j = int(np.argmax(bad))
+            i = int(idx[j])
+            if e_geom[j]:
+                raise GeometryError(f"node {i} is not a boundary node")
+            if e_store[j]:
+                raise StorageError(f"no weights stored for node {i}")
+            for a in range(nodes.dim):
+                store._family(f"d1_{a}")
+            raise StorageError(f"row {i} is already committed")
+        kind[idx] = 3
+        rhs_vec[idx] = g
+        neu_nodes.append(idx)
+        neu_normals.append(nodes.normals[idx])
+    missing = np.flatnonzero(kind == 0)
+    if missing.size:
+        raise StorageError(f"{missing.size} rows never committed (first: node {missing[0]})")
+
+    # values: interior term combination over every stored row (storage order of
+    # the reference's `acc`), Neumann normal combinations for the Neumann rows
+    dev = _lib.device()
+    v_int = None
+    for coeff, key in terms:
+        part = float(coeff) * store._family(key).reshape(-1)
+        v_int = part if v_int is None else v_int + part
+    if v_int is None:
+        v_int = torch.zeros(1, dtype=torch.float64, device=dev)
+    v_neu = torch.zeros(1, dtype=torch.float64, device=dev)
+    neu_row = torch.zeros(1, dtype=torch.int64, device=dev)
+    if neu_nodes:
+        nn = np.concatenate(neu_nodes)
+        nrm = np.concatenate(neu_normals, axis=0)
+        rows_n = _lib.to_device(node_row[nn], torch.int64)
+        nrm_d = _lib.to_device(nrm, torch.float64)
+        acc = None
+        for a in range(nrm.shape[1]):
+            part = nrm_d[:, a:a + 1] * store._family(f"d1_{a}")[rows_n]
+            acc = part if acc is None else acc + part
+        v_neu = acc.contiguous()
+        nr = np.zeros(n, dtype=np.int64)
+        nr[nn] = np.arange(nn.size)
+        neu_row = _lib.to_device(nr, torch.int64)
+    s = store.structure()
+    kind_d = _lib.to_device(kind, torch.int8)
+    indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    miss = torch.empty(1, dtype=torch.int64, device=dev)
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.mf_assemble_workspace_size(n, ctypes.byref(size)), "mf_assemble_workspace_size")
+    ws = _lib.workspace(size.value)
+    nnz = ctypes.c_int64(0)
+    _lib.check(lib.mf_assemble_rows(s.indptr.data_ptr(), kind_d.data_ptr(), n, indptr.data_ptr(), miss.data_ptr(),
+                                    ctypes.byref(nnz), ws.data_ptr(), size.value, _lib.stream_ptr()),
+               "mf_assemble_rows")
+    bad = int(miss.item())
+    if bad != _lib.SENTINEL_OK:  # pre-checked above; kept as a device-side guard
+        raise StorageError(f"no weights stored for node {bad}")
+    indices = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+    data = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+    _lib.check(lib.mf_assemble_fill(s.indptr.data_ptr(), s.indices.data_ptr(), s.perm.data_ptr(), store.n,
+                                    v_int.data_ptr(), v_neu.data_ptr(), neu_row.data_ptr(), kind_d.data_ptr(), n,
+                                    indptr.data_ptr(), indices.data_ptr(), data.data_ptr(), _lib.stream_ptr()),
+               "mf_assemble_fill")
+    return SystemMatrix(indptr, indices[: nnz.value], data[: nnz.value], n), rhs_vec
+
+
+def solve_poisson_implicit(
+    nodes,
+    store,
+    *,
+    terms,
+    rhs,
+    dirichlet=None,
+    neumann=None,
+    config: SolverConfig | None = None,
+    system_out: list | None = None,
+):
+    """Assemble and solve a steady collocation problem (drivers.py:114-157).
+
+    ``terms`` is a family name or ``(coeff, family)`` list and ``rhs`` a
+    constant or callable ``f(points)`` for the interior rows.  Every node must
+    end up covered: interior by the PDE, boundary by exactly one of the
+    condition dictionaries.  ``system_out``, when given, receives the
+    assembled ``(matrix, rhs)`` (a device SystemMatrix; ``.to_scipy()`` gives
+    the reference's scipy CSR).
+    """
+    matrix, rhs_vec = assemble_poisson_system(nodes, store, terms=terms, rhs=rhs, dirichlet=dirichlet,
+                                              neumann=neumann)
+    if system_out is not None:
+        system_out.append((matrix, rhs_vec))
+    return solve_sparse(matrix, rhs_vec, config)

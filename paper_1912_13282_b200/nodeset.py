@@ -239,6 +239,12 @@ class NodeSet:
     def boundary_indices(self):
         return np.flatnonzero(self.types < 0)
 
+    def normal(self, i: int):
+        """Outward normal of boundary node i (nodeset.py:85-88)."""
+        if self.types[i] >= 0:
+            raise GeometryError(f"node {i} is not a boundary node")
+        return self.normals[i]
+
     def select(self, which):
         """Resolve a node selector (see module docstring) to an index array."""
         n = len(self)

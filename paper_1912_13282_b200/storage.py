@@ -509,14 +509,18 @@ class WeightStore:
         r = self._row(i)
         return self.values[key][r * self.n:(r + 1) * self.n]
 
+    def structure(self) -> _CsrStructure:
+        """The canonical CSR structure every family shares (built once)."""
+        if self._structure is None:
+            self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n,
+                                            self.positions_device)
+        return self._structure
+
     def matrix(self, key: str) -> DeviceCSR:
         """Canonical CSR view: N x N, rows only for stored nodes."""
         if key not in self._matrices:
             vals = self._family(key)
-            if self._structure is None:
-                self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n,
-                                                self.positions_device)
-            s = self._structure
+            s = self.structure()
             data = torch.empty(max(s.nnz, 1), dtype=torch.float64, device=vals.device)
             _lib.check(_lib.load().mf_csr_gather(s.perm.data_ptr(), vals.data_ptr(), s.nnz, data.data_ptr(),
                                                  _lib.stream_ptr()), "mf_csr_gather")
