@@ -191,6 +191,15 @@ int mf_apply_terms_rows(const int32_t* indptr, const int32_t* indices, const int
 int mf_permute(const double* src, const int32_t* order, int64_t N, int32_t scatter, double* dst,
                void* stream);
 
+/* ---- row-partitioned explicit step (multi-GPU heat loop) --------------------------
+ * One forward-Euler step on a block of n rows (drivers.py:88-98 per block):
+ * lap = the rows' Laplacian of the gathered field (mf_apply on the rank's CSR
+ * rows, global columns), out = interior ? u + dt * (D * lap + f) : u, then g on
+ * Dirichlet rows; peak (nullable) max-ed with the IEEE bits of |out|. */
+int mf_heat_rows(const double* lap, const double* u, const uint8_t* interior, const uint8_t* dirichlet,
+                 const double* g, const double* source, double dt, double diffusivity, int64_t n, double* out,
+                 uint64_t* peak, void* stream);
+
 /* ---- explicit Neumann closure ---------------------------------------------------
  * For listed node i with stencil row r = node_row[i] (stencils m x n int32,
  * stencil order, listed as nodes[k]): c_j = sum_a normals[k,a] * w_d1[a*mn + r*n + j]
@@ -362,6 +371,31 @@ int mf_bicgstab_workspace_size(int64_t N, size_t* bytes);
 int mf_bicgstab(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, const mf_ilu0_t* M,
                 const double* b, double* x, double rtol, double atol, int64_t maxiter, int64_t* iterations,
                 int32_t* info, double* residual_norm, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- node generation: fill_interior's acceptance pass ---------------------------
+ * fill_interior (geometry/fill.py:204-298) expands a FIFO of nodes generation
+ * by generation; each generation's candidates are accepted strictly in order
+ * when no node accepted so far lies within gamma * min(h_c, h_j)
+ * (_accept_batch_numba, fill.py:38-117).  Nodes live in a uniform grid of
+ * linked lists (head: one int32 per cell, -1 empty; nxt: one per node):
+ * mf_fill_insert links nodes [a, b); mf_fill_accept decides one generation
+ * (M candidates, cand M x d, hc M) -- the same set as the sequential pass --,
+ * appends the accepted ones at pos[count..] / hv[count..] in candidate order,
+ * links them, and writes their candidate indices to accepted_idx.  head2 is a
+ * second all -1 cell array (scratch; left all -1).  Synchronises. */
+typedef struct {
+    double lo[3];    /* grid origin */
+    double cell;     /* cell edge */
+    int32_t dims[3]; /* cells per axis (unused axes: 1) */
+    int32_t d;
+} mf_fill_grid_t;
+int mf_fill_workspace_size(int64_t M, size_t* bytes);
+int mf_fill_insert(const double* pos, int64_t a, int64_t b, const mf_fill_grid_t* grid, int32_t* head,
+                   int32_t* nxt, void* stream);
+int mf_fill_accept(double* pos, double* hv, int32_t* nxt, int64_t count, int64_t cap, const mf_fill_grid_t* grid,
+                   int32_t* head, int32_t* head2, const double* cand, const double* hc, int64_t M, double gamma,
+                   int32_t* accepted_idx, int64_t* n_accepted, int32_t* rounds, void* ws, size_t ws_bytes,
+                   void* stream);
 
 #ifdef __cplusplus
 }

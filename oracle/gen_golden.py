@@ -503,9 +503,59 @@ def dump_implicit():
     save("implicit.npz", **arrs)
 
 
+# -- node generation (fill_interior) ------------------------------------------------
+
+def dump_fill():
+    import time
+
+    from meshfree.geometry import shapes as rshapes
+    from meshfree.geometry import spacing as rspacing
+    from meshfree.geometry.fill import fill_interior
+
+    from gen_golden_specs import FILL_CASES, fill_seeds
+
+    ns = {**vars(rshapes), **vars(rspacing)}
+    arrs = {"names": np.array([c[0] for c in FILL_CASES])}
+    for name, shape_expr, h_expr, seeds_kind, kw in FILL_CASES:
+        shape = eval(shape_expr, ns)
+        h = eval(h_expr, ns)
+        seeds = fill_seeds(seeds_kind)
+        d = shape.dim
+        nodes = NodeSet(seeds, -np.ones(seeds.shape[0], dtype=np.int64)) if seeds is not None else \
+            NodeSet(np.empty((0, d)), np.empty(0, dtype=np.int64))
+        kw = dict(kw)
+        seed = kw.pop("seed", 0)
+        t = time.perf_counter()
+        out = fill_interior(nodes, shape, h, seed, **kw)
+        dt = time.perf_counter() - t
+        arrs[f"{name}_positions"] = out.positions
+        arrs[f"{name}_types"] = out.types
+        arrs[f"{name}_time"] = np.array(dt)
+        print(name, len(out), f"{dt:.2f}s")
+    errs = {}
+    disk = rshapes.Ball([0.0, 0.0], 1.0)
+    empty = NodeSet(np.empty((0, 2)), np.empty(0, dtype=np.int64))
+    for key, fn in [
+        ("gamma", lambda: fill_interior(empty, disk, 0.1, start=[[0, 0]], gamma=1.6)),
+        ("start_outside", lambda: fill_interior(empty, disk, 0.1, start=[[2.0, 0.0]])),
+        ("no_seeds", lambda: fill_interior(empty, disk, 0.1)),
+        ("max_nodes", lambda: fill_interior(empty, disk, 0.02, start=[[0, 0]], max_nodes=500)),
+        ("dims", lambda: fill_interior(NodeSet(np.zeros((1, 3)), np.ones(1, dtype=np.int64)), disk, 0.1)),
+    ]:
+        try:
+            fn()
+            errs[key] = ""
+        except Exception as exc:  # noqa: BLE001
+            errs[key] = f"{type(exc).__name__}: {exc}"
+        print(key, "->", errs[key])
+    arrs["err_keys"] = np.array(list(errs))
+    arrs["err_msgs"] = np.array([errs[k] for k in errs])
+    save("fill.npz", **arrs)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector", "engines", "implicit"]
+    which = sys.argv[1:] or ["knn", "configs", "variants", "errors", "csr", "heat", "vector", "engines", "implicit", "fill"]
     if "knn" in which:
         dump_knn()
     if "variants" in which:
@@ -522,5 +572,7 @@ if __name__ == "__main__":
         dump_engines()
     if "implicit" in which:
         dump_implicit()
+    if "fill" in which:
+        dump_fill()
     if "configs" in which:
         dump_configs()

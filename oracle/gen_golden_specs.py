@@ -62,3 +62,34 @@ def family_specs(mod, fams):
         else:
             out.append(f)
     return out
+
+
+# fill_interior cases: name, shape expression (Ball / Box / differences, evaluated
+# against the reference's geometry.shapes here and paper_1912_13282_b200 in the
+# tests), spacing expression, seed-node generator, keyword arguments
+FILL_CASES = [
+    ("disk_hole_2d", "Ball([0.0, 0.0], 1.0) - Ball([0.3, 0.1], 0.25, tag=-2)", "0.02", "circles", {}),
+    ("box_linear_2d", "Box([0.0, 0.0], [1.0, 0.5])", "LinearSpacing(0.01, [0.02, 0.0])", "box_edges", {}),
+    ("ball_start_3d", "Ball([0.0, 0.0, 0.0], 1.0)", "0.07", "none", {"start": [[0.1, 0.0, 0.0]]}),
+    ("interval_1d", "Ball([0.0], 1.0)", "0.01", "none", {"start": [[0.05]], "gamma": 0.6}),
+    ("box3d_gamma", "Box([0.0, 0.0, 0.0], [1.0, 1.0, 0.6])", "0.06", "none",
+     {"start": [[0.5, 0.5, 0.3], [0.2, 0.2, 0.2]], "gamma": 0.9, "n_candidates": 10, "seed": 7}),
+]
+
+
+def fill_seeds(kind):
+    """Seed node positions for FILL_CASES (analytic boundary samples)."""
+    import numpy as np
+
+    if kind == "circles":
+        t = np.arange(0, 2 * np.pi, 0.02)
+        outer = np.stack([np.cos(t), np.sin(t)], 1)
+        t2 = np.arange(0, 2 * np.pi, 0.02 / 0.25)
+        inner = np.stack([0.3 + 0.25 * np.cos(t2), 0.1 + 0.25 * np.sin(t2)], 1)
+        return np.concatenate([outer, inner])
+    if kind == "box_edges":
+        x = np.linspace(0, 1, 61)
+        y = np.linspace(0, 0.5, 31)[1:-1]
+        return np.concatenate([np.stack([x, 0 * x], 1), np.stack([x, 0 * x + 0.5], 1),
+                               np.stack([0 * y, y], 1), np.stack([0 * y + 1, y], 1)])
+    return None

@@ -7,6 +7,7 @@ Public API mirrors the reference:
     WeightedLeastSquares, Gaussian, ...      general engines, batched (csrc/engines.cu)
     WeightStore.matrix / apply / apply_all  canonical CSR + explicit apply (csrc/sparse.cu)
     run_heat_explicit                       fused forward-Euler stepping (csrc/sparse.cu)
+    fill_interior                           node generation, GPU acceptance pass (csrc/fill.cu)
     SparseSystem, solve_sparse,             implicit assembly + multicolour ILU(0) BiCGStab
     solve_poisson_implicit                  (csrc/solve.cu)
 
@@ -47,12 +48,19 @@ from .errors import (
     StorageError,
     WeightError,
 )
+from .geometry import Ball, Box, ConstantSpacing, LinearSpacing, Shape, fill_interior
 from .nodeset import NodeSet
 from .solve import SolverConfig, SolveResult, SystemMatrix, make_preconditioner, solve_sparse
 from .stencils import find_closest_stencils
 from .storage import DeviceCSR, WeightStore, compute_weights, expand_families
 
 __all__ = [
+    "Ball",
+    "Box",
+    "ConstantSpacing",
+    "LinearSpacing",
+    "Shape",
+    "fill_interior",
     "ConfigError",
     "ConstantWeight",
     "Directional",

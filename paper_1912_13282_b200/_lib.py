@@ -86,6 +86,11 @@ class Ilu0T(ctypes.Structure):
                 ("ncolors", _I32), ("rounds", _I32), ("color_off", _I32 * (MF_MAX_COLORS + 1))]
 
 
+class FillGridT(ctypes.Structure):
+    """mf_fill_grid_t (include/meshfree_b200.h)."""
+    _fields_ = [("lo", _D * 3), ("cell", _D), ("dims", _I32 * 3), ("d", _I32)]
+
+
 _SIGNATURES = {
     "mf_abi_version": ([], _I32),
     "mf_last_error": ([], ctypes.c_char_p),
@@ -123,6 +128,11 @@ _SIGNATURES = {
     "mf_bicgstab_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
     "mf_bicgstab": ([_P, _P, _P, _I64, ctypes.POINTER(Ilu0T), _P, _P, _D, _D, _I64, ctypes.POINTER(_I64),
                      ctypes.POINTER(_I32), ctypes.POINTER(_D), _P, _SZ, _P], _I32),
+    "mf_fill_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
+    "mf_fill_insert": ([_P, _I64, _I64, ctypes.POINTER(FillGridT), _P, _P, _P], _I32),
+    "mf_fill_accept": ([_P, _P, _P, _I64, _I64, ctypes.POINTER(FillGridT), _P, _P, _P, _P, _I64, _D, _P,
+                        ctypes.POINTER(_I64), ctypes.POINTER(_I32), _P, _SZ, _P], _I32),
+    "mf_heat_rows": ([_P, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P], _I32),
     "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
                        _I64, _P, _P, _P, ctypes.POINTER(HeatPackT), _P], _I32),

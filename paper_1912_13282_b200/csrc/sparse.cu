@@ -607,6 +607,48 @@ extern "C" int mf_apply_rows(const int32_t* indptr, const int32_t* indices, cons
     return MF_OK;
 }
 
+// one explicit step on a block of rows (the row-partitioned heat loop,
+// drivers.py:88-98 per block): lap = rows' Laplacian of the gathered field,
+// interior u + dt * (D * lap + f) (f = 0.0 when absent, as the reference's
+// `+ 0.0`), Dirichlet rows g, others unchanged; peak |u_new| as IEEE bits
+__global__ void heat_rows_k(const double* __restrict__ lap, const double* __restrict__ u,
+                            const uint8_t* __restrict__ interior, const uint8_t* __restrict__ dirichlet,
+                            const double* __restrict__ g, const double* __restrict__ src, double dt, double D,
+                            int64_t n, double* __restrict__ out, unsigned long long* peak) {
+    unsigned long long mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = u[i];
+        if (interior[i]) {
+            const double f = src ? src[i] : 0.0;
+            v = __dadd_rn(v, __dmul_rn(dt, __dadd_rn(__dmul_rn(D, lap[i]), f)));
+        }
+        if (dirichlet[i]) v = g[i];
+        out[i] = v;
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+        mx = b > mx ? b : mx;
+    }
+    if (peak) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(FULL, mx, o);
+            mx = t > mx ? t : mx;
+        }
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(peak, mx);
+    }
+}
+
+extern "C" int mf_heat_rows(const double* lap, const double* u, const uint8_t* interior, const uint8_t* dirichlet,
+                            const double* g, const double* source, double dt, double diffusivity, int64_t n,
+                            double* out, uint64_t* peak, void* stream) {
+    MF_REQUIRE(n >= 0, "mf_heat_rows: bad n");
+    if (n == 0) return MF_OK;
+    heat_rows_k<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(lap, u, interior, dirichlet, g, source, dt,
+                                                                      diffusivity, n, out,
+                                                                      reinterpret_cast<unsigned long long*>(peak));
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
 static int ell_grid(int64_t N) { return grid_for(((N + 31) / 32) * 32, 256, 8); }
 
 extern "C" int mf_neumann_values(const mf_neumann_t* nm, const double* u, double* out, double* u_scatter,

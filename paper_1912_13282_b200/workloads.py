@@ -98,8 +98,8 @@ def c3(N: int = 1_000_000) -> Workload:
     return Workload("C3", pts, np.ones(N, dtype=np.int64), 35, 2, ["laplacian"], u)
 
 
-def c4(N: int = 1_000_000) -> Workload:
-    rng = np.random.default_rng(0)
+def c4(N: int = 1_000_000, seed: int = 0) -> Workload:
+    rng = np.random.default_rng(seed)
     pts = rng.uniform(0.0, 1.0, (N, 2))
     h = 1.0 / math.sqrt(N)
     edge = np.minimum(np.minimum(pts[:, 0], pts[:, 1]), np.minimum(1.0 - pts[:, 0], 1.0 - pts[:, 1]))
