@@ -17,8 +17,12 @@ cpu_baseline  the C oracle (bit-exact restatement of the reference's numba
            kernel + kNN + CSR + matvec) on host cores over a bounded sample
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU (torchrun): every rank runs its own C3-size node set (seed = rank),
-no collective on the data path; value = all stencils / max-over-ranks time.
+Multi-GPU (torchrun): ONE sharded problem of world x 1M nodes in
+the unit cube (weak scaling: 1M targets per rank); positions replicated, each
+rank selects stencils and solves shapes for its contiguous target block (no
+collective), builds its CSR rows (global columns) and applies the Laplacian
+after one NCCL all-gather of the field; value = all stencils / max-over-ranks
+time.
 """
 
 from __future__ import annotations
@@ -232,6 +236,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if world > 1 or os.environ.get("MF_BENCH_SHARDED"):  # (the env switch runs the sharded path at N=1)
+        return run_sharded(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -517,6 +523,131 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local):
+    """One C3-density problem of world x N nodes, targets sharded over the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_13282_b200 as mf
+    from paper_1912_13282_b200 import _lib, build as mfbuild
+    from paper_1912_13282_b200.parallel import RowPartition, ShardedProblem, allgather_field
+    from paper_1912_13282_b200.stencils import knn_device
+    from paper_1912_13282_b200.storage import expand_families, phs_weights_device
+
+    mfbuild.build()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    N = world * args.N
+    n, deg = 35, 2
+    # the same node set on every rank (positions replicated, 24 MB per 1M nodes)
+    pts = np.random.default_rng(0).uniform(0.0, 1.0, (N, 3))
+    part = RowPartition(N, world, rank)
+    lo, hi = part.lo, part.hi
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=deg, scale="support", solver="lu", mode=args.mode)
+    fams = expand_families(["laplacian"], 3)
+    u_host = np.random.default_rng(1).standard_normal(N)
+    nodes = mf.NodeSet(pts, np.ones(N, dtype=np.int64))
+    pos_d = nodes.positions_device()
+    tg_host = np.arange(lo, hi, dtype=np.int64)
+    tg_d = torch.arange(lo, hi, dtype=torch.int64, device=dev)
+    pool_d = torch.arange(N, dtype=torch.int64, device=dev)
+    u_loc = torch.from_numpy(u_host[lo:hi]).to(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        st, _ = knn_device(nodes, n, tg_d, pool_d)
+        if ev:
+            ev[1].record(stream)
+        w, _, first_fail, _ = phs_weights_device(pos_d, tg_d, st, eng, fams, 3)
+        if ev:
+            ev[2].record(stream)
+        store = mf.WeightStore(N, tg_host, st, {"laplacian": w[:, 0, :]}, n, rows_d=tg_d, positions_d=pos_d)
+        mat = store.matrix("laplacian")
+        if ev:
+            ev[3].record(stream)
+        u_full = allgather_field(u_loc, part)  # NCCL all-gather of the field blocks
+        y = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+        _lib.check(lib.mf_apply(mat.indptr_device[lo:].data_ptr(), mat.indices_device.data_ptr(),
+                                mat.data_device.data_ptr(), u_full.data_ptr(), y.data_ptr(), hi - lo,
+                                _lib.stream_ptr()), "mf_apply")
+        if ev:
+            ev[4].record(stream)
+        return y, first_fail
+
+    for _ in range(args.warmup):
+        y, ff = step()
+    torch.cuda.synchronize()
+    assert int(ff.item()) == _lib.SENTINEL_OK, "shape solve reported a failing stencil"
+    gc.collect()
+    gc.disable()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    launches0 = lib.mf_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for ev in evs:
+            flush.zero_()
+            step(ev)
+        torch.cuda.synchronize()
+    dist.barrier()
+    gc.enable()
+    launches = (lib.mf_launch_count() - launches0) / max(args.steps, 1)
+    stage = np.array([[a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])] for ev in evs])
+    step_list = stage.sum(axis=1)
+    t_local = torch.tensor([float(np.mean(step_list))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t_local.item())
+    value = N / (step_ms_max * 1e-3)
+
+    # e2e through the public sharded API: host positions and field block in,
+    # the rank's applied block out
+    e2e = None
+    if not args.no_e2e:
+        ts = []
+        for it in range(4):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sh = ShardedProblem(mf.NodeSet(pts, np.ones(N, dtype=np.int64)), n, eng, ["laplacian"], part=part)
+            yb = sh.apply_all("laplacian", torch.from_numpy(u_host[lo:hi]).to(dev)).cpu().numpy()
+            torch.cuda.synchronize()
+            if it:
+                ts.append(time.perf_counter() - t0)
+        e2e_t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": N / float(e2e_t.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(pts.nbytes + 8 * (hi - lo)), "d2h_bytes_per_step": int(yb.nbytes),
+               "stat": f"median of {len(ts)} wall-clock steps, max over ranks"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3-density sharded", "N": N, "n": n, "degree": deg, "families": ["laplacian"],
+                       "shape_mode": args.mode, "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"sharded x{world}: one {N}-node problem, contiguous target blocks, "
+                                      "positions replicated, one NCCL all-gather of the field per apply"},
+            "stage_ms": dict(zip(["knn", "shape_solve", "csr", "allgather_and_apply"],
+                                 [float(x) for x in stage.mean(axis=0)])),
+            "gpu_launches": int(launches),
+            "timing": {"value_from": f"{args.steps} eager steps, device events, max over ranks",
+                       "steps_ms": [round(float(t), 4) for t in step_list]},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def ctypes_double():

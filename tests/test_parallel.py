@@ -83,3 +83,109 @@ def test_gloo_world2_apply_and_heat(N):
         assert p.exitcode == 0
     ok_apply, ok_heat = out.get(timeout=10)
     assert ok_apply and ok_heat
+
+
+def _sharded_worker(rank, world, port, N, out):
+    """ShardedOperator over the canonical-CSR slice of each rank's rows (global
+    columns), with a host product injected for the local rows (CPU test)."""
+    import scipy.sparse
+
+    from paper_1912_13282_b200.parallel import ShardedOperator
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(3)
+    n = 7
+    stencils = np.stack([np.concatenate([[i], rng.choice(np.delete(np.arange(N), i), n - 1, replace=False)])
+                         for i in range(N)])
+    vals = rng.standard_normal((N, n))
+    part = RowPartition(N, world, rank)
+    lo, hi = part.lo, part.hi
+    # this rank's store: rows lo..hi only -> canonical N x N CSR with empty rows elsewhere
+    rows = np.repeat(np.arange(lo, hi), n)
+    A_loc = scipy.sparse.csr_matrix((vals[lo:hi].ravel(), (rows, stencils[lo:hi].ravel())), shape=(N, N))
+    A_loc.sort_indices()
+    ip, ix, da = (torch.from_numpy(A_loc.indptr.astype(np.int32)), torch.from_numpy(A_loc.indices.astype(np.int32)),
+                  torch.from_numpy(A_loc.data))
+
+    def host_rows(u_full):  # the rows lo..hi addressed through the slice, as mf_apply does
+        ipl = ip[lo:].numpy()
+        y = np.zeros(hi - lo)
+        for k in range(hi - lo):
+            acc = 0.0
+            for p in range(ipl[k], ipl[k + 1]):
+                acc = acc + da.numpy()[p] * u_full.numpy()[ix.numpy()[p]]
+            y[k] = acc
+        return torch.from_numpy(y)
+
+    op = ShardedOperator(ip, ix, da, part, local_apply=host_rows)
+    u = rng.standard_normal(N)
+    y_loc = op.apply(torch.from_numpy(u[lo:hi]))
+    ys = [None] * world
+    dist.all_gather_object(ys, y_loc.numpy())
+    if rank == 0:
+        full = scipy.sparse.csr_matrix((vals.ravel(), (np.repeat(np.arange(N), n), stencils.ravel())), shape=(N, N))
+        full.sort_indices()
+        out.put(bool(np.array_equal(np.concatenate(ys), full @ u)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N", [9, 50])
+def test_gloo_world2_sharded_operator_slices(N):
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, N, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert out.get(timeout=10)
+
+
+@pytest.mark.gpu
+def test_sharded_problem_emulated_two_ranks_bitwise():
+    """Two partitions of one node set on one GPU (no process group): stencils,
+    weights, the exchanged apply and the row-partitioned heat loop equal the
+    unsharded run bitwise."""
+    import paper_1912_13282_b200 as mf
+    from paper_1912_13282_b200 import _lib
+    from paper_1912_13282_b200.parallel import ShardedProblem
+
+    rng = np.random.default_rng(4)
+    N = 6000
+    pts = rng.uniform(0, 1, (N, 2))
+    types = np.ones(N, dtype=np.int64)
+    types[np.min(np.minimum(pts, 1 - pts), axis=1) < 0.02] = -1
+    nodes = mf.NodeSet(pts, types)
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=2, scale="support", solver="lu")
+    full = mf.compute_weights(mf.find_closest_stencils(nodes, 15), eng, ["laplacian"])
+    u = rng.standard_normal(N)
+    y_ref = full.apply_all("laplacian", u)
+    shards = [ShardedProblem(nodes, 15, eng, ["laplacian"], part=RowPartition(N, 2, r)) for r in range(2)]
+    u_d = _lib.to_device(u, torch.float64)
+    ys = [sh.operator("laplacian")._local(u_d).cpu().numpy() for sh in shards]
+    assert np.array_equal(np.concatenate(ys), y_ref)
+    # heat: 5 steps, the exchange done by hand between the two partitions
+    dt = 1e-6
+    interior = torch.from_numpy((types > 0).astype(np.uint8)).cuda()
+    dirichlet = torch.from_numpy((types == -1).astype(np.uint8)).cuda()
+    g = torch.zeros(N, dtype=torch.float64, device="cuda")
+    u0 = np.exp(-50 * np.sum((pts - 0.5) ** 2, axis=1))
+    u0[types == -1] = 0.0
+    ref = mf.run_heat_explicit(nodes, full, dt=dt, steps=5, dirichlet={-1: 0.0}, initial=u0)
+    cur = _lib.to_device(u0, torch.float64)
+    lib = _lib.load()
+    for _ in range(5):
+        nxt = torch.empty_like(cur)
+        for sh in shards:
+            lo, hi = sh.part.lo, sh.part.hi
+            lap = sh.operator("laplacian")._local(cur)
+            _lib.check(lib.mf_heat_rows(lap.data_ptr(), cur[lo:].data_ptr(), interior[lo:].data_ptr(),
+                                        dirichlet[lo:].data_ptr(), g[lo:].data_ptr(), None, dt, 1.0, hi - lo,
+                                        nxt[lo:].data_ptr(), None, _lib.stream_ptr()), "mf_heat_rows")
+        cur = nxt
+    assert np.array_equal(cur.cpu().numpy(), ref)
