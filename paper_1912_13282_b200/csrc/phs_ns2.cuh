@@ -94,11 +94,11 @@ struct Ns2Cfg {
     static constexpr int WARPS = 4;
     // per-warp shared layout (doubles)
     static constexpr int UP = ns_even(M + 1);   // Gauss-Jordan column pitch
-    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * UP + M * NR));
+    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * UP + M * (NR + 1)));
     static constexpr int XS_DBL = ns_even(DD * NP + DD);  // scaled coords (permuted), then the staged raw positions
     static constexpr int NC = NN + NR + LL;     // columns of [Q^T | g | I] in the Gauss-Jordan sweep
     static constexpr int CS = (NC + 31) / 32;   // column slots per lane
-    static constexpr int QLU_DBL = ns_even(LL * LL + 2 * LL);  // rows of Q1^-1, then two pivot-column buffers
+    static constexpr int QLU_DBL = ns_even(LL * LL + 2 * (LL + 1));  // rows of Q1^-1, then two pivot-column buffers
     static constexpr int W_DBL = M * LP;
     static constexpr int Y_DBL = (M + NR) * LP;  // Y columns, then the pivot residuals (rows M..)
     static constexpr int F_DBL = ns_even(NN * NR + NN);   // node rhs (permuted) + |Q| row sums
@@ -259,19 +259,21 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
                 fr[s][f] = t * facs[f];
             }
         }
+        // (branch-free: every lane forms the three candidates, selects are uniform
+        // loads of the constraint rows plus per-lane selects)
 #pragma unroll
         for (int s = 0; s < CS; ++s) {
+            if (32 * s + 31 < NN) continue;  // slot holds only node columns
             const int j = lane + 32 * s;
-            if (j >= NN) {
-                const int f = j - NN, m = j - NN - NR;
+            const int f = j - NN, m = j - NN - NR;
 #pragma unroll
-                for (int k = 0; k < LL; ++k) {
-                    double v = 0.0;
-                    if (f < NF) v = P_.base_bot[(f < NF ? f : 0) * MF_MAX_MONOMIALS + k] * facs[f < NF ? f : 0];
-                    else if (f == NF) v = probe_sign(idx, NN + k);
-                    else if (m == k) v = 1.0;
-                    q[s][k] = v;
-                }
+            for (int k = 0; k < LL; ++k) {
+                double vb = 0.0;
+#pragma unroll
+                for (int ff = 0; ff < NF; ++ff) vb = f == ff ? P_.base_bot[ff * MF_MAX_MONOMIALS + k] * facs[ff] : vb;
+                const double vp = probe_sign(idx, NN + k);
+                const double v = f < NF ? vb : (f == NF ? vp : (m == k ? 1.0 : 0.0));
+                if (j >= NN) q[s][k] = v;
             }
         }
 
@@ -289,14 +291,16 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
                 const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(fabs(q[0][k])) >> 32);
                 key = (hi & ~31u) | (unsigned)(31 - lane);
             }
+            // the reciprocal of every candidate pivot is formed while the REDUX runs:
+            // the winner publishes its own, so no reciprocal sits on the step's chain
+            const double my_inv = rcp_c3(q[0][k]);
             const unsigned mk = __reduce_max_sync(FULL, key);
             const int wl = 31 - (int)(mk & 31u);
             ok = ok && (mk >> 5) != 0u;
-            double* pc = PV + (k & 1) * LL;  // two buffers: the next step's winner never overwrites a column being read
+            double* pc = PV + (k & 1) * (LL + 1);  // two buffers: the next step's winner never overwrites a column being read
             if (lane == wl && live) {
 #pragma unroll
-                for (int r = 0; r + 1 < LL; r += 2) *reinterpret_cast<double2*>(pc + r) = make_double2(q[0][r], q[0][r + 1]);
-                if (LL & 1) pc[LL - 1] = q[0][LL - 1];
+                for (int r = 0; r < LL; ++r) pc[r] = r == k ? my_inv : q[0][r];
                 live = false;
                 myk = k;
             }
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
             double pv[LL];
 #pragma unroll
             for (int r = 0; r < LL; ++r) pv[r] = pc[r];
-            const double inv = rcp_c3(pv[k]);
+            const double inv = pv[k];
 #pragma unroll
             for (int s = 0; s < CS; ++s) {
                 const double t = q[s][k] * inv;
@@ -370,8 +374,9 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
         double anorm = 0.0;
         bool bad = !ok;
         if (ok) {
-            // ---- (3) Phi in the permuted order [pivots; free]: lane t owns node t and
-            //      walks t+1 .. t+(NN-1)/2 (mod NN); nodes 32.. take the tail
+            // ---- (3) Phi in the permuted order [pivots; free]
+            // pair walk: lane t owns node t and walks t+1 .. t+(NN-1)/2 (mod NN);
+            // nodes 32.. take the tail
             {
                 constexpr int H = (NN - 1) / 2;
                 // loads of a chunk of pairs first, then the arithmetic, then the
@@ -632,27 +637,30 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
             //      on a 16-byte boundary, so the pivot row streams in pairs
             double* Us = PH;
             double* Bs = PH + M * Cfg::UP;
+            // the pivot lane publishes 1 / d_k with its right-hand sides; every lane
+            // forms the reciprocal of its next diagonal candidate as soon as that
+            // entry is final (the first update of the step), off the broadcast chain
+            double rnext = rcp_c3(K[0]);
 #pragma unroll
             for (int k = 0; k < M; ++k) {
                 double* urow = Us + k * Cfg::UP + ((k + 1) & 1);
                 if (act) urow[lane] = K[k];
                 if (lane == k) {
 #pragma unroll
-                    for (int f = 0; f < NR; ++f) Bs[k * NR + f] = bb[f];
+                    for (int f = 0; f < NR; ++f) Bs[k * (NR + 1) + f] = bb[f];
+                    Bs[k * (NR + 1) + NR] = rnext;
                 }
                 __syncwarp();
-                const double rk = rcp_c3(urow[k]);
+                const double rk = Bs[k * (NR + 1) + NR];
                 const double fac = lane != k ? K[k] * rk : 0.0;
-                int j = k + 1;
-#pragma unroll
-                for (; j + 1 < M; j += 2) {
-                    const double2 u = *reinterpret_cast<const double2*>(urow + j);
-                    K[j] = fma(-fac, u.x, K[j]);
-                    K[j + 1] = fma(-fac, u.y, K[j + 1]);
+                if (k + 1 < M) {
+                    K[k + 1] = fma(-fac, urow[k + 1], K[k + 1]);
+                    rnext = rcp_c3(K[k + 1]);
                 }
-                if (j < M) K[j] = fma(-fac, urow[j], K[j]);
 #pragma unroll
-                for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * NR + f], bb[f]);
+                for (int j = k + 2; j < M; ++j) K[j] = fma(-fac, urow[j], K[j]);
+#pragma unroll
+                for (int f = 0; f < NR; ++f) bb[f] = fma(-fac, Bs[k * (NR + 1) + f], bb[f]);
             }
             // v_c = b_c / d_c with d_c the pivot lane c stored at its step
             {
