@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmeshfree_b200.so")
-SOURCES = ["api.cu", "engines.cu", "solve.cu", "fill.cu", "knn.cu", "phs.cu", "phs_reg.cu", "phs_reg_c3.cu", "phs_reg_c14.cu", "phs_reg_c2.cu", "sparse.cu", "plan.cu", "phs_cta.cu"]
-HEADERS = ["common.cuh", "phs_params.cuh", "phs_reg.cuh", "phs_nullspace.cuh", "phs_ns2.cuh"]
+SOURCES = ["api.cu", "engines.cu", "solve.cu", "fill.cu", "knn.cu", "phs.cu", "phs_reg.cu", "phs_reg_c3.cu", "phs_reg_c14.cu", "phs_reg_c2.cu", "sparse.cu", "plan.cu", "phs_cta.cu"] + [f"phs_ns2_t{i}.cu" for i in range(8)]
+HEADERS = ["common.cuh", "phs_params.cuh", "phs_reg.cuh", "phs_nullspace.cuh", "phs_ns2.cuh", "phs_ns2_shapes.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

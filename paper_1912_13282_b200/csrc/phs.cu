@@ -338,6 +338,7 @@ extern "C" int mf_phs_workspace_size(int64_t m, size_t* bytes) {
     Arena ar{nullptr, 0, 0, true};
     ar.take<int64_t>(1);
     ar.take<int64_t>((size_t)m + 1);
+    ar.take<int>((size_t)m + 1);  // flag marks (family chunks)
     *bytes = ar.off;
     return MF_OK;
 }
@@ -376,6 +377,9 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
         const double sep = (opts && opts->min_separation > 0.0) ? opts->min_separation : MF_PHS_DEFAULT_MIN_SEPARATION;
         a.min_sep2 = sep * sep;
     }
+    a.out_nf = nf;
+    a.out_f0 = 0;
+    a.flag_mark = nullptr;
     int rc = fill_phs_params(a.P, d, k, even, expos, l, base_bot, kinds, ax_a, ax_b, orders, nf, scale_code);
     if (rc != MF_OK) return rc;
 
@@ -393,6 +397,7 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
         Arena ar{(char*)ws, ws_bytes, 0, ws == nullptr};
         flag_count = ar.take<int64_t>(1);
         flag_list = ar.take<int64_t>((size_t)m + 1);
+        int* flag_mark = ar.take<int>((size_t)m + 1);
         if (ws == nullptr || !ar.ok()) {
             set_error("mf_phs_weights: HYBRID mode needs a workspace of mf_phs_workspace_size bytes");
             return MF_ERR_WORKSPACE;
@@ -400,6 +405,7 @@ extern "C" int mf_phs_weights(const double* pos, int64_t N, int32_t d, const int
         MF_CUDA_CHECK(cudaMemsetAsync(flag_count, 0, sizeof(int64_t), st));
         a.flag_list = flag_list;
         a.flag_count = flag_count;
+        a.flag_mark = flag_mark;  // used (and zeroed) only when the first pass runs in family chunks
     }
     rc = launch_phs_fast(a, st, sm_count());
     if (rc == MF_ERR_UNSUPPORTED && big) rc = launch_phs_ns_cta(a, st, sm_count());

@@ -94,7 +94,8 @@ struct Ns2Cfg {
     static constexpr int WARPS = 4;
     // per-warp shared layout (doubles)
     static constexpr int UP = ns_even(M + 1);   // Gauss-Jordan column pitch
-    static constexpr int PH_DBL = ns_even(ns_max(NN * P, M * UP + M * (NR + 1)));
+    static constexpr int KTP = (M + NR <= 16 && M <= 16) ? 20 : 36;  // [K | b] staging pitch (4 mod 16 doubles)
+    static constexpr int PH_DBL = ns_even(ns_max(ns_max(NN * P, M * UP + M * (NR + 1)), M * KTP));
     static constexpr int XS_DBL = ns_even(DD * NP + DD);  // scaled coords (permuted), then the staged raw positions
     static constexpr int NC = NN + NR + LL;     // columns of [Q^T | g | I] in the Gauss-Jordan sweep
     static constexpr int CS = (NC + 31) / 32;   // column slots per lane
@@ -110,8 +111,14 @@ struct Ns2Cfg {
     static constexpr size_t SMEM = (size_t)WARPS * WARP_DBL * sizeof(double);
     static_assert(M >= 1 && M <= 32, "the reduced system must fit one warp");
     static_assert(RN <= 2 && LL <= 32 && NR <= 8, "shape outside the kernel's layout");
-    static_assert(NN % 2 == 1, "pair enumeration assumes an odd stencil size");
 };
+
+// queue a row for the REPLAY re-solve (once, however many family chunks flag it)
+__device__ __forceinline__ void flag_row(const PhsArgs& a, int64_t idx) {
+    if (a.flag_mark && atomicExch(a.flag_mark + idx, 1) != 0) return;
+    unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
+    a.flag_list[slot] = idx;
+}
 
 template <int NN, int DEG, int DD, int NF>
 __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns2(PhsArgs a) {
@@ -378,7 +385,9 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
             // pair walk: lane t owns node t and walks t+1 .. t+(NN-1)/2 (mod NN);
             // nodes 32.. take the tail
             {
-                constexpr int H = (NN - 1) / 2;
+                // pairs (t, t + s), s = 1 .. H: every unordered pair once for odd NN; for
+                // even NN the antipodal pair is met from both ends (same value stored twice)
+                constexpr int H = NN / 2;
                 // loads of a chunk of pairs first, then the arithmetic, then the
                 // stores: shared stores would otherwise order every pair's loads
                 // behind the previous pair's stores and serialise the chains
@@ -611,7 +620,7 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
             // ---- (6) [K | b] to one row per lane through shared memory: element (r, c)
             //      at r * 36 + (c ^ r), which keeps both the accumulator-fragment stores
             //      and the row reads free of bank conflicts
-            constexpr int KTP = (MR <= 16 && M <= 16) ? 20 : 36;  // 4 mod 16 doubles
+            constexpr int KTP = Cfg::KTP;
             static_assert(M * KTP <= Cfg::PH_DBL && MR <= 32, "[K | b] staging");
             const bool act = lane < M;
             const int cc = act ? lane : 0;
@@ -681,7 +690,7 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
                     bad |= !isfinite(bb[f]);
-                    a.out[((size_t)idx * NF + f) * NN + node] = bb[f];
+                    a.out[((size_t)idx * a.out_nf + a.out_f0 + f) * NN + node] = bb[f];
                     xw[f] = fabs(bb[f]);
                 }
                 zw = fabs(bb[NF]);
@@ -716,7 +725,7 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
                             const double w = VS[r * NR + f] - oacc[rt][h];
                             if (f < NF) {
                                 bad |= !isfinite(w);
-                                a.out[((size_t)idx * NF + f) * NN + IDX[r]] = w;
+                                a.out[((size_t)idx * a.out_nf + a.out_f0 + f) * NN + IDX[r]] = w;
                                 xw[f] = fmax(xw[f], fabs(w));
                             } else {
                                 zw = fmax(zw, fabs(w));
@@ -752,16 +761,10 @@ __global__ void __launch_bounds__(128, NN <= 16 ? 8 : (NN <= 25 ? 5 : 3)) phs_ns
             const double est = anorm * zw * ratio;
             close = __any_sync(FULL, close);
             bad = __any_sync(FULL, bad);
-            if (!bad && lane == 0 && (close || !(est <= a.hybrid_thresh))) {
-                unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
-                a.flag_list[slot] = idx;
-            }
+            if (!bad && lane == 0 && (close || !(est <= a.hybrid_thresh))) flag_row(a, idx);
         }
         // failed / indefinite / non-finite rows are re-solved in the reference's order
-        if (bad && lane == 0) {
-            unsigned long long slot = atomicAdd((unsigned long long*)a.flag_count, 1ull);
-            a.flag_list[slot] = idx;
-        }
+        if (bad && lane == 0) flag_row(a, idx);
         if (lane == 0) a.status[idx] = 0;
         __syncwarp();
     }

@@ -30,6 +30,11 @@ struct PhsArgs {
     double hybrid_thresh;
     double* kappa;        // optional per-row conditioning diagnostics (FAST/HYBRID)
     double min_sep2;      // HYBRID: (min node separation / stencil radius)^2 below which to re-solve
+    // family chunks (nullspace first pass): the kernel solves P.nf families and
+    // writes them as families out_f0 .. of an out_nf-family output; flag_mark
+    // (m ints, zeroed, nullable) keeps a row flagged by several chunks listed once
+    int out_nf, out_f0;
+    int* flag_mark;
     PhsParams P;
 };
 

@@ -3,6 +3,7 @@
 // so nvcc builds them in parallel).
 #include "common.cuh"
 #include "phs_params.cuh"
+#include "phs_ns2_shapes.h"
 
 namespace mf {
 
@@ -25,16 +26,67 @@ int dispatch_reg(const PhsArgs& a, const int64_t* list, const int64_t* list_coun
     return MF_ERR_UNSUPPORTED;
 }
 
-// FAST/HYBRID first pass: HYBRID runs the nullspace kernel (phs_ns2.cuh) on the
-// shapes it is instantiated for; FAST, and HYBRID on every other shape, the
-// register rank-1 LU (phs_reg.cuh).
+// FAST/HYBRID first pass.  HYBRID runs the nullspace kernel (phs_ns2.cuh) on
+// every shape of the generated list (phs_ns2_shapes.h: r^3, degree 1..3, the
+// usual stencil sizes in 2D and 3D, NF = 1 and d + 1); a family count without
+// its own instantiation runs as chunks of instantiated ones -- each chunk
+// writes its families into the full output and flags rows for the REPLAY
+// re-solve at most once (flag_mark).  FAST, and HYBRID on shapes outside the
+// list, run the register rank-1 LU (phs_reg.cuh) where it is instantiated.
+namespace {
+struct Ns2Entry {
+    int nn, deg, dd, nf;
+    int (*fn)(const PhsArgs&, cudaStream_t, int);
+};
+#define MF_NS2_ENTRY(NN, DEG, DD, NF) {NN, DEG, DD, NF, &launch_ns2<NN, DEG, DD, NF>},
+const Ns2Entry kNs2[] = {MF_NS2_SHAPES(MF_NS2_ENTRY)};
+#undef MF_NS2_ENTRY
+
+int monomials(int deg, int d) {
+    int c = 1;
+    for (int i = 1; i <= d; ++i) c = c * (deg + i) / i;
+    return c;
+}
+const Ns2Entry* find_ns2(int d, int n, int l, int nf) {
+    for (const Ns2Entry& e : kNs2)
+        if (e.dd == d && e.nn == n && e.nf == nf && monomials(e.deg, e.dd) == l) return &e;
+    return nullptr;
+}
+}  // namespace
+
 int launch_phs_fast(const PhsArgs& a, cudaStream_t st, int sms) {
     const int n = a.n, l = a.P.l, d = a.P.d, nf = a.P.nf;
-    int rc = MF_ERR_UNSUPPORTED;
-    if (d == 3 && n == 35 && l == 10 && nf == 1) rc = launch_ns2<35, 2, 3, 1>(a, st, sms);
-    else if (d == 2 && n == 15 && l == 6 && nf == 1) rc = launch_ns2<15, 2, 2, 1>(a, st, sms);
-    else if (d == 2 && n == 25 && l == 6 && nf == 3) rc = launch_ns2<25, 2, 2, 3>(a, st, sms);
-    if (rc != MF_ERR_UNSUPPORTED) return rc;
+    if (a.flag_list && !a.kappa) {
+        if (const Ns2Entry* e = find_ns2(d, n, l, nf)) {
+            PhsArgs x = a;
+            x.flag_mark = nullptr;  // one pass: every row is flagged at most once anyway
+            const int rc = e->fn(x, st, sms);
+            if (rc != MF_ERR_UNSUPPORTED) return rc;
+        } else if (a.flag_mark && find_ns2(d, n, l, 1)) {
+            // family chunks: the largest instantiated count that fits, down to 1
+            MF_CUDA_CHECK(cudaMemsetAsync(a.flag_mark, 0, (size_t)a.m * sizeof(int), st));
+            PhsArgs c = a;
+            c.out_nf = nf;
+            for (int f0 = 0; f0 < nf;) {
+                const Ns2Entry* e = nullptr;
+                for (int k = nf - f0; k >= 1 && !e; --k) e = find_ns2(d, n, l, k);
+                c.P.nf = e->nf;
+                for (int f = 0; f < e->nf; ++f) {
+                    c.P.kinds[f] = a.P.kinds[f0 + f];
+                    c.P.ax_a[f] = a.P.ax_a[f0 + f];
+                    c.P.ax_b[f] = a.P.ax_b[f0 + f];
+                    c.P.orders[f] = a.P.orders[f0 + f];
+                    for (int j = 0; j < l; ++j)
+                        c.P.base_bot[f * MF_MAX_MONOMIALS + j] = a.P.base_bot[(f0 + f) * MF_MAX_MONOMIALS + j];
+                }
+                c.out_f0 = f0;
+                const int rc = e->fn(c, st, sms);
+                if (rc != MF_OK) return rc;  // (the graded-lex check fails on every chunk alike)
+                f0 += e->nf;
+            }
+            return MF_OK;
+        }
+    }
     return dispatch_reg<false>(a, nullptr, nullptr, a.m, st, sms);
 }
 
