@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=250_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the secondary C5 measurement")
     return ap.parse_args()
 
 
@@ -479,6 +480,10 @@ def main():
                "sample": f"{cnt} strided C3 targets through oracle kNN + shape solve + CSR + apply "
                          f"({secs:.2f} s, {cores} threads)"}
 
+    c5 = None
+    if rank == 0 and world == 1 and not args.no_c5:
+        c5 = measure_c5(mf, lib, dev, fp64_peak, hbm_peak)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -519,10 +524,62 @@ def main():
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "secondary": {"C5": c5},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_c5(mf, lib, dev, fp64_peak, hbm_peak):
+    """Config C5 (3D ball, N = 4M, n = 70, degree 4, laplacian + gradient) once
+    through the same stages (not part of the headline value): stage times with
+    CUDA events after one warm-up pass, the shape-solve roofline and the
+    one-pass four-family apply against HBM."""
+    import torch
+
+    from paper_1912_13282_b200 import workloads
+
+    w = workloads.c5()
+    nodes = mf.NodeSet(w.positions, w.types)
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=w.degree, scale="support", solver="lu")
+    u = torch.from_numpy(w.field).to(dev)
+    stream = torch.cuda.current_stream()
+    res = None
+    for it in range(2):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        nd = mf.find_closest_stencils(nodes, w.n)
+        ev[1].record(stream)
+        store = mf.compute_weights(nd, eng, w.families)
+        ev[2].record(stream)
+        keys = store.families
+        for k in keys:
+            store.matrix(k).plan(True)
+        ev[3].record(stream)
+        ys = store.apply_families(keys, u)
+        ev[4].record(stream)
+        torch.cuda.synchronize()
+        res = [a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])]
+        del store, nd, ys
+        torch.cuda.empty_cache()
+    knn_ms, shape_ms, plan_ms, apply_ms = res
+    n, l, r = w.n, 35, len(keys)
+    s_ = n + l
+    F = (2.0 / 3.0) * s_ ** 3 + 2.0 * r * s_ * s_
+    tflops = w.N * F / (shape_ms * 1e-3) / 1e12
+    nnz = w.N * n
+    b_apply = nnz * (8 * r + 4) + w.N * 8 + r * w.N * 8 + (w.N + 1) * 4
+    return {"workload": "C5: 3D ball, N=4,000,000, n=70, degree 4, laplacian + gradient (4 families)",
+            "stage_ms": {"knn": knn_ms, "shape_solve": shape_ms, "csr_and_plans": plan_ms,
+                         "apply_4_families_one_pass": apply_ms},
+            "stencils_per_s_through_step": w.N / (sum(res) * 1e-3),
+            "shape_roofline": {"bound": "fp64", "achieved": tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                               "frac": tflops / fp64_peak, "note": "F = (2/3)s^3 + 2rs^2, s = 105, r = 4"},
+            "apply_roofline": {"bound": "hbm", "achieved": b_apply / (apply_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                               "unit": "GB/s", "frac": b_apply / (apply_ms * 1e-3) / 1e9 / hbm_peak,
+                               "bytes": b_apply, "note": "stage incl. the field permutes (u gather, y scatters)"},
+            "timing": "one pass after one warm-up pass, CUDA events; not part of value"}
 
 
 def run_sharded(args, rank, world, local):
