@@ -192,7 +192,8 @@ class NodeSet:
         missing = np.flatnonzero(blk < 0)
         if missing.size:
             raise StencilError(f"node {int(idx[missing[0]])} has no stencil")
-        used = np.unique(blk)
+        bmin, bmax = int(blk.min()), int(blk.max())
+        used = np.array([bmin]) if bmin == bmax else np.unique(blk)  # (one block: no sort)
         sizes = sorted({self._blocks[b].size for b in used} - {None})
         if len(sizes) != 1 or any(self._blocks[b].size is None for b in used):
             all_sizes = set()
@@ -202,7 +203,8 @@ class NodeSet:
                 all_sizes |= {len(blkobj.row(int(k))) for k in rows}
             if len(all_sizes) != 1:
                 raise StencilError(f"stencil sizes differ: {sorted(all_sizes)}")
-        n = len(self._blocks[int(blk[0])].row(int(self._row[idx[0]])))
+        b0 = self._blocks[int(blk[0])]
+        n = b0.size if b0.mat is not None else len(b0.row(int(self._row[idx[0]])))  # (no host copy of a device block)
 
         def rows_of(b, sel_rows):
             """Device (k, n) int32 stencils of block b's rows sel_rows: blocks held as
