@@ -397,6 +397,20 @@ int mf_fill_accept(double* pos, double* hv, int32_t* nxt, int64_t count, int64_t
                    int32_t* accepted_idx, int64_t* n_accepted, int32_t* rounds, void* ws, size_t ws_bytes,
                    void* stream);
 
+/* The same recurrence with every branch decided on the device, so one
+ * iteration is a fixed launch sequence that can be captured in a CUDA graph
+ * and replayed past convergence without changing a bit (mf_bicgstab's
+ * results, bitwise).  state: mf_bicgstab_state_size device bytes, read back by
+ * the host as {double atol, rho, rho_prev, alpha, omega, beta, rr, rv, ts,
+ * tt; int64 it, maxiter; int32 done, info, pad}: done = 1 finished (info as
+ * mf_bicgstab, it = iterations, rr = last ||r||^2), 3 when b = 0 (x = b). */
+int mf_bicgstab_state_size(size_t* bytes);
+int mf_bicgstab_init(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, const double* b,
+                     const double* x, double rtol, double atol, int64_t maxiter, void* state, void* ws,
+                     size_t ws_bytes, void* stream);
+int mf_bicgstab_iter(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                     const mf_ilu0_t* M, double* x, void* state, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

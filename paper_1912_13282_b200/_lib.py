@@ -133,6 +133,9 @@ _SIGNATURES = {
     "mf_fill_accept": ([_P, _P, _P, _I64, _I64, ctypes.POINTER(FillGridT), _P, _P, _P, _P, _I64, _D, _P,
                         ctypes.POINTER(_I64), ctypes.POINTER(_I32), _P, _SZ, _P], _I32),
     "mf_heat_rows": ([_P, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P], _I32),
+    "mf_bicgstab_state_size": ([ctypes.POINTER(_SZ)], _I32),
+    "mf_bicgstab_init": ([_P, _P, _P, _I64, _P, _P, _D, _D, _I64, _P, _P, _SZ, _P], _I32),
+    "mf_bicgstab_iter": ([_P, _P, _P, _I64, ctypes.POINTER(Ilu0T), _P, _P, _P, _SZ, _P], _I32),
     "mf_heat_pack": ([_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_heat_steps": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _D, _D, ctypes.POINTER(NeumannT),
                        _I64, _P, _P, _P, ctypes.POINTER(HeatPackT), _P], _I32),

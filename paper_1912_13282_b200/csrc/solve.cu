@@ -332,6 +332,206 @@ __global__ void xupd_k(double* x, const double* __restrict__ ph, double alpha, c
 
 inline int vgrid(int64_t N) { return grid_cap(N, 256, 8); }
 
+// ---- device-controlled iteration (graph-capturable) ---------------------------
+// The same recurrence with every branch decided on the device: the scalars
+// live in a BicgState, every kernel returns at once when `done` is set, so a
+// graph of one iteration can be replayed any number of times past convergence
+// without changing a bit.
+struct BicgState {
+    double atol, rho, rho_prev, alpha, omega, beta, rr, rv, ts, tt;
+    long long it, maxiter;
+    int done;   // 0 running, 1 finished
+    int info;   // scipy's info once done
+    int phase;  // (unused padding)
+};
+
+__device__ __forceinline__ double dot_sum(const double* __restrict__ partial) {
+    double s = 0.0;
+    for (int i = 0; i < RED_BLOCKS; ++i) s += partial[i];
+    return s;
+}
+__global__ void __launch_bounds__(RED_THREADS) dot2_partial_k(const double* __restrict__ a, const double* __restrict__ b,
+                                                              const double* __restrict__ c, const double* __restrict__ e,
+                                                              int64_t N, double* partial, const BicgState* stt) {
+    if (stt->done) return;
+    __shared__ double sm[2][RED_THREADS / 32];
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < N; i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        s0 = fma(a[i], b[i], s0);
+        if (c) s1 = fma(c[i], e[i], s1);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(FULL, s0, o);
+        s1 += __shfl_xor_sync(FULL, s1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sm[0][threadIdx.x >> 5] = s0;
+        sm[1][threadIdx.x >> 5] = s1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s0 = threadIdx.x < RED_THREADS / 32 ? sm[0][threadIdx.x] : 0.0;
+        s1 = threadIdx.x < RED_THREADS / 32 ? sm[1][threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            s0 += __shfl_xor_sync(FULL, s0, o);
+            s1 += __shfl_xor_sync(FULL, s1, o);
+        }
+        if (threadIdx.x == 0) {
+            partial[blockIdx.x] = s0;
+            partial[RED_BLOCKS + blockIdx.x] = s1;
+        }
+    }
+}
+// step 1: ||r||, rho = (rt, r); the stop / breakdown tests and beta
+__global__ void bicg_head_k(const double* __restrict__ partial, BicgState* stt) {
+    if (threadIdx.x || stt->done) return;
+    const double rr = dot_sum(partial), rho = dot_sum(partial + RED_BLOCKS);
+    stt->rr = rr;
+    if (stt->it >= stt->maxiter) {
+        stt->done = 1;
+        stt->info = (int)(stt->maxiter > 2147483647LL ? 2147483647LL : stt->maxiter);
+        return;
+    }
+    if (sqrt(rr) < stt->atol) {
+        stt->done = 1;
+        stt->info = 0;
+        return;
+    }
+    if (fabs(rho) < DBL_EPSILON * DBL_EPSILON) {
+        stt->done = 1;
+        stt->info = -10;
+        return;
+    }
+    if (stt->it > 0) {
+        if (fabs(stt->omega) < DBL_EPSILON * DBL_EPSILON) {
+            stt->done = 1;
+            stt->info = -11;
+            return;
+        }
+        stt->beta = (rho / stt->rho_prev) * (stt->alpha / stt->omega);
+    }
+    stt->rho = rho;
+}
+__global__ void bicg_p_k(double* p, const double* __restrict__ v, const double* __restrict__ r, int64_t N,
+                         const BicgState* stt) {
+    if (stt->done) return;
+    const bool first = stt->it == 0;
+    const double om = stt->omega, be = stt->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = first ? r[i] : __dadd_rn(__dmul_rn(__dsub_rn(p[i], __dmul_rn(om, v[i])), be), r[i]);
+}
+// step 2: rv = (rt, v), alpha
+__global__ void bicg_alpha_k(const double* __restrict__ partial, BicgState* stt) {
+    if (threadIdx.x || stt->done) return;
+    const double rv = dot_sum(partial);
+    stt->rv = rv;
+    if (rv == 0.0) {
+        stt->done = 1;
+        stt->info = -11;
+        return;
+    }
+    stt->alpha = stt->rho / rv;
+}
+__global__ void bicg_axmy_k(double* r, const double* __restrict__ v, int64_t N, const BicgState* stt, int which) {
+    if (stt->done) return;
+    const double a = which == 0 ? stt->alpha : stt->omega;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = __dsub_rn(r[i], __dmul_rn(a, v[i]));
+}
+// step 3: ||s||: the half-step exit (x += alpha phat) decided here, applied by bicg_x_k
+__global__ void bicg_mid_k(const double* __restrict__ partial, BicgState* stt) {
+    if (threadIdx.x || stt->done) return;
+    const double ss = dot_sum(partial);
+    stt->rr = ss;
+    if (sqrt(ss) < stt->atol) {
+        stt->done = 2;  // half step: x += alpha phat still to apply
+        stt->info = 0;
+    }
+}
+__global__ void bicg_xhalf_k(double* x, const double* __restrict__ ph, int64_t N, BicgState* stt) {
+    if (stt->done != 2) return;
+    const double a = stt->alpha;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], __dmul_rn(a, ph[i]));
+}
+__global__ void bicg_xhalf_done_k(BicgState* stt) {
+    if (threadIdx.x == 0 && stt->done == 2) stt->done = 1;
+}
+// step 4: omega = (t, s) / (t, t)
+__global__ void bicg_omega_k(const double* __restrict__ partial, BicgState* stt) {
+    if (threadIdx.x || stt->done) return;
+    stt->ts = dot_sum(partial);
+    stt->tt = dot_sum(partial + RED_BLOCKS);
+    stt->omega = stt->ts / stt->tt;
+}
+__global__ void bicg_x_k(double* x, const double* __restrict__ ph, const double* __restrict__ sh, int64_t N,
+                         const BicgState* stt) {
+    if (stt->done) return;
+    const double a = stt->alpha, om = stt->omega;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(a, ph[i])), __dmul_rn(om, sh[i]));
+}
+__global__ void bicg_tail_k(BicgState* stt) {
+    if (threadIdx.x || stt->done) return;
+    stt->rho_prev = stt->rho;
+    stt->it += 1;
+}
+// ILU(0) substitutions and products that stop with the iteration
+__global__ void ilu_fwd_ctl_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                              const int8_t* __restrict__ part, const double* __restrict__ lu,
+                              const int32_t* __restrict__ rows, int cnt, const double* __restrict__ x, double* y,
+                              const BicgState* stt) {
+    if (stt->done) return;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+        const int i = rows[t];
+        double acc = x[i];
+        for (int p = indptr[i]; p < indptr[i + 1]; ++p)
+            if (part[p] < 0) acc -= lu[p] * y[indices[p]];
+        y[i] = acc;
+    }
+}
+__global__ void ilu_bwd_ctl_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                              const int8_t* __restrict__ part, const double* __restrict__ lu,
+                              const int32_t* __restrict__ diag, const int32_t* __restrict__ rows, int cnt, double* y,
+                              const BicgState* stt) {
+    if (stt->done) return;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+        const int i = rows[t];
+        double acc = y[i];
+        for (int p = indptr[i]; p < indptr[i + 1]; ++p)
+            if (part[p] > 0) acc -= lu[p] * y[indices[p]];
+        y[i] = acc / lu[diag[i]];
+    }
+}
+__global__ void spmv_ctl_k(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                           const double* __restrict__ data, const double* __restrict__ x, int64_t N, double* y,
+                           const BicgState* stt) {
+    if (stt->done) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int p = indptr[i]; p < indptr[i + 1]; ++p) acc = __dadd_rn(acc, __dmul_rn(data[p], x[indices[p]]));
+        y[i] = acc;
+    }
+}
+__global__ void copy_ctl_k(const double* __restrict__ a, int64_t N, double* b, const BicgState* stt) {
+    if (stt->done) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+__global__ void bicg_init_k(const double* __restrict__ partial, BicgState* stt, double rtol, double atol,
+                            long long maxiter) {
+    if (threadIdx.x) return;
+    const double bn = sqrt(dot_sum(partial));
+    stt->atol = fmax(atol, rtol * bn);
+    stt->it = 0;
+    stt->maxiter = maxiter;
+    stt->done = bn == 0.0 ? 3 : 0;  // 3: b == 0 (x = b, handled by the host)
+    stt->info = 0;
+    stt->rho_prev = stt->alpha = stt->omega = stt->beta = 0.0;
+}
+
 }  // namespace
 
 // ILU(0) application (shared by mf_ilu0_apply and mf_bicgstab)
@@ -523,7 +723,7 @@ extern "C" int mf_ilu0_apply(const mf_ilu0_t* M, const double* x, double* y, voi
 }
 
 extern "C" int mf_bicgstab_workspace_size(int64_t N, size_t* bytes) {
-    *bytes = align_up((size_t)N * 8) * 7 + align_up(RED_BLOCKS * 8) + 1024;
+    *bytes = align_up((size_t)N * 8) * 7 + align_up(2 * RED_BLOCKS * 8) + 1024;
     return MF_OK;
 }
 
@@ -659,5 +859,118 @@ extern "C" int mf_bicgstab(const int32_t* indptr, const int32_t* indices, const 
 #undef MF_TRY
     *iterations = it;
     *info = (int32_t)(maxiter > INT32_MAX ? INT32_MAX : maxiter);
+    return MF_OK;
+}
+
+
+// ---- device-controlled BiCGStab ---------------------------------------------------
+// state: BICG_STATE_BYTES device bytes (mf_bicgstab_state_size); ws as mf_bicgstab.
+extern "C" int mf_bicgstab_state_size(size_t* bytes) {
+    *bytes = sizeof(BicgState);
+    return MF_OK;
+}
+
+// r = b - A x, rt = r, ||b||, atol: the state is ready for mf_bicgstab_iter
+extern "C" int mf_bicgstab_init(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                                const double* b, const double* x, double rtol, double atol, int64_t maxiter,
+                                void* state, void* ws, size_t ws_bytes, void* stream) {
+    MF_REQUIRE(N >= 1 && maxiter >= 0 && state, "mf_bicgstab_init: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    Arena ar{(char*)ws, ws_bytes, 0, ws == nullptr};
+    double* r = ar.take<double>(N);
+    double* rt = ar.take<double>(N);
+    for (int k = 0; k < 5; ++k) ar.take<double>(N);  // p, v, phat, shat, t (same layout as mf_bicgstab_iter)
+    double* partial = ar.take<double>(2 * RED_BLOCKS);
+    MF_REQUIRE(ar.ok() && ws, "mf_bicgstab_init: workspace too small");
+    BicgState* stt = reinterpret_cast<BicgState*>(state);
+    dot_partial_k<<<RED_BLOCKS, RED_THREADS, 0, st>>>(b, b, N, partial);
+    MF_LAUNCH_CHECK();
+    bicg_init_k<<<1, 32, 0, st>>>(partial, stt, rtol, atol, (long long)maxiter);
+    MF_LAUNCH_CHECK();
+    const int g = vgrid(N);
+    resid_k<<<g, 256, 0, st>>>(indptr, indices, data, x, b, N, r);
+    MF_LAUNCH_CHECK();
+    copy2_k<<<g, 256, 0, st>>>(r, N, rt, nullptr);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+// one iteration of scipy's recurrence, every step gated by the device state (a
+// fixed launch sequence: capture it once in a graph and replay)
+extern "C" int mf_bicgstab_iter(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
+                                const mf_ilu0_t* M, double* x, void* state, void* ws, size_t ws_bytes, void* stream) {
+    MF_REQUIRE(N >= 1 && state, "mf_bicgstab_iter: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    Arena ar{(char*)ws, ws_bytes, 0, ws == nullptr};
+    double* r = ar.take<double>(N);
+    double* rt = ar.take<double>(N);
+    double* p = ar.take<double>(N);
+    double* v = ar.take<double>(N);
+    double* ph = ar.take<double>(N);
+    double* sh = ar.take<double>(N);
+    double* t = ar.take<double>(N);
+    double* partial = ar.take<double>(2 * RED_BLOCKS);
+    MF_REQUIRE(ar.ok() && ws, "mf_bicgstab_iter: workspace too small");
+    BicgState* stt = reinterpret_cast<BicgState*>(state);
+    const int g = vgrid(N);
+    auto precond = [&](const double* in, double* out) -> int {
+        if (!M) {
+            copy_ctl_k<<<g, 256, 0, st>>>(in, N, out, stt);
+            MF_LAUNCH_CHECK();
+            return MF_OK;
+        }
+        for (int c = 0; c < M->ncolors; ++c) {
+            const int a = M->color_off[c], cnt = M->color_off[c + 1] - a;
+            if (cnt <= 0) continue;
+            ilu_fwd_ctl_k<<<grid_cap(cnt, 128, 16), 128, 0, st>>>(M->indptr, M->indices, M->part, M->lu,
+                                                                  M->order + a, cnt, in, out, stt);
+            MF_LAUNCH_CHECK();
+        }
+        for (int c = M->ncolors - 1; c >= 0; --c) {
+            const int a = M->color_off[c], cnt = M->color_off[c + 1] - a;
+            if (cnt <= 0) continue;
+            ilu_bwd_ctl_k<<<grid_cap(cnt, 128, 16), 128, 0, st>>>(M->indptr, M->indices, M->part, M->lu, M->diag,
+                                                                  M->order + a, cnt, out, stt);
+            MF_LAUNCH_CHECK();
+        }
+        return MF_OK;
+    };
+    int rc;
+    dot2_partial_k<<<RED_BLOCKS, RED_THREADS, 0, st>>>(r, r, rt, r, N, partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_head_k<<<1, 32, 0, st>>>(partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_p_k<<<g, 256, 0, st>>>(p, v, r, N, stt);
+    MF_LAUNCH_CHECK();
+    if ((rc = precond(p, ph)) != MF_OK) return rc;
+    spmv_ctl_k<<<g, 256, 0, st>>>(indptr, indices, data, ph, N, v, stt);
+    MF_LAUNCH_CHECK();
+    dot2_partial_k<<<RED_BLOCKS, RED_THREADS, 0, st>>>(rt, v, nullptr, nullptr, N, partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_alpha_k<<<1, 32, 0, st>>>(partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_axmy_k<<<g, 256, 0, st>>>(r, v, N, stt, 0);
+    MF_LAUNCH_CHECK();
+    dot2_partial_k<<<RED_BLOCKS, RED_THREADS, 0, st>>>(r, r, nullptr, nullptr, N, partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_mid_k<<<1, 32, 0, st>>>(partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_xhalf_k<<<g, 256, 0, st>>>(x, ph, N, stt);
+    MF_LAUNCH_CHECK();
+    bicg_xhalf_done_k<<<1, 32, 0, st>>>(stt);
+    MF_LAUNCH_CHECK();
+    if ((rc = precond(r, sh)) != MF_OK) return rc;
+    spmv_ctl_k<<<g, 256, 0, st>>>(indptr, indices, data, sh, N, t, stt);
+    MF_LAUNCH_CHECK();
+    dot2_partial_k<<<RED_BLOCKS, RED_THREADS, 0, st>>>(t, r, t, t, N, partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_omega_k<<<1, 32, 0, st>>>(partial, stt);
+    MF_LAUNCH_CHECK();
+    bicg_x_k<<<g, 256, 0, st>>>(x, ph, sh, N, stt);
+    MF_LAUNCH_CHECK();
+    bicg_axmy_k<<<g, 256, 0, st>>>(r, t, N, stt, 1);
+    MF_LAUNCH_CHECK();
+    bicg_tail_k<<<1, 32, 0, st>>>(stt);
+    MF_LAUNCH_CHECK();
     return MF_OK;
 }

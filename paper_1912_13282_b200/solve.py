@@ -240,27 +240,68 @@ def solve_sparse(system, rhs=None, config: SolverConfig | None = None,
     else:
         x_d = b_d.clone()
         desc = None
-    lib = _lib.load()
-    size = ctypes.c_size_t(0)
-    _lib.check(lib.mf_bicgstab_workspace_size(N, ctypes.byref(size)), "mf_bicgstab_workspace_size")
-    ws = _lib.workspace(size.value)
-    iters = ctypes.c_int64(0)
-    info = ctypes.c_int32(0)
-    rnorm = ctypes.c_double(0.0)
-    _lib.check(lib.mf_bicgstab(matrix.indptr_device.data_ptr(), matrix.indices_device.data_ptr(),
-                               matrix.data_device.data_ptr(), N, desc, b_d.data_ptr(), x_d.data_ptr(),
-                               float(config.tol), 0.0, int(max_iter), ctypes.byref(iters), ctypes.byref(info),
-                               ctypes.byref(rnorm), ws.data_ptr(), size.value, _lib.stream_ptr()),
-               "mf_bicgstab")
+    iters, info, rnorm = _bicgstab_graph(matrix, desc, b_d, x_d, float(config.tol), int(max_iter))
     r_d = matrix.matvec_device(x_d)
     r_d.sub_(b_d)
     rhs_norm = float(torch.linalg.vector_norm(b_d))
     residual = float(torch.linalg.vector_norm(r_d)) / (rhs_norm if rhs_norm else 1.0)
-    if info.value != 0:
+    if info != 0:
         raise NumericalError(
-            f"bicgstab failed to converge in {iters.value} iterations "
-            f"(info={info.value}, residual={residual:.3e})"
+            f"bicgstab failed to converge in {iters} iterations "
+            f"(info={info}, residual={residual:.3e})"
         )
     u = x_d if return_device else x_d.cpu().numpy()
-    extra = {"preconditioner": repr(preconditioner), "recurrence_residual": rnorm.value}
-    return SolveResult(u=u, iterations=int(iters.value), residual=residual, converged=True, info=extra)
+    extra = {"preconditioner": repr(preconditioner), "recurrence_residual": rnorm}
+    return SolveResult(u=u, iterations=int(iters), residual=residual, converged=True, info=extra)
+
+
+_STATE_DT = np.dtype([("d", "<f8", 10), ("it", "<i8"), ("maxiter", "<i8"), ("done", "<i4"), ("info", "<i4"),
+                      ("pad", "<i4"), ("pad2", "<i4")])
+
+
+def _bicgstab_graph(matrix, desc, b_d, x_d, tol, max_iter, replays=8):
+    """scipy's bicgstab (mf_bicgstab_init / _iter): one iteration captured as a
+    CUDA graph and replayed in batches; the device state stops every kernel at
+    convergence, so over-shooting a batch changes nothing.  Returns (iterations,
+    info, last ||r||)."""
+    lib = _lib.load()
+    N = matrix.shape[0]
+    dev = x_d.device
+    size = ctypes.c_size_t(0)
+    _lib.check(lib.mf_bicgstab_workspace_size(N, ctypes.byref(size)), "mf_bicgstab_workspace_size")
+    ws = torch.empty(max(size.value, 1), dtype=torch.uint8, device=dev)  # owned: the graph holds its pointers
+    st_size = ctypes.c_size_t(0)
+    _lib.check(lib.mf_bicgstab_state_size(ctypes.byref(st_size)), "mf_bicgstab_state_size")
+    state = torch.zeros(max(st_size.value, _STATE_DT.itemsize), dtype=torch.uint8, device=dev)
+    ptrs = (matrix.indptr_device.data_ptr(), matrix.indices_device.data_ptr(), matrix.data_device.data_ptr())
+    _lib.check(lib.mf_bicgstab_init(*ptrs, N, b_d.data_ptr(), x_d.data_ptr(), tol, 0.0, int(max_iter),
+                                    state.data_ptr(), ws.data_ptr(), size.value, _lib.stream_ptr()),
+               "mf_bicgstab_init")
+
+    def read():
+        return np.frombuffer(state[: _STATE_DT.itemsize].cpu().numpy().tobytes(), dtype=_STATE_DT)[0]
+
+    s = read()
+    if s["done"] == 3:  # b == 0: x = b (solve.py: scipy returns b)
+        x_d.copy_(b_d)
+        return 0, 0, 0.0
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        # (capture_begin/end directly: the torch.cuda.graph context manager runs a
+        # full gc.collect() on entry, which costs more than a short solve)
+        graph.capture_begin()
+        try:
+            _lib.check(lib.mf_bicgstab_iter(*ptrs, N, desc, x_d.data_ptr(), state.data_ptr(), ws.data_ptr(),
+                                            size.value, _lib.stream_ptr()), "mf_bicgstab_iter")
+        finally:
+            graph.capture_end()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    while True:
+        for _ in range(replays):
+            graph.replay()
+        s = read()
+        if s["done"]:
+            return int(s["it"]), int(s["info"]), float(np.sqrt(s["d"][6]))
+        replays = min(replays * 2, 256)

@@ -193,3 +193,35 @@ def test_implicit_records():
         os.makedirs(out, exist_ok=True)
         with open(os.path.join(out, "implicit_parity.json"), "w") as fh:
             json.dump(RECORD, fh, indent=1, sort_keys=True)
+
+
+def test_graph_iteration_equals_host_loop(g):
+    """The device-controlled, graph-replayed BiCGStab (the solve_sparse path)
+    and the host-driven mf_bicgstab give the same iterate bitwise."""
+    import ctypes
+
+    from paper_1912_13282_b200 import _lib
+    from paper_1912_13282_b200.solve import Ilu0Preconditioner, SystemMatrix, _bicgstab_graph
+
+    mod = m()
+    nodes, store = problem(g, "dir2d", 15, inject=True)
+    out = []
+    mod.solve_poisson_implicit(nodes, store, terms=[(-1.0, "laplacian")], rhs=rhs_f,
+                               dirichlet={-1: lambda p: p[:, 0] * p[:, 1]}, system_out=out)
+    A, b = out[0]
+    M = Ilu0Preconditioner(A)
+    b_d = _lib.to_device(b, torch.float64)
+    x1 = M.apply_device(b_d)
+    x2 = x1.clone()
+    it1, info1, _ = _bicgstab_graph(A, ctypes.byref(M.desc), b_d, x1, 1e-10, 10 * A.shape[0])
+    lib = _lib.load()
+    size = ctypes.c_size_t(0)
+    lib.mf_bicgstab_workspace_size(A.shape[0], ctypes.byref(size))
+    ws = torch.empty(size.value, dtype=torch.uint8, device="cuda")
+    it2, info2, rn = ctypes.c_int64(0), ctypes.c_int32(0), ctypes.c_double(0)
+    _lib.check(lib.mf_bicgstab(A.indptr_device.data_ptr(), A.indices_device.data_ptr(), A.data_device.data_ptr(),
+                               A.shape[0], ctypes.byref(M.desc), b_d.data_ptr(), x2.data_ptr(), 1e-10, 0.0,
+                               10 * A.shape[0], ctypes.byref(it2), ctypes.byref(info2), ctypes.byref(rn),
+                               ws.data_ptr(), size.value, _lib.stream_ptr()), "mf_bicgstab")
+    assert (it1, info1) == (it2.value, info2.value)
+    assert torch.equal(x1, x2)
