@@ -224,6 +224,46 @@ __global__ void __launch_bounds__(256) plan_terms_k(const int32_t* __restrict__ 
         terms_finish<NT>(T, s, order ? (int64_t)order[r] : r);
     }
 }
+// every term reads the same field (several families of one operator applied to
+// one field, WeightStore.apply_families): u[c] loaded once per entry, four
+// entries in flight per row; each term's addends still in the row's order
+template <int NT>
+__global__ void __launch_bounds__(256) plan_terms1f_k(const int32_t* __restrict__ ell_idx,
+                                                      const int32_t* __restrict__ ell_len, int64_t N, int W,
+                                                      const int32_t* __restrict__ order, const TermsDev T) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const double* __restrict__ u = T.fld[0];
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        const int len = ell_len[r];
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double s[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) s[t] = 0.0;
+        int j = 0;
+        for (; j + 4 <= len; j += 4) {
+            int32_t c[4];
+            double uc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = __ldcs(ell_idx + base + 32 * (j + q));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) uc[q] = __ldg(u + c[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t e = base + 32 * (j + q);
+#pragma unroll
+                for (int t = 0; t < NT; ++t) s[t] = __dadd_rn(s[t], __dmul_rn(__ldcs(T.val[t] + e), uc[q]));
+            }
+        }
+        for (; j < len; ++j) {
+            const int64_t e = base + 32 * j;
+            const double uc = __ldg(u + __ldcs(ell_idx + e));
+#pragma unroll
+            for (int t = 0; t < NT; ++t) s[t] = __dadd_rn(s[t], __dmul_rn(__ldcs(T.val[t] + e), uc));
+        }
+        terms_finish<NT>(T, s, order ? (int64_t)order[r] : r);
+    }
+}
+
 
 template <int NT>
 __global__ void __launch_bounds__(128) rows_terms_k(const int32_t* __restrict__ indptr,
@@ -384,7 +424,10 @@ template <int NT>
 struct PlanTermsL {
     static int go(const int32_t* idx, const int32_t* len, int64_t N, int W, const int32_t* order, const TermsDev* T,
                   cudaStream_t st) {
-        plan_terms_k<NT><<<grid_of(N, 256), 256, 0, st>>>(idx, len, N, W, order, *T);
+        bool one_field = true;
+        for (int t = 1; t < NT; ++t) one_field = one_field && T->fld[t] == T->fld[0];
+        if (one_field) plan_terms1f_k<NT><<<grid_of(N, 256), 256, 0, st>>>(idx, len, N, W, order, *T);
+        else plan_terms_k<NT><<<grid_of(N, 256), 256, 0, st>>>(idx, len, N, W, order, *T);
         MF_LAUNCH_CHECK();
         return MF_OK;
     }
