@@ -245,6 +245,18 @@ def release_workspaces() -> None:
 
 
 _COPY_STREAM = None
+_SIDE_STREAMS: dict = {}
+
+
+def side_stream() -> torch.cuda.Stream:
+    """A second (lower-priority) stream of the current device for work that may
+    overlap the main stream's kernels (created once)."""
+    dev = device()
+    st = _SIDE_STREAMS.get(dev.index)
+    if st is None:
+        st = torch.cuda.Stream(device=dev, priority=0)
+        _SIDE_STREAMS[dev.index] = st
+    return st
 
 
 def to_device_async(a, dtype):

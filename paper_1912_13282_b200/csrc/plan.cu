@@ -106,6 +106,13 @@ __global__ void plan_ell_build(const int32_t* __restrict__ indptr, const int32_t
         if (ell_idx) ell_idx[e] = ci;
         if (ell_val) ell_val[e] = v;
     }
+    // W = 0 (no stored row has an entry): the loop above has no slots, the
+    // lengths still have to be written (they are read by every apply)
+    if (W == 0 && ell_len)
+        for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t ro = order ? order[r] : r;
+            ell_len[r] = indptr[ro + 1] - indptr[ro];
+        }
 }
 
 // Block per 32-row tile: the tile's 32 W entries are built by one block, so

@@ -509,8 +509,16 @@ class WeightStore:
         r = self._row(i)
         return self.values[key][r * self.n:(r + 1) * self.n]
 
+    def _adopt_structure(self, s, ev):
+        self._structure = s
+        self._structure_ev = ev
+
     def structure(self) -> _CsrStructure:
         """The canonical CSR structure every family shares (built once)."""
+        ev = getattr(self, "_structure_ev", None)
+        if ev is not None:  # built on the side stream: order after it
+            torch.cuda.current_stream().wait_event(ev)
+            self._structure_ev = None
         if self._structure is None:
             self._structure = _CsrStructure(self.n_nodes, self.rows_device(), self.stencils_device, self.n,
                                             self.positions_device)
@@ -817,6 +825,11 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
         stencils_d = nodes.stencil_matrix_device(rows)
         rows_d = _lib.to_device(rows, torch.int64)
     n = int(stencils_d.shape[1]) if rows.size else 0
+    # the canonical CSR structure and the locality order depend on the stencils
+    # only: on large stores they are built on a side stream while the shape
+    # solve (and its re-solve pass, which leaves most SMs idle) runs
+    pre = _structure_async(len(nodes), rows_d, stencils_d, n, nodes.positions_device()) \
+        if rows.size >= ASYNC_STRUCTURE_ROWS else None
     values = {}
     for eng, sub in groups:
         if _batchable(eng, sub):
@@ -824,8 +837,11 @@ def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
         else:
             values.update(_run_general(nodes, eng, sub, rows, rows_d, stencils_d, n))
     values = {k: values[k] for k in fams}
-    return WeightStore(len(nodes), rows, stencils_d, values, n, rows_d=rows_d,
+    store = WeightStore(len(nodes), rows, stencils_d, values, n, rows_d=rows_d,
                        positions_d=nodes.positions_device())
+    if pre is not None:
+        store._adopt_structure(*pre)
+    return store
 
 
 _ELEMENTARY = (Identity, FirstDerivative, SecondDerivative, Laplacian)
@@ -859,6 +875,28 @@ def _check_engine(engine, fams):
                 raise ConfigError(f"family {key!r}: operator {elem!r} has no GPU implementation")
     if _batchable(engine, fams):
         _check_batchable(engine)
+
+
+ASYNC_STRUCTURE_ROWS = 1 << 16
+
+
+def _structure_async(n_nodes, rows_d, stencils_d, n, positions_d):
+    """(_CsrStructure, event): the structure and its Morton order built on the
+    side stream after the stencils are ready; the event marks completion."""
+    main = torch.cuda.current_stream()
+    side = _lib.side_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        s = _CsrStructure(n_nodes, rows_d, stencils_d, n, positions_d)
+        s._order(True)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    for t in (rows_d, stencils_d, positions_d):
+        if isinstance(t, torch.Tensor):
+            t.record_stream(side)
+    for t in (s.indptr, s.indices, s.perm, s._dup) + tuple(s._morton or ()):
+        t.record_stream(main)
+    return s, ev
 
 
 def _check_batchable(engine):
