@@ -301,25 +301,21 @@ def main():
         store = mf.WeightStore(N, all_idx, st, {"laplacian": w[:, 0, :]}, n, rows_d=rows_d, positions_d=pos_d)
         store._adopt_structure(*pre)
         mat = store.matrix("laplacian")
-        mat.plan(True)
+        order_p, idx_p, val_p, len_p = mat.plan_direct()
         hm.append(time.perf_counter())
         if ev:
             ev[3].record(stream)
-        # mat.apply_device(u_d), spelled out through the C ABI so the ELL kernel
-        # itself is bracketed by events (u gather / y scatter around it)
-        p = mat.plan(True)
+        # mat.apply_device(u_d), spelled out through the C ABI so the apply kernel
+        # is bracketed by events: one launch (Morton-row plan, node-numbered
+        # columns: the field is read in place, the result scattered by the kernel)
         y = torch.empty(N, dtype=torch.float64, device=dev)
-        _lib.check(lib.mf_permute(u_d.data_ptr(), p.order.data_ptr(), N, 0, su.data_ptr(), _lib.stream_ptr()),
-                   "mf_permute")
         if ev:
             kev[0].record(stream)
-        _lib.check(lib.mf_plan_apply(p.ell_idx.data_ptr(), p.ell_val.data_ptr(), p.ell_len.data_ptr(), N, p.W,
-                                     None, su.data_ptr(), sy.data_ptr(), None, None, _lib.stream_ptr()),
-                   "mf_plan_apply")
+        _lib.check(lib.mf_plan_apply_direct(idx_p.data_ptr(), val_p.data_ptr(), len_p.data_ptr(), N, n,
+                                            order_p.data_ptr(), u_d.data_ptr(), y.data_ptr(), _lib.stream_ptr()),
+                   "mf_plan_apply_direct")
         if ev:
             kev[1].record(stream)
-        _lib.check(lib.mf_permute(sy.data_ptr(), p.order.data_ptr(), N, 1, y.data_ptr(), _lib.stream_ptr()),
-                   "mf_permute")
         hm.append(time.perf_counter())
         if ev:
             ev[4].record(stream)
@@ -504,10 +500,10 @@ def main():
                          "frac": phs_tflops / fp64_peak, "traffic": ncu_traffic("phs_ns2"),
                          "note": "F=(2/3)s^3+2rs^2 per stencil (s=45, r=1); peak = DFMA probe measured "
                                  "in this run (MEASURED_PEAKS.json has no fp64 entry)"},
-            "apply_roofline": {"bound": "hbm", "kernel": "plan_apply_k (Morton-ordered ELL-32 row sums)",
+            "apply_roofline": {"bound": "hbm", "kernel": "plan_apply_direct_k (Morton-ordered ELL-32 row sums, node-numbered columns, result scattered in-kernel)",
                                "achieved": ell_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ell_gbs / hbm_peak,
-                               "kernel_ms": ell_ms, "stage_gbs_incl_permutes": apply_gbs,
-                               "traffic": ncu_traffic("plan_apply_k"), "bytes_per_launch": b_apply,
+                               "kernel_ms": ell_ms, "stage_gbs": apply_gbs,
+                               "traffic": ncu_traffic("plan_apply_direct_k"), "bytes_per_launch": b_apply,
                                "note": "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"},
             "knn_roofline": {"bound": "latency/issue (reported against HBM)", "kernel": "mf_knn (fast passes + fallback)",
                              "achieved": (N * 3 * 8 + N * n * 4) / (knn_ms * 1e-3) / 1e9, "peak": hbm_peak,

@@ -157,6 +157,11 @@ int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_t* order, i
 int mf_plan_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N,
                   int32_t W, const int32_t* order, const int32_t* inv, int32_t* ell_idx,
                   double* ell_val, int32_t* ell_len, void* stream);
+/* A plan built with order but inv = NULL keeps the columns in node numbering:
+ * mf_plan_apply_direct then reads u in node order and writes y[order[r]] (one
+ * launch, no permutes; bitwise the same sums). */
+int mf_plan_apply_direct(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
+                         int32_t W, const int32_t* order, const double* u, double* y, void* stream);
 /* y = A u in node order; with an order, u/y are permuted through scratch_u/scratch_y (N each) */
 int mf_plan_apply(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
                   int32_t W, const int32_t* order, const double* u, double* y, double* scratch_u,

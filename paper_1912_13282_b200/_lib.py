@@ -110,6 +110,7 @@ _SIGNATURES = {
     "mf_order_workspace_size": ([_I64, ctypes.POINTER(_SZ)], _I32),
     "mf_locality_order": ([_P, _I64, _I32, _P, _P, _P, _SZ, _P], _I32),
     "mf_plan_build": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
+    "mf_plan_apply_direct": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P], _I32),
     "mf_plan_apply": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P], _I32),
     "mf_permute": ([_P, _P, _I64, _I32, _P, _P], _I32),
     "mf_plan_apply_terms": ([_P, _P, _I64, _I32, _P, ctypes.POINTER(TermsT), _P], _I32),

@@ -354,7 +354,7 @@ extern "C" int mf_locality_order(const double* pos, int64_t N, int32_t d, int32_
 extern "C" int mf_plan_build(const int32_t* indptr, const int32_t* indices, const double* data, int64_t N, int32_t W,
                              const int32_t* order, const int32_t* inv, int32_t* ell_idx, double* ell_val,
                              int32_t* ell_len, void* stream) {
-    MF_REQUIRE(N >= 0 && W >= 0 && ((order == nullptr) == (inv == nullptr)), "mf_plan_build: bad arguments");
+    MF_REQUIRE(N >= 0 && W >= 0 && (order != nullptr || inv == nullptr), "mf_plan_build: bad arguments");
     int64_t total = ((N + 31) / 32) * 32 * (int64_t)W;
     if (total == 0 && N == 0) return MF_OK;
     int64_t work = total > N ? total : N;
@@ -477,6 +477,39 @@ extern "C" int mf_permute(const double* src, const int32_t* order, int64_t N, in
     if (N == 0) return MF_OK;
     if (scatter) plan_scatter<<<grid_of(N, 256), 256, 0, (cudaStream_t)stream>>>(src, order, N, dst);
     else plan_gather<<<grid_of(N, 256), 256, 0, (cudaStream_t)stream>>>(src, order, N, dst);
+    MF_LAUNCH_CHECK();
+    return MF_OK;
+}
+
+// rows in the plan's (Morton) order, columns in node numbering: the field is read
+// in node order straight from L2 (it is N doubles) and each row's sum lands at
+// y[order[r]] -- one launch, no permutes of the field or the result
+__global__ void __launch_bounds__(256) plan_apply_direct_k(const int32_t* __restrict__ ell_idx,
+                                                           const double* __restrict__ ell_val,
+                                                           const int32_t* __restrict__ ell_len, int64_t N, int W,
+                                                           const int32_t* __restrict__ order,
+                                                           const double* __restrict__ u, double* __restrict__ y) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        const int len = ell_len[r];
+        const int64_t base = (r >> 5) * 32 * (int64_t)W + (r & 31);
+        double acc = 0.0;
+#pragma unroll 5
+        for (int j = 0; j < len; ++j) {
+            const double a = __ldcs(ell_val + base + 32 * j);
+            const int32_t c = __ldcs(ell_idx + base + 32 * j);
+            acc = __dadd_rn(acc, __dmul_rn(a, __ldg(u + c)));
+        }
+        y[order[r]] = acc;
+    }
+}
+
+extern "C" int mf_plan_apply_direct(const int32_t* ell_idx, const double* ell_val, const int32_t* ell_len, int64_t N,
+                                    int32_t W, const int32_t* order, const double* u, double* y, void* stream) {
+    MF_REQUIRE(N >= 0 && W >= 0 && order, "mf_plan_apply_direct: bad arguments");
+    if (N == 0) return MF_OK;
+    plan_apply_direct_k<<<grid_of(N, 256), 256, 0, (cudaStream_t)stream>>>(ell_idx, ell_val, ell_len, N, W, order, u,
+                                                                            y);
     MF_LAUNCH_CHECK();
     return MF_OK;
 }

@@ -247,6 +247,30 @@ class _CsrStructure:
             self._plans[ordered] = (order, inv, ell_idx, ell_len)
         return self._plans[ordered]
 
+    def plan_direct(self, data):
+        """(order, ell_idx, ell_val, ell_len) of a Morton-row plan whose columns stay
+        in node numbering (mf_plan_apply_direct: one launch, no permutes).  Values
+        are those of `data`; the index arrays are built once."""
+        if self.positions_d is None:  # no positions: no locality order (node-ordered plan instead)
+            return None
+        total = ((self.N + 31) // 32) * 32 * self.n
+        order, _ = self._order(True)
+        val = torch.empty(max(total, 1), dtype=torch.float64, device=data.device)
+        fresh = getattr(self, "_direct", None) is None
+        if fresh:
+            idx = torch.empty(max(total, 1), dtype=torch.int32, device=data.device)
+            ln = torch.empty(max(self.N, 1), dtype=torch.int32, device=data.device)
+        else:
+            idx, ln = self._direct
+        _lib.check(_lib.load().mf_plan_build(self.indptr.data_ptr(), self.indices.data_ptr(), data.data_ptr(),
+                                             self.N, self.n, order.data_ptr(), None,
+                                             idx.data_ptr() if fresh else None, val.data_ptr(),
+                                             ln.data_ptr() if fresh else None, _lib.stream_ptr()),
+                   "mf_plan_build")
+        if fresh:
+            self._direct = (idx, ln)
+        return order, idx, val, ln
+
     def plan_values(self, data, ordered: bool):
         """ELL values of `data` in the plan's layout (the first call also builds the
         structure arrays in the same pass over the CSR)."""
@@ -338,11 +362,26 @@ class DeviceCSR:
             self._plan[ordered] = ApplyPlan(order, inv, idx, val, ln, self._s.N, self._s.n)
         return self._plan[ordered]
 
+    def plan_direct(self):
+        """The Morton-row plan with node-numbered columns (built once per matrix)."""
+        if getattr(self, "_pd", None) is None:
+            self._pd = self._s.plan_direct(self.data_device)
+        return self._pd
+
     def apply_device(self, u_d: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """y = A u on the device through the locality-ordered plan (mf_plan_apply)."""
+        """y = A u on the device: the Morton-row plan read with node-numbered columns
+        (mf_plan_apply_direct, one launch; the field is L2-resident), or the
+        node-ordered plan when the store has no positions."""
         lib = _lib.load()
         N = self._s.N
         y = out if out is not None else torch.empty(N, dtype=torch.float64, device=u_d.device)
+        pd = self.plan_direct()
+        if pd is not None:
+            order, idx, val, ln = pd
+            _lib.check(lib.mf_plan_apply_direct(idx.data_ptr(), val.data_ptr(), ln.data_ptr(), N, self._s.n,
+                                                order.data_ptr(), u_d.data_ptr(), y.data_ptr(), _lib.stream_ptr()),
+                       "mf_plan_apply_direct")
+            return y
         p = self.plan(True)
         su = sy = None
         if p.ordered:
@@ -559,7 +598,7 @@ class WeightStore:
         # the field's host-to-device copy overlaps the CSR and apply-plan builds
         u_d, ready = _lib.to_device_async(arr, torch.float64)
         mat = self.matrix(key)
-        mat.plan(True)
+        mat.plan_direct()
         torch.cuda.current_stream(u_d.device).wait_event(ready)
         y = mat.apply_device(u_d)
         return _result_to_host(y, mat._s)
