@@ -296,3 +296,35 @@ def to_device(a, dtype) -> torch.Tensor:
 
 
 SENTINEL_OK = int.from_bytes(b"\x7f" * 8, "little", signed=True)
+
+
+class nvtx_range:
+    """NVTX range around a public entry point (a no-op without a CUDA device)."""
+
+    def __init__(self, name):
+        self.name = name
+        self.on = False
+
+    def __enter__(self):
+        if torch.cuda.is_available():
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            torch.cuda.nvtx.range_pop()
+        return False
+
+
+def traced(name):
+    """Decorator: run the function inside an NVTX range `name`."""
+    def wrap(fn):
+        import functools
+
+        @functools.wraps(fn)
+        def inner(*a, **k):
+            with nvtx_range(name):
+                return fn(*a, **k)
+        return inner
+    return wrap

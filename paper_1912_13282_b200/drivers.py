@@ -60,6 +60,7 @@ def _instability(step, peak):
     )
 
 
+@_lib.traced("meshfree.run_heat_explicit")
 def run_heat_explicit(
     nodes,
     store,
@@ -348,6 +349,7 @@ def assemble_poisson_system(nodes, store, *, terms, rhs, dirichlet=None, neumann
     return SystemMatrix(indptr, indices[: nnz.value], data[: nnz.value], n), rhs_vec
 
 
+@_lib.traced("meshfree.solve_poisson_implicit")
 def solve_poisson_implicit(
     nodes,
     store,

@@ -310,6 +310,7 @@ class _DeviceFill:
         return acc[: na.value].cpu().numpy()
 
 
+@_lib.traced("meshfree.fill_interior")
 def fill_interior(nodes, shape, h, seed: int = 0, *, interior_tag: int = 1, gamma: float = 0.75,
                   n_candidates: int = 15, start=None, max_nodes: int = 4_000_000):
     """Fill the interior of ``shape`` with nodes spaced by ``h`` (fill.py:204-298).

@@ -206,6 +206,7 @@ def _finalize(system):
     raise ConfigError("solve_sparse needs a SparseSystem or a matrix and a right-hand side")
 
 
+@_lib.traced("meshfree.solve_sparse")
 def solve_sparse(system, rhs=None, config: SolverConfig | None = None,
                  preconditioner=None, *, return_device: bool = False) -> SolveResult:
     """Solve ``M u = r`` from a SparseSystem or an explicit (matrix, rhs) (solve.py:65-108).

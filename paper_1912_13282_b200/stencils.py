@@ -46,6 +46,7 @@ def _is_all(which) -> bool:
     return which is None or (isinstance(which, str) and which == "all")
 
 
+@_lib.traced("meshfree.find_closest_stencils")
 def find_closest_stencils(nodes: NodeSet, n: int, for_which=None, search_among=None) -> NodeSet:
     """Attach n-nearest-neighbour stencils to the selected nodes.
 

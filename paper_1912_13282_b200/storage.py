@@ -563,6 +563,7 @@ class WeightStore:
                                             self.positions_device)
         return self._structure
 
+    @_lib.traced("meshfree.WeightStore.matrix")
     def matrix(self, key: str) -> DeviceCSR:
         """Canonical CSR view: N x N, rows only for stored nodes."""
         if key not in self._matrices:
@@ -585,6 +586,7 @@ class WeightStore:
         out = self._combine([[(key, 0)]], [field], i)
         return float(out[0][0]) if scalar else out[0]
 
+    @_lib.traced("meshfree.WeightStore.apply_all")
     def apply_all(self, key: str, field):
         """(L u) at every stored node as a length-N vector (zeros elsewhere)."""
         if isinstance(field, torch.Tensor) and field.is_cuda:
@@ -799,6 +801,7 @@ def _host_arange(n: int) -> np.ndarray:
     return a
 
 
+@_lib.traced("meshfree.compute_weights")
 def compute_weights(nodes, engine, families, for_which=None) -> WeightStore:
     """Evaluate ``engine`` on every selected node for all families (storage.py:258-307).
 
