@@ -697,24 +697,28 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
                 base += __popc(bal);
             }
             const int S = base;
-            if (lane < 4) sm.sk32[S + lane] = 0xffffffffu;  // pad to a multiple of 4
+            if (lane < 4) sm.sk32[S + lane] = 0x7fffffffu;  // pad to a multiple of 4
             __syncwarp();
             // ranks on the high word of d2 (monotone in d2: four keys per 16-byte load,
             // two survivors per lane); equal high words collide in `slot` and fall back
-            // to the full key
+            // to the full key.  d2 is finite and >= +0, so every key (and the pad) is
+            // below 2^31 and [v < d] is the sign bit of v - d: one IADD + one LEA.HI
+            // per comparison instead of ISETP + IADD + a predicated move
             {
                 const int ea = lane, eb = lane + 32;
-                const uint32_t da = ea < S ? sm.sk32[ea] : 0xffffffffu;
-                const uint32_t db = eb < S ? sm.sk32[eb] : 0xffffffffu;
-                int ra = 0, rb = 0;
+                const uint32_t da = ea < S ? sm.sk32[ea] : 0u;
+                const uint32_t db = eb < S ? sm.sk32[eb] : 0u;
+                uint32_t ra = 0, rb = 0, ra2 = 0, rb2 = 0;
 #pragma unroll 4
                 for (int f = 0; f < S; f += 4) {
                     const uint4 v = *reinterpret_cast<const uint4*>(sm.sk32 + f);
-                    ra += (v.x < da) + (v.y < da) + (v.z < da) + (v.w < da);
-                    rb += (v.x < db) + (v.y < db) + (v.z < db) + (v.w < db);
+                    ra += ((v.x - da) >> 31) + ((v.y - da) >> 31);
+                    ra2 += ((v.z - da) >> 31) + ((v.w - da) >> 31);
+                    rb += ((v.x - db) >> 31) + ((v.y - db) >> 31);
+                    rb2 += ((v.z - db) >> 31) + ((v.w - db) >> 31);
                 }
-                if (ea < S) sm.srank[ea] = ra;
-                if (eb < S) sm.srank[eb] = rb;
+                if (ea < S) sm.srank[ea] = (int)(ra + ra2);
+                if (eb < S) sm.srank[eb] = (int)(rb + rb2);
             }
             __syncwarp();
             for (int e = lane; e < S; e += 32) sm.slot[sm.srank[e]] = e;
