@@ -720,6 +720,22 @@ __global__ void __launch_bounds__(CTA_THREADS) phs_ns_cta(PhsArgs a) {
 //     the warps, the particular solution's residuals riding as extra columns;
 //   * the pivot-free Gauss-Jordan on [K | b] is register-resident the same way.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void cta_cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cta_cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cta_cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cta_cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// barrier over the first `count` threads of the block (ids 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 template <int NN, int DD, int DEG, int NF>
 struct Cta2Cfg {
     static constexpr int LL = binom(DEG + DD, DD);
@@ -731,19 +747,21 @@ struct Cta2Cfg {
     static constexpr int GP = LL | 1;        // [Q; g] pitch
     static constexpr int YP = ((LL + 3) / 8) * 8 + 4;  // Y column pitch, 4 mod 8 (conflict-free fragments)
     static constexpr int KP = MR | 1;
-    // register-resident sweeps: thread = (column, row group)
-    static constexpr int QG = CTA_THREADS / LL;          // row groups of the [Q; g] sweep
-    static constexpr int QI = (RG + QG - 1) / QG;        // rows per thread
-    static constexpr int KG = CTA_THREADS / MR;          // row groups of the [K | b] sweep
-    static constexpr int KI = (M + KG - 1) / KG;
+    // sweeps with rows in lanes: a lane pair per row, one column half each
+    static constexpr int QH = (LL + 1) / 2;              // [Q; g] columns per lane (halves)
+    static constexpr int QWARPS = (RG + 15) / 16;        // warps of the [Q; g] sweep
+    static constexpr int KH = (MR + 1) / 2;              // [K | b] columns per lane (interleaved)
+    static constexpr int KWARPS = (MR + 15) / 16;        // warps of the [K | b] elimination
+    static constexpr int UPK = MR;                       // pivot-row slot pitch
     static constexpr int RT = (LL + 7) / 8, CT = (MR + 7) / 8, MT = (M + 7) / 8;
     // shared layout (doubles)
     static constexpr int LOC = 0;
-    // Phi packed (upper triangle with the diagonal, row-major): 3 stencils per SM
-    // fit in shared memory; [K | b] reuses the region once Phi is consumed
-    static constexpr int EPK = NN * (NN + 1) / 2;
+    // Phi in full (both triangles, node order): two stencils per SM (the register
+    // budget's limit) fit in shared memory; [K | b] and the elimination's pivot
+    // rows reuse the region once Phi is consumed
+    static constexpr int EFULL = NN * EP;
     static constexpr int E = LOC + ((NN * DD + 1) & ~1);
-    static constexpr int G = E + ((EPK + 1) & ~1);
+    static constexpr int G = E + ((EFULL + 1) & ~1);
     static constexpr int F = G + ((RG * GP + 1) & ~1);
     static constexpr int Y = F + NN * NR;
     static constexpr int K = E;
@@ -753,23 +771,24 @@ struct Cta2Cfg {
     static constexpr int COLK = PROW + 128;              // 2 x 80
     static constexpr int RED = COLK + 160;               // reductions / candidates
     static constexpr int INTS = RED + 4 * CTA_WARPS + 16;  // isp[NN], piv[LL], nonpiv[M] (ints)
-    static constexpr int TOTAL = INTS + (NN + LL + M + 16) / 2 + 2;
-    static_assert(QG * LL <= CTA_THREADS && KG * MR <= CTA_THREADS, "sweep layouts");
+    static constexpr int AUX = INTS + (NN + LL + M + 16) / 2 + 2;  // partial maxima, flags, pivot keys
+    static constexpr int SIDX = AUX + 8 + QWARPS + 1;    // staged next-stencil indices (ints), row
+    static constexpr int SROW = 2 * ((NN + 1) / 2);       // int offset of the row (8-byte aligned)
+    static constexpr int SPOS = SIDX + SROW / 2 + 1;      // staged next-stencil positions, centre
+    static constexpr int TOTAL = SPOS + NN * DD + DD + 1;
+    static_assert(NN * DD + DD <= CTA_THREADS, "one staged position per thread");
+    static_assert(QWARPS < CTA_WARPS && CTA_WARPS - QWARPS <= 3 && KWARPS <= CTA_WARPS, "sweep layouts");
+    static_assert(NN % 2 == 0 && NN < 128, "Phi row pairing / pivot keys");
+    static_assert(M * UPK <= EFULL, "pivot-row slots fit the Phi region");
     static_assert(MR <= 64 && RG <= 80 && M <= 80, "pivot buffers");
-    static_assert(M * KP <= EPK, "[K | b] fits the Phi region");
-    static constexpr int TILES_PER_WARP = (MT * CT + CTA_WARPS - 1) / CTA_WARPS;
-    // packed offset of Phi(i, j)
-    __device__ __forceinline__ static int po(int i, int j) {
-        const int lo = i < j ? i : j, hi = i < j ? j : i;
-        return lo * (2 * NN - lo + 1) / 2 + (hi - lo);
-    }
+    static_assert(M * KP <= EFULL, "[K | b] fits the Phi region");
 };
 
 template <int NN, int DD, int DEG, int NF>
-__global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
+__global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
     using C = Cta2Cfg<NN, DD, DEG, NF>;
     constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, GP = C::GP, YP = C::YP,
-                  KP = C::KP, QG = C::QG, QI = C::QI, KG = C::KG, KI = C::KI;
+                  KP = C::KP, EP = C::EP;
     extern __shared__ __align__(16) double sm2[];
     double* loc = sm2 + C::LOC;
     double* E = sm2 + C::E;
@@ -787,20 +806,59 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
     int* isp = reinterpret_cast<int*>(sm2 + C::INTS);
     int* piv = isp + NN;
     int* nonpiv = piv + LL;
+    double* aux = sm2 + C::AUX;
+#ifdef MF_CTA_TIMING
+    long long ts_[12] = {};
+#define MF_TS(i) if (tid == 0) ts_[i] = clock64()
+#else
+#define MF_TS(i)
+#endif
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
     const PhsParams& P = a.P;
 
+    // The next stencil's node positions are staged by cp.async while the current
+    // one is solved: its node indices (and row) right after the coordinates are
+    // read, its positions once the sweep has joined (two dependent global loads
+    // off the chain)
+    int* sidx = reinterpret_cast<int*>(sm2 + C::SIDX);  // NN node indices, then the row (int64)
+    double* spos = sm2 + C::SPOS;                        // NN * DD positions, then the centre
+    auto stage_idx = [&](int64_t id) {
+        if (id < a.m) {
+            if (tid < NN) cta_cp_async4(sidx + tid, a.stencils + id * NN + tid);
+            else if (tid == NN) cta_cp_async8(sidx + C::SROW, a.rows + id);
+        }
+        cta_cp_async_commit();
+    };
+    auto stage_pos = [&](int64_t id) {
+        if (id < a.m) {
+            if (tid < NN * DD) {
+                const int j = tid / DD, ax = tid - j * DD;
+                cta_cp_async8(spos + tid, a.pos + (int64_t)sidx[j] * DD + ax);
+            } else if (tid < NN * DD + DD) {
+                const int64_t rw = *reinterpret_cast<const int64_t*>(sidx + C::SROW);
+                cta_cp_async8(spos + tid, a.pos + rw * DD + (tid - NN * DD));
+            }
+        }
+        cta_cp_async_commit();
+    };
+    stage_idx(blockIdx.x);
+    cta_cp_async_wait_all();
+    __syncthreads();
+    stage_pos(blockIdx.x);
+
     for (int64_t idx = blockIdx.x; idx < a.m; idx += gridDim.x) {
-        const int64_t row = a.rows[idx];
-        const int32_t* sti = a.stencils + idx * NN;
         // ---- local coordinates, scale, family factors
+        MF_TS(0);
+        cta_cp_async_wait_all();
+        __syncthreads();  // staged positions (and indices) visible
         for (int e = tid; e < NN * DD; e += CTA_THREADS) {
-            const int j = e / DD, ax = e - j * DD;
-            loc[e] = a.pos[(int64_t)sti[j] * DD + ax] - a.pos[row * DD + ax];
+            const int ax = e % DD;
+            loc[e] = spos[e] - spos[NN * DD + ax];
         }
         for (int i = tid; i < NN; i += CTA_THREADS) isp[i] = 0;
         __syncthreads();
+        stage_idx(idx + gridDim.x);  // sidx was consumed by the last position staging
         int stat = 0;
         double sc = 1.0;
         if (P.scale_code != MF_SCALE_NONE) {
@@ -826,25 +884,9 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
         for (int e = tid; e < NN * DD; e += CTA_THREADS) loc[e] *= rs;
         __syncthreads();
 
-        // ---- Phi (zero diagonal), [Q; g], node right-hand sides, ||A||_inf
-        double r2min = INFINITY, rc2max = 0.0;
-        for (int e = tid; e < NN * NN; e += CTA_THREADS) {
-            const int i = e / NN, j = e - i * NN;
-            if (j < i) continue;
-            double v = 0.0;
-            if (j > i) {
-                double df = loc[i * DD] - loc[j * DD];
-                double r2 = df * df;
-#pragma unroll
-                for (int ax = 1; ax < DD; ++ax) {
-                    df = loc[i * DD + ax] - loc[j * DD + ax];
-                    r2 = fma(df, df, r2);
-                }
-                r2min = r2 < r2min ? r2 : r2min;
-                v = r2 * (r2 * fast_rsqrt(fmax(r2, 1e-300)));
-            }
-            E[C::po(i, j)] = v;
-        }
+        // ---- [Q; g] and the node right-hand sides (all threads)
+        MF_TS(1);
+        double rc2max = 0.0;
         for (int i = tid; i < NN; i += CTA_THREADS) {
             double x[DD], q[LL];
 #pragma unroll
@@ -866,125 +908,166 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
             const int f = e / LL, m = e - f * LL;
             G[(NN + f) * GP + m] = f < NF ? __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + m], facs[f]) : probe_sign(idx, NN + m);
         }
-        __syncthreads();
-        r2min = block_reduce_min(r2min, red);
-        rc2max = block_reduce_max(rc2max, red);
-        double anorm = 0.0;
-        for (int r = tid; r < NN + LL; r += CTA_THREADS) {
-            double acc = 0.0;
-            if (r < NN) {
-                for (int j = 0; j < NN; ++j) acc += E[C::po(j, r)];  // r^3 >= 0
-                for (int m = 0; m < LL; ++m) acc += fabs(G[r * GP + m]);
-            } else {
-                for (int i = 0; i < NN; ++i) acc += fabs(G[i * GP + (r - NN)]);
-            }
-            anorm = fmax(anorm, acc);
-        }
-        anorm = block_reduce_max(anorm, red);
+        unsigned* qkw = reinterpret_cast<unsigned*>(aux + 8);  // [2][QWARPS] pivot keys
+        rc2max = block_reduce_max(rc2max, red);  // (its barriers publish [Q; g] and the key slots)
+        MF_TS(2);
 
-        // ---- Gauss-Jordan column sweep of [Q; g] with node pivoting, register-resident:
-        //      thread (jj = tid % LL, rg = tid / LL) owns rows rg, rg + QG, ... of column jj
         bool ok = stat == 0;
-        const int qjj = tid % LL, qrg = tid / LL;
-        const bool qact = qrg < QG;
-        double gq[QI];
+        // the sweep's row registers stay live until G is written back after the join
+        double gq[C::QH];
+        const int qr = w * 16 + (lane >> 1), qh = lane & 1;  // row, column half (sweep warps)
+        if (w < C::QWARPS) {
+            // ---- Gauss-Jordan column sweep of [Q; g] with node pivoting, rows in lanes:
+            //      lane pair (2 r, 2 r + 1) of the first QWARPS warps owns row r, one
+            //      column half each.  Per step the pivot row (two threads) goes through
+            //      shared memory and every lane folds it into its own row: one broadcast
+            //      load and one FMA per element, the column-k factor from the partner
+            //      lane by one shuffle.  Pivot search: one 32-bit key per candidate row
+            //      (float bits of |v|, low 7 bits = 127 - row), warp REDUX into a per-warp
+            //      slot (double-buffered), every thread merges the QWARPS slots; column
+            //      k+1 is updated first so its keys and the reciprocals of the candidate
+            //      pivots leave early (the winner publishes its own: no reciprocal on
+            //      the step's chain).  Two barriers per step over the sweep warps only
+            //      (publishing every warp's candidate row to save one measured slower).
+            const bool qrow = qr < RG;
 #pragma unroll
-        for (int i = 0; i < QI; ++i) {
-            const int r = qrg + QG * i;
-            gq[i] = (qact && r < RG) ? G[r * GP + qjj] : 0.0;
-        }
-        // pivot search: one 32-bit key per candidate, the float bits of |v| with
-        // the low 7 bits replaced by 127 - row (largest |v| to 2^-16, then the
-        // lowest row), merged by a shared-memory atomicMax; column k+1's owners
-        // form their keys right after updating it in step k (three key slots).
-        // Pivot rows are a per-thread bit mask of the thread's rows.
-        unsigned* qkey = reinterpret_cast<unsigned*>(red + 40);
-        uint32_t ispm = 0;
-        auto key_of = [](double v, int r) -> unsigned {
-            const float f = __double2float_ru(fabs(v));
-            return (__float_as_uint(f) & ~127u) | (unsigned)(127 - r);
-        };
-        if (tid < 3) qkey[tid] = 0u;
-        __syncthreads();
-        if (ok && qact && qjj == 0) {
-            unsigned kb = 0;
+            for (int j = 0; j < C::QH; ++j) {
+                const int c = qh * C::QH + j;
+                gq[j] = (qrow && c < LL) ? G[qr * GP + c] : 0.0;
+            }
+            auto key_of = [](double v, int r) -> unsigned {
+                const float f = __double2float_ru(fabs(v));
+                return (__float_as_uint(f) & ~127u) | (unsigned)(127 - r);
+            };
+            bool isp_row = false;
+            double myinv = fast_rcp(gq[0]);
+            {
+                const unsigned kb = (ok && qh == 0 && qr < NN) ? key_of(gq[0], qr) : 0u;
+                const unsigned km = __reduce_max_sync(FULL, kb);
+                if (lane == 0) qkw[w] = km;
+            }
 #pragma unroll
-            for (int i = 0; i < QI; ++i) {
-                const int r = qrg + QG * i;
-                if (r < NN) kb = max(kb, key_of(gq[i], r));
+            for (int k = 0; k < LL; ++k) {
+                constexpr int QH = C::QH;
+                const int hk = k / QH, kk = k - hk * QH;
+                named_bar(1, C::QWARPS * 32);  // keys of column k complete
+                if (!ok) break;
+                unsigned key = qkw[(k & 1) * C::QWARPS];
+#pragma unroll
+                for (int q = 1; q < C::QWARPS; ++q) key = max(key, qkw[(k & 1) * C::QWARPS + q]);
+                const int pr = 127 - (int)(key & 127u);
+                const float best = __uint_as_float(key & ~127u);
+                if (key == 0u || !(best > 0.0f) || !isfinite(best) || pr >= NN) {
+                    ok = false;  // uniform: every thread read the same key
+                    break;
+                }
+                if (tid == 0) {
+                    isp[pr] = 1;
+                    piv[k] = pr;
+                }
+                if (qr == pr) {
+                    // the raw pivot row (kept for the lambda back substitution) and 1 / pivot
+#pragma unroll
+                    for (int j = 0; j < QH; ++j)
+                        if (qh == 0 || j < LL - QH) ops[k * GP + qh * QH + j] = gq[j];
+                    if (qh == hk) invs[k] = myinv;
+                    isp_row = true;
+                }
+                named_bar(1, C::QWARPS * 32);  // pivot row and 1 / pivot published
+                const double inv = invs[k];
+                const double tk = __shfl_sync(FULL, gq[kk], (lane & ~1) | hk);
+                const double s = tk * inv;
+                const double* prw = ops + k * GP + qh * QH;
+                if (k + 1 < LL) {
+                    // column k + 1 first: its pivot keys and reciprocals
+                    const int h1 = (k + 1) / QH, k1 = (k + 1) - h1 * QH;
+                    if (qh == h1) gq[k1] = fma(-s, prw[k1], gq[k1]);
+                    const unsigned kb = (qh == h1 && qr < NN && !isp_row) ? key_of(gq[k1], qr) : 0u;
+                    const unsigned km = __reduce_max_sync(FULL, kb);
+                    if (lane == 0) qkw[((k + 1) & 1) * C::QWARPS + w] = km;
+                    myinv = fast_rcp(gq[k1]);
+                }
+#pragma unroll
+                for (int j = 0; j < QH; ++j) {
+                    const int h1 = (k + 1) / QH, k1 = (k + 1) - h1 * QH;
+                    if (k + 1 < LL && j == k1) {
+                        if (qh != h1) gq[j] = fma(-s, prw[j], gq[j]);
+                    } else if (j == kk) {
+                        gq[j] = qh == hk ? s : fma(-s, prw[j], gq[j]);
+                    } else {
+                        gq[j] = fma(-s, prw[j], gq[j]);
+                    }
+                }
             }
-            if (kb) atomicMax(&qkey[0], kb);
-        }
-        __syncthreads();
-        for (int k = 0; k < LL && ok; ++k) {
-            double* pr_buf = prow + (k & 1) * 64;
-            double* ck_buf = colk + (k & 1) * 80;
-            const unsigned key = qkey[k % 3];
-            const int pr = 127 - (int)(key & 127u);
-            const float best = __uint_as_float(key & ~127u);
-            if (key == 0u || !(best > 0.0f) || !isfinite(best) || pr >= NN) {
-                ok = false;  // uniform: every thread read the same key
-                break;
-            }
-            if (tid == 0) qkey[(k + 2) % 3] = 0u;  // read in step k - 1, written in step k + 1
-            // stage the pivot row (its owners) and column k (unscaled)
-            if (qact) {
-                if (qrg == pr % QG) {
+            if (tid == 0) aux[6] = ok ? 1.0 : 0.0;
+        } else {
+            // ---- Phi (both triangles, zero diagonal) and ||A||_inf while the
+            //      sweep runs: rows i and NN-1-i pair up to NN+1 entries, split in two
+            const int pt = tid - C::QWARPS * 32;
+            constexpr int PT = (CTA_WARPS - C::QWARPS) * 32;
+            constexpr int UNIT = (NN + 1 + 1) / 2;
+            double r2min = INFINITY;
+            for (int u = pt; u < NN; u += PT) {  // NN/2 row pairs x 2 halves
+                const int pp = u >> 1, half = u & 1;
+                const int q0 = half * UNIT, q1 = half ? NN + 1 : UNIT;
+                for (int q = q0; q < q1; ++q) {
+                    const bool first = q < NN - pp;
+                    const int i = first ? pp : NN - 1 - pp;
+                    const int j = first ? pp + q : i + (q - (NN - pp));
                     double v = 0.0;
+                    if (j > i) {
+                        double df = loc[i * DD] - loc[j * DD];
+                        double r2 = df * df;
 #pragma unroll
-                    for (int i = 0; i < QI; ++i)
-                        if (qrg + QG * i == pr) v = gq[i];
-                    pr_buf[qjj] = v;
-                    ops[k * GP + qjj] = v;
-                    ispm |= 1u << (pr / QG);
-                }
-                if (qjj == k) {
-#pragma unroll
-                    for (int i = 0; i < QI; ++i) {
-                        const int r = qrg + QG * i;
-                        if (r < RG) ck_buf[r] = gq[i];
+                        for (int ax = 1; ax < DD; ++ax) {
+                            df = loc[i * DD + ax] - loc[j * DD + ax];
+                            r2 = fma(df, df, r2);
+                        }
+                        r2min = r2 < r2min ? r2 : r2min;
+                        v = r2 * (r2 * fast_rsqrt(fmax(r2, 1e-300)));
                     }
+                    E[i * EP + j] = v;
+                    E[j * EP + i] = v;
                 }
             }
-            if (tid == 0) {
-                isp[pr] = 1;
-                piv[k] = pr;
-            }
-            __syncthreads();
-            const double inv = fast_rcp(pr_buf[k]);
-            if (tid == 0) invs[k] = inv;
-            if (qact) {
-                if (qjj == k) {
-#pragma unroll
-                    for (int i = 0; i < QI; ++i) {
-                        const int r = qrg + QG * i;
-                        if (r < RG) gq[i] = ck_buf[r] * inv;
-                    }
+            named_bar(2, PT);
+            double an = 0.0;
+            for (int r = pt; r < NN + LL; r += PT) {
+                double acc = 0.0;
+                if (r < NN) {
+                    for (int j = 0; j < NN; ++j) acc += E[r * EP + j];  // r^3 >= 0
+                    for (int m = 0; m < LL; ++m) acc += fabs(G[r * GP + m]);
                 } else {
-                    const double pjs = pr_buf[qjj] * inv;
-#pragma unroll
-                    for (int i = 0; i < QI; ++i) {
-                        const int r = qrg + QG * i;
-                        if (r < RG) gq[i] = fma(-ck_buf[r], pjs, gq[i]);
-                    }
+                    for (int i = 0; i < NN; ++i) acc += fabs(G[i * GP + (r - NN)]);
                 }
-                if (qjj == k + 1) {
-                    unsigned kb = 0;
-#pragma unroll
-                    for (int i = 0; i < QI; ++i) {
-                        const int r = qrg + QG * i;
-                        if (r < NN && !((ispm >> i) & 1u)) kb = max(kb, key_of(gq[i], r));
-                    }
-                    if (kb) atomicMax(&qkey[(k + 1) % 3], kb);
-                }
+                an = fmax(an, acc);
             }
-            __syncthreads();
-        }
-        if (ok) {
 #pragma unroll
-            for (int i = 0; i < QI; ++i) {
-                const int r = qrg + QG * i;
-                if (qact && r < RG) G[r * GP + qjj] = gq[i];
+            for (int o = 16; o > 0; o >>= 1) {
+                an = fmax(an, __shfl_xor_sync(FULL, an, o));
+                r2min = fmin(r2min, __shfl_xor_sync(FULL, r2min, o));
+            }
+            if (lane == 0) {
+                aux[w - C::QWARPS] = r2min;
+                aux[3 + w - C::QWARPS] = an;
+            }
+        }
+        cta_cp_async_wait_all();  // the next stencil's indices
+        __syncthreads();  // join: sweep done, Phi and the estimates' inputs ready
+        stage_pos(idx + gridDim.x);
+        MF_TS(3);
+        ok = aux[6] != 0.0;
+        double r2min = aux[0], anorm = aux[3];
+#pragma unroll
+        for (int q = 1; q < CTA_WARPS - C::QWARPS; ++q) {
+            r2min = fmin(r2min, aux[q]);
+            anorm = fmax(anorm, aux[3 + q]);
+        }
+        if (ok && w < C::QWARPS && qr < RG) {
+#pragma unroll
+            for (int j = 0; j < C::QH; ++j) {
+                const int c = qh * C::QH + j;
+                if (c < LL) G[qr * GP + c] = gq[j];
             }
         }
         __syncthreads();
@@ -1006,141 +1089,193 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
 
         bool definite = true;
         if (ok) {
-            // ---- Y (l x [M | NR]) on the tensor cores: tiles over the warps
-            for (int tt = w; tt < C::RT * C::CT; tt += CTA_WARPS) {
-                const int lt = tt / C::CT, mt = tt - lt * C::CT;
-                const int kr = lt * 8 + g8;
-                const int pk = piv[kr < LL ? kr : 0];
-                double acc[2];
+            // ---- Y (l x [M | NR]) on the tensor cores, then [K | b]: 8 x 8 tiles spread
+            //      over the warps, each warp's tiles advanced together (k-step outer,
+            //      tiles inner: independent accumulator chains); the row and column
+            //      offsets of every fragment are resolved once per tile
+            MF_TS(4);
+            {
+                constexpr int NT = C::RT * C::CT, TPW = (NT + CTA_WARPS - 1) / CTA_WARPS;
+                double acc[TPW][2];
+                int arow[TPW], brow[TPW];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = mt * 8 + 2 * t4 + h;
-                    double v = 0.0;
-                    if (kr < LL && c < M) v = E[C::po(pk, nonpiv[c])];
-                    else if (kr < LL && c < MR) v = F[pk * NR + (c - M)];
-                    acc[h] = v;
+                for (int ti = 0; ti < TPW; ++ti) {
+                    const int tt = w + ti * CTA_WARPS;
+                    const int lt = tt < NT ? tt / C::CT : 0, mt = tt < NT ? tt - lt * C::CT : 0;
+                    const int kr = lt * 8 + g8;
+                    const int pk = piv[kr < LL ? kr : 0];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = mt * 8 + 2 * t4 + h;
+                        double v = 0.0;
+                        if (kr < LL && c < M) v = E[pk * EP + nonpiv[c]];
+                        else if (kr < LL && c < MR) v = F[pk * NR + (c - M)];
+                        acc[ti][h] = v;
+                    }
+                    const int cb = mt * 8 + g8;
+                    arow[ti] = kr < LL ? pk * EP : -1;
+                    brow[ti] = cb < M ? nonpiv[cb] * GP : (cb < MR ? (NN + cb - M) * GP : -1);
                 }
-                const int cb = mt * 8 + g8;
-                const int grow = cb < M ? nonpiv[cb] : (cb < MR ? NN + (cb - M) : 0);
 #pragma unroll
                 for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
                     const int k2 = ks * 4 + t4;
-                    const double av = (k2 < LL && kr < LL) ? -E[C::po(pk, piv[k2 < LL ? k2 : 0])] : 0.0;
-                    const double bv = (k2 < LL && cb < MR) ? G[grow * GP + k2] : 0.0;
-                    dmma_f64(acc[0], acc[1], av, bv);
+                    const bool kin = k2 < LL;
+                    const int pv = piv[kin ? k2 : 0];
+#pragma unroll
+                    for (int ti = 0; ti < TPW; ++ti) {
+                        if (w + ti * CTA_WARPS >= NT) continue;  // warp-uniform
+                        const double av = (kin && arow[ti] >= 0) ? -E[arow[ti] + pv] : 0.0;
+                        const double bv = (kin && brow[ti] >= 0) ? G[brow[ti] + k2] : 0.0;
+                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
+                    }
                 }
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = mt * 8 + 2 * t4 + h;
-                    if (kr < LL && c < MR) Y[c * YP + kr] = acc[h];
-                }
-            }
-            __syncthreads();
-            // ---- [K | b] on the tensor cores (accumulated in registers: the tiles land in
-            //      the Phi region once every warp has read Phi)
-            double kacc[C::TILES_PER_WARP][2];
+                for (int ti = 0; ti < TPW; ++ti) {
+                    const int tt = w + ti * CTA_WARPS;
+                    if (tt >= NT) continue;
+                    const int lt = tt / C::CT, mt = tt - lt * C::CT;
+                    const int kr = lt * 8 + g8;
 #pragma unroll
-            for (int ti = 0; ti < C::TILES_PER_WARP; ++ti) {
-                const int tt = w + ti * CTA_WARPS;
-                kacc[ti][0] = kacc[ti][1] = 0.0;
-                if (tt >= C::MT * C::CT) continue;
-                const int rt = tt / C::CT, ct = tt - rt * C::CT;
-                const int c = rt * 8 + g8;
-                const int qc = nonpiv[c < M ? c : 0];
-                double acc[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c2 = ct * 8 + 2 * t4 + h;
-                    double v = 0.0;
-                    if (c < M && c2 < M) v = E[C::po(qc, nonpiv[c2])];
-                    else if (c < M && c2 < MR) v = F[qc * NR + (c2 - M)];
-                    acc[h] = v;
-                }
-                const int cb = ct * 8 + g8;
-                const int grow = cb < M ? nonpiv[cb] : (cb < MR ? NN + (cb - M) : 0);
-#pragma unroll 6
-                for (int ks = 0; ks < (2 * LL + 3) / 4; ++ks) {
-                    const int kk = ks * 4 + t4;
-                    const bool hp = kk < LL, kv = kk < 2 * LL;
-                    const int kh = hp ? kk : 0, kw = hp ? 0 : (kv ? kk - LL : 0);
-                    double av = 0.0, bv = 0.0;
-                    if (c < M && kv) av = -(hp ? E[C::po(qc, piv[kh])] : G[qc * GP + kw]);
-                    if (cb < MR && kv) bv = hp ? G[grow * GP + kh] : Y[cb * YP + kw];
-                    dmma_f64(acc[0], acc[1], av, bv);
-                }
-                kacc[ti][0] = acc[0];
-                kacc[ti][1] = acc[1];
-            }
-            __syncthreads();  // Phi is consumed: [K | b] takes its place
-#pragma unroll
-            for (int ti = 0; ti < C::TILES_PER_WARP; ++ti) {
-                const int tt = w + ti * CTA_WARPS;
-                if (tt >= C::MT * C::CT) continue;
-                const int rt = tt / C::CT, ct = tt - rt * C::CT;
-                const int c = rt * 8 + g8;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c2 = ct * 8 + 2 * t4 + h;
-                    if (c < M && c2 < MR) K[c * KP + c2] = kacc[ti][h];
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = mt * 8 + 2 * t4 + h;
+                        if (kr < LL && c < MR) Y[c * YP + kr] = acc[ti][h];
+                    }
                 }
             }
             __syncthreads();
-            // ---- pivot-free Gauss-Jordan on [K | b], register-resident:
-            //      thread (jj = tid % MR, rg = tid / MR) owns rows rg, rg + KG, ...
-            const int kjj = tid % MR, krg = tid / MR;
-            const bool kact = krg < KG;
-            double kv[KI];
+            MF_TS(5);
+            // [K | b] = [Phi22 | f] - H [W^T | w1p] - W [Y | r_piv]
+            {
+                constexpr int NT = C::MT * C::CT, TPW = (NT + CTA_WARPS - 1) / CTA_WARPS;
+                double acc[TPW][2];
+                int arE[TPW], arG[TPW], brG[TPW], brY[TPW];
 #pragma unroll
-            for (int i = 0; i < KI; ++i) {
-                const int r = krg + KG * i;
-                kv[i] = (kact && r < M) ? K[r * KP + kjj] : 0.0;
-            }
-            const double d0 = K[0];
-            for (int k = 0; k < M; ++k) {
-                double* pr_buf = prow + (k & 1) * 64;
-                double* ck_buf = colk + (k & 1) * 80;
-                if (kact) {
-                    if (krg == k % KG) {
+                for (int ti = 0; ti < TPW; ++ti) {
+                    const int tt = w + ti * CTA_WARPS;
+                    const int rt = tt < NT ? tt / C::CT : 0, ct = tt < NT ? tt - rt * C::CT : 0;
+                    const int c = rt * 8 + g8;
+                    const int qc = nonpiv[c < M ? c : 0];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c2 = ct * 8 + 2 * t4 + h;
                         double v = 0.0;
-#pragma unroll
-                        for (int i = 0; i < KI; ++i)
-                            if (krg + KG * i == k) v = kv[i];
-                        pr_buf[kjj] = v;
+                        if (c < M && c2 < M) v = E[qc * EP + nonpiv[c2]];
+                        else if (c < M && c2 < MR) v = F[qc * NR + (c2 - M)];
+                        acc[ti][h] = v;
                     }
-                    if (kjj == k) {
+                    const int cb = ct * 8 + g8;
+                    arE[ti] = c < M ? qc * EP : -1;
+                    arG[ti] = c < M ? qc * GP : -1;
+                    brG[ti] = cb < M ? nonpiv[cb] * GP : (cb < MR ? (NN + cb - M) * GP : -1);
+                    brY[ti] = cb < MR ? cb * YP : -1;
+                }
 #pragma unroll
-                        for (int i = 0; i < KI; ++i) {
-                            const int r = krg + KG * i;
-                            if (r < M) ck_buf[r] = kv[i];
-                        }
+                for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
+                    const int kk = ks * 4 + t4;
+                    const bool kin = kk < LL;
+                    const int pv = piv[kin ? kk : 0];
+#pragma unroll
+                    for (int ti = 0; ti < TPW; ++ti) {
+                        if (w + ti * CTA_WARPS >= NT) continue;
+                        const double av = (kin && arE[ti] >= 0) ? -E[arE[ti] + pv] : 0.0;
+                        const double bv = (kin && brG[ti] >= 0) ? G[brG[ti] + kk] : 0.0;
+                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
                     }
                 }
-                __syncthreads();
-                const double dk = pr_buf[k];
-                definite = definite && dk * d0 > 0.0;
-                const double inv = fast_rcp(dk);
-                if (kact && kjj > k) {
-                    const double pjs = pr_buf[kjj] * inv;
 #pragma unroll
-                    for (int i = 0; i < KI; ++i) {
-                        const int r = krg + KG * i;
-                        if (r < M) kv[i] = r == k ? pjs : fma(-ck_buf[r], pjs, kv[i]);
+                for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
+                    const int kw = ks * 4 + t4;
+                    const bool kin = kw < LL;
+#pragma unroll
+                    for (int ti = 0; ti < TPW; ++ti) {
+                        if (w + ti * CTA_WARPS >= NT) continue;
+                        const double av = (kin && arG[ti] >= 0) ? -G[arG[ti] + kw] : 0.0;
+                        const double bv = (kin && brY[ti] >= 0) ? Y[brY[ti] + kw] : 0.0;
+                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
                     }
                 }
-            }
-            // the solution columns
-            if (kact && kjj >= M) {
+                __syncthreads();  // Phi is consumed: [K | b] takes its place
 #pragma unroll
-                for (int i = 0; i < KI; ++i) {
-                    const int r = krg + KG * i;
-                    if (r < M) V[r * NR + (kjj - M)] = kv[i];
+                for (int ti = 0; ti < TPW; ++ti) {
+                    const int tt = w + ti * CTA_WARPS;
+                    if (tt >= NT) continue;
+                    const int rt = tt / C::CT, ct = tt - rt * C::CT;
+                    const int c = rt * 8 + g8;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c2 = ct * 8 + 2 * t4 + h;
+                        if (c < M && c2 < MR) K[c * KP + c2] = acc[ti][h];
+                    }
                 }
             }
             __syncthreads();
+            // ---- pivot-free Gauss-Jordan on [K | b], rows in lanes: lane pair (2 c,
+            //      2 c + 1) of the first KWARPS warps owns row c, columns interleaved
+            //      (col = 2 j + half).  Rows M .. M+NR-1 carry b^T, so column k of the
+            //      symmetric [K b; b^T .] -- stored by its owners in one instruction --
+            //      is the whole pivot row including b(k, :); the pivot stores 1 / d_k in
+            //      the diagonal slot.  One barrier per step (every step has its own
+            //      row slot in the free Phi region) over the elimination warps only.
+            if (w < C::KWARPS) {
+                constexpr int KH = C::KH;
+                const int kc = w * 16 + (lane >> 1), kh = lane & 1;
+                double kv[KH];
+#pragma unroll
+                for (int j = 0; j < KH; ++j) {
+                    const int col = 2 * j + kh;
+                    double v = 0.0;
+                    if (kc < M && col < MR) v = K[kc * KP + col];
+                    else if (kc < MR && col < M) v = K[col * KP + kc];  // b^T rows
+                    kv[j] = v;
+                }
+                named_bar(1, C::KWARPS * 32);  // [K | b] read: the slots may overwrite it
+                MF_TS(6);
+                double* U = K;  // step k's pivot row at k * UPK
+                double rnext = fast_rcp(kv[0]);  // (lane pair of row 0 holds column 0 in half 0)
+                bool def = true;
+                double d0inv = 0.0;
+#pragma unroll
+                for (int k = 0; k < M; ++k) {
+                    const int hk = k & 1, jk = k >> 1;
+                    if (kh == hk && kc < MR) U[k * C::UPK + kc] = kc == k ? rnext : kv[jk];
+                    named_bar(1, C::KWARPS * 32);
+                    const double rk = U[k * C::UPK + k];
+                    if (k == 0) d0inv = rk;
+                    def = def && rk * d0inv > 0.0;
+                    const double tk = __shfl_sync(FULL, kv[jk], (lane & ~1) | hk);
+                    const double fac = kc != k ? tk * rk : 0.0;
+                    // the next pivot's reciprocal as soon as its entry is final
+                    if (k + 1 < M) {
+                        const int h1 = (k + 1) & 1, j1 = (k + 1) >> 1;
+                        if (kh == h1) kv[j1] = fma(-fac, U[k * C::UPK + k + 1], kv[j1]);
+                        rnext = fast_rcp(kv[j1]);
+                    }
+#pragma unroll
+                    for (int j = k >> 1; j < KH; ++j) {
+                        const int h1 = (k + 1) & 1, j1 = (k + 1) >> 1;
+                        const int col = 2 * j + kh;
+                        if (col > k && !(j == j1 && kh == h1 && k + 1 < M) && col < MR)
+                            kv[j] = fma(-fac, U[k * C::UPK + col], kv[j]);
+                    }
+                }
+                // the solution columns: v_c = b_c / d_c
+                if (kc < M) {
+                    const double dinv = U[kc * C::UPK + kc];
+#pragma unroll
+                    for (int j = 0; j < KH; ++j) {
+                        const int col = 2 * j + kh;
+                        if (col >= M && col < MR) V[kc * NR + (col - M)] = kv[j] * dinv;
+                    }
+                }
+                if (tid == 0) aux[7] = def ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            definite = aux[7] != 0.0;
         }
         ok = ok && definite;
 
         // ---- outputs: free weights v, pivot weights w1p - W^T v; estimate
+        MF_TS(7);
         bool bad = !ok;
         double zw = 0.0, xw[NF], la[NF];
 #pragma unroll
@@ -1157,55 +1292,90 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                     zw = fmax(zw, fabs(v));
                 }
             }
-            for (int e = tid; e < LL * NR; e += CTA_THREADS) {
-                const int k = e / NR, f = e - k * NR;
-                double wv = G[(NN + f) * GP + k];
-                for (int c = 0; c < M; ++c) wv = fma(-G[nonpiv[c] * GP + k], V[c * NR + f], wv);
-                if (f < NF) {
-                    bad |= !isfinite(wv);
-                    a.out[((size_t)idx * NF + f) * NN + piv[k]] = wv;
-                    xw[f] = fmax(xw[f], fabs(wv));
-                } else {
-                    zw = fmax(zw, fabs(wv));
+            // pivot weights w1p - W^T v (rows k < LL) and the multipliers' right-hand
+            // side r_piv - Y v (rows LL + k) as one tensor-core product over the free
+            // columns c: A(r, c) = W(c, r) | Y(c, r - LL), B(c, f) = v(c, f)
+            {
+                constexpr int R2 = (2 * LL + 7) / 8, TPW = (R2 + CTA_WARPS - 1) / CTA_WARPS;
+                double acc[TPW][2];
+#pragma unroll
+                for (int ti = 0; ti < TPW; ++ti) acc[ti][0] = acc[ti][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < (M + 3) / 4; ++ks) {
+                    const int c = ks * 4 + t4;
+                    const bool cin = c < M;
+                    const int cr = cin ? c : 0;
+                    const int wrow = nonpiv[cr] * GP;
+                    const double bv = (cin && g8 < NR) ? V[cr * NR + (g8 < NR ? g8 : 0)] : 0.0;
+#pragma unroll
+                    for (int ti = 0; ti < TPW; ++ti) {
+                        const int rt = w + ti * CTA_WARPS;
+                        if (rt >= R2) continue;  // warp-uniform
+                        const int r = rt * 8 + g8;
+                        double av = 0.0;
+                        if (cin && r < 2 * LL) av = r < LL ? G[wrow + r] : Y[cr * YP + (r - LL)];
+                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
+                    }
+                }
+#pragma unroll
+                for (int ti = 0; ti < TPW; ++ti) {
+                    const int rt = w + ti * CTA_WARPS;
+                    if (rt >= R2) continue;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = rt * 8 + g8, f = 2 * t4 + h;
+                        if (r < LL && f < NR) {
+                            const double wv = G[(NN + f) * GP + r] - acc[ti][h];
+                            if (f < NF) {
+                                bad |= !isfinite(wv);
+                                a.out[((size_t)idx * NF + f) * NN + piv[r]] = wv;
+#pragma unroll
+                                for (int ff = 0; ff < NF; ++ff)
+                                    if (ff == f) xw[ff] = fmax(xw[ff], fabs(wv));
+                            } else {
+                                zw = fmax(zw, fabs(wv));
+                            }
+                        } else if (r >= LL && r < 2 * LL && f < NF) {
+                            colk[(r - LL) * NF + f] = Y[(M + f) * YP + (r - LL)] - acc[ti][h];
+                        }
+                    }
                 }
             }
+            MF_TS(9);
             // lambda_f = Q1^-1 (r_piv - Y v): the recorded column operations, last
             // first.  Step k needs the finished x_j (j > k) and the untouched s_j
             // (j < k): the j < k part is one parallel product up front, the rest a
             // column-oriented back substitution (x_k broadcast by one shuffle, the
             // lanes j < k fold it in) -- a 35-step chain of shuffle + FMA instead
             // of a warp reduction per step.  Only the estimate uses lambda.
-            for (int e = tid; e < LL * NF; e += CTA_THREADS) {
-                const int k = e / NF, f = e - k * NF;
-                double sv = Y[(M + f) * YP + k];
-                for (int c = 0; c < M; ++c) sv = fma(-Y[c * YP + k], V[c * NR + f], sv);
-                colk[k * NF + f] = sv;
-            }
             __syncthreads();
+            MF_TS(10);
             constexpr int LS = (LL + 31) / 32;
             for (int f = w; f < NF; f += CTA_WARPS) {
                 double acc[LS];
 #pragma unroll
                 for (int q = 0; q < LS; ++q) {
                     const int jr = lane + 32 * q;
-                    double a = 0.0;
-                    if (jr < LL) {
-                        a = colk[jr * NF + f];
-                        for (int i2 = 0; i2 < jr; ++i2) a = fma(-ops[jr * GP + i2], colk[i2 * NF + f], a);
+                    const int jc = jr < LL ? jr : 0;
+                    // two interleaved partial sums halve the FMA chain
+                    double a0 = jr < LL ? colk[jc * NF + f] : 0.0, a1 = 0.0;
+#pragma unroll
+                    for (int i2 = 0; i2 < LL - 1; ++i2) {
+                        if (i2 < 32 * q + 31 && i2 < jr) {
+                            if (i2 & 1) a1 = fma(-ops[jc * GP + i2], colk[i2 * NF + f], a1);
+                            else a0 = fma(-ops[jc * GP + i2], colk[i2 * NF + f], a0);
+                        }
                     }
-                    acc[q] = a;
+                    acc[q] = a0 + a1;
                 }
                 double mx = 0.0;
-                for (int k = LL - 1; k >= 0; --k) {
-                    const int owner = k & 31, qk = k >> 5;
-                    double xk = 0.0;
 #pragma unroll
-                    for (int q = 0; q < LS; ++q)
-                        if (q == qk) xk = acc[q];
-                    xk = __shfl_sync(FULL, invs[k] * xk, owner);
+                for (int k = LL - 1; k >= 0; --k) {
+                    const double xk = __shfl_sync(FULL, acc[k >> 5], k & 31) * invs[k];
                     mx = fmax(mx, fabs(xk));
 #pragma unroll
                     for (int q = 0; q < LS; ++q) {
+                        if (32 * q >= k) continue;
                         const int jr = lane + 32 * q;
                         if (jr < k) acc[q] = fma(-ops[jr * GP + k], xk, acc[q]);
                     }
@@ -1213,6 +1383,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                 la[f] = mx;  // uniform over the warp
             }
         }
+        MF_TS(11);
         // one fused reduction of the failure flag and the 1 + 2 NF maxima (all
         // >= 0); only thread 0 consumes them
         {
@@ -1225,23 +1396,30 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                 rv[2 + f] = xw[f];
                 rv[2 + NF + f] = la[f];
             }
+            // warp maxima by two REDUX on the IEEE bits (non-negative doubles order
+            // like their bit patterns), then lane v of warp 0 merges value v
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) rv[v] = fmax(rv[v], __shfl_xor_sync(FULL, rv[v], o));
+                const unsigned long long b = (unsigned long long)__double_as_longlong(rv[v]);
+                const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+                const unsigned mh = __reduce_max_sync(FULL, hi);
+                const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+                rv[v] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
             }
             if (lane == 0) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) prow[v * CTA_WARPS + w] = rv[v];
             }
             __syncthreads();
-            if (tid == 0) {
+            if (w == 0) {
+                double m = 0.0;
+                if (lane < NV) {
+                    m = prow[lane * CTA_WARPS];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    double m = prow[v * CTA_WARPS];
-                    for (int q = 1; q < CTA_WARPS; ++q) m = fmax(m, prow[v * CTA_WARPS + q]);
-                    rv[v] = m;
+                    for (int q = 1; q < CTA_WARPS; ++q) m = fmax(m, prow[lane * CTA_WARPS + q]);
                 }
+#pragma unroll
+                for (int v = 0; v < NV; ++v) rv[v] = __shfl_sync(FULL, m, v);
                 bad = rv[0] != 0.0;
                 zw = rv[1];
             }
@@ -1260,9 +1438,17 @@ __global__ void __launch_bounds__(CTA_THREADS, 3) phs_ns_cta2(PhsArgs a) {
                 a.flag_list[slot] = idx;
             }
             a.status[idx] = 0;  // failures are re-derived in reference order by the re-solve
+            MF_TS(8);
+#ifdef MF_CTA_TIMING
+            if (blockIdx.x == 0 && idx < 4 * (int64_t)gridDim.x)
+                printf("cta2 %lld: coords %lld qg %lld sweep %lld joinY %lld Y %lld Kprod %lld elim %lld out %lld [dmma %lld bar %lld lam %lld red %lld]\n", (long long)idx,
+                       ts_[1] - ts_[0], ts_[2] - ts_[1], ts_[3] - ts_[2], ts_[4] - ts_[3], ts_[5] - ts_[4], ts_[6] - ts_[5], ts_[7] - ts_[6], ts_[8] - ts_[7],
+                       ts_[9] - ts_[7], ts_[10] - ts_[9], ts_[11] - ts_[10], ts_[8] - ts_[11]);
+#endif
         }
         __syncthreads();
     }
+    cta_cp_async_wait_all();
 }
 
 template <int NN, int DD, int DEG, int NF>
