@@ -752,7 +752,7 @@ struct Cta2Cfg {
     static constexpr int QWARPS = (RG + 15) / 16;        // warps of the [Q; g] sweep
     static constexpr int KH = (MR + 1) / 2;              // [K | b] columns per lane (interleaved)
     static constexpr int KWARPS = (MR + 15) / 16;        // warps of the [K | b] elimination
-    static constexpr int UPK = MR;                       // pivot-row slot pitch
+    static constexpr int UPB = 2 * MR + 2;               // block slot: column pairs, 1 / det
     static constexpr int RT = (LL + 7) / 8, CT = (MR + 7) / 8, MT = (M + 7) / 8;
     // shared layout (doubles)
     static constexpr int LOC = 0;
@@ -779,7 +779,7 @@ struct Cta2Cfg {
     static_assert(NN * DD + DD <= CTA_THREADS, "one staged position per thread");
     static_assert(QWARPS < CTA_WARPS && CTA_WARPS - QWARPS <= 3 && KWARPS <= CTA_WARPS, "sweep layouts");
     static_assert(NN % 2 == 0 && NN < 128, "Phi row pairing / pivot keys");
-    static_assert(M * UPK <= EFULL, "pivot-row slots fit the Phi region");
+    static_assert((M / 2 + 1) * UPB <= EFULL && UPB % 2 == 0, "block slots fit the Phi region");
     static_assert(MR <= 64 && RG <= 80 && M <= 80, "pivot buffers");
     static_assert(M * KP <= EFULL, "[K | b] fits the Phi region");
 };
@@ -1209,15 +1209,18 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 }
             }
             __syncthreads();
-            // ---- pivot-free Gauss-Jordan on [K | b], rows in lanes: lane pair (2 c,
-            //      2 c + 1) of the first KWARPS warps owns row c, columns interleaved
-            //      (col = 2 j + half).  Rows M .. M+NR-1 carry b^T, so column k of the
-            //      symmetric [K b; b^T .] -- stored by its owners in one instruction --
-            //      is the whole pivot row including b(k, :); the pivot stores 1 / d_k in
-            //      the diagonal slot.  One barrier per step (every step has its own
-            //      row slot in the free Phi region) over the elimination warps only.
+            // ---- pivot-free block Gauss-Jordan on [K | b] with 2 x 2 pivots, rows in
+            //      lanes: lane pair (2 c, 2 c + 1) of the first KWARPS warps owns row c,
+            //      columns interleaved (col = 2 j + half), so both columns of block p sit
+            //      at register j = p of the pair.  Rows M .. M+NR-1 carry b^T: the two
+            //      block columns of the symmetric [K b; b^T .] -- stored by every lane in
+            //      ONE instruction, pairs adjacent -- are the two pivot rows including
+            //      b; each row reads a pivot-row pair with one 16-byte load.  The block's
+            //      lane quad forms 1 / det of the next block as soon as its entries are
+            //      final (off the chain).  One barrier per TWO columns (each block has
+            //      its own slot in the free Phi region) over the elimination warps.
             if (w < C::KWARPS) {
-                constexpr int KH = C::KH;
+                constexpr int KH = C::KH, NB = M / 2, UB = C::UPB;
                 const int kc = w * 16 + (lane >> 1), kh = lane & 1;
                 double kv[KH];
 #pragma unroll
@@ -1230,41 +1233,90 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 }
                 named_bar(1, C::KWARPS * 32);  // [K | b] read: the slots may overwrite it
                 MF_TS(6);
-                double* U = K;  // step k's pivot row at k * UPK
-                double rnext = fast_rcp(kv[0]);  // (lane pair of row 0 holds column 0 in half 0)
+                double* U = K;  // block p's two columns at p * UB (pairs), 1 / det at p * UB + 2 MR
+                // 1 / det of the 2 x 2 block whose entries sit at register j in this quad
+                auto quad_rdet = [&](int j) {
+                    const int base = lane & ~3;
+                    const double d00 = __shfl_sync(FULL, kv[j], base), d01 = __shfl_sync(FULL, kv[j], base + 1);
+                    const double d10 = __shfl_sync(FULL, kv[j], base + 2), d11 = __shfl_sync(FULL, kv[j], base + 3);
+                    return fast_rcp(fma(d00, d11, -d01 * d10));
+                };
+                double rdet = NB > 0 ? quad_rdet(0) : 0.0;
                 bool def = true;
-                double d0inv = 0.0;
+                double s0 = 0.0;
 #pragma unroll
-                for (int k = 0; k < M; ++k) {
-                    const int hk = k & 1, jk = k >> 1;
-                    if (kh == hk && kc < MR) U[k * C::UPK + kc] = kc == k ? rnext : kv[jk];
+                for (int p = 0; p < NB; ++p) {
+                    const int k0 = 2 * p, k1 = 2 * p + 1;
+                    double* Up = U + p * UB;
+                    const double own = kv[p], oth = __shfl_xor_sync(FULL, kv[p], 1);
+                    if (kc < MR) Up[2 * kc + kh] = own;
+                    if (kc == k0 && kh == 0) Up[2 * MR] = rdet;
                     named_bar(1, C::KWARPS * 32);
-                    const double rk = U[k * C::UPK + k];
-                    if (k == 0) d0inv = rk;
-                    def = def && rk * d0inv > 0.0;
-                    const double tk = __shfl_sync(FULL, kv[jk], (lane & ~1) | hk);
-                    const double fac = kc != k ? tk * rk : 0.0;
-                    // the next pivot's reciprocal as soon as its entry is final
-                    if (k + 1 < M) {
-                        const int h1 = (k + 1) & 1, j1 = (k + 1) >> 1;
-                        if (kh == h1) kv[j1] = fma(-fac, U[k * C::UPK + k + 1], kv[j1]);
-                        rnext = fast_rcp(kv[j1]);
+                    const double2 r0 = *reinterpret_cast<const double2*>(Up + 2 * k0);  // D00 D01
+                    const double2 r1 = *reinterpret_cast<const double2*>(Up + 2 * k1);  // D10 D11
+                    const double rd = Up[2 * MR];
+                    if (p == 0) s0 = r0.x;
+                    def = def && r0.x * s0 > 0.0 && rd > 0.0;
+                    const double t0 = kh == 0 ? own : oth, t1 = kh == 0 ? oth : own;  // K(c, k0), K(c, k1)
+                    const bool piv_row = kc == k0 || kc == k1;
+                    const double fa = piv_row ? 0.0 : rd * fma(t0, r1.y, -t1 * r1.x);
+                    const double fb = piv_row ? 0.0 : rd * fma(t1, r0.x, -t0 * r0.y);
+                    // the next block's columns first, then its 1 / det
+                    if (p + 1 < KH) {
+                        const int col = 2 * (p + 1) + kh;
+                        if (col < MR) {
+                            const double2 u = *reinterpret_cast<const double2*>(Up + 2 * col);
+                            kv[p + 1] = fma(-fa, u.x, fma(-fb, u.y, kv[p + 1]));
+                        }
+                        if (p + 1 < NB) rdet = quad_rdet(p + 1);
                     }
 #pragma unroll
-                    for (int j = k >> 1; j < KH; ++j) {
-                        const int h1 = (k + 1) & 1, j1 = (k + 1) >> 1;
+                    for (int j = p + 2; j < KH; ++j) {
                         const int col = 2 * j + kh;
-                        if (col > k && !(j == j1 && kh == h1 && k + 1 < M) && col < MR)
-                            kv[j] = fma(-fac, U[k * C::UPK + col], kv[j]);
+                        if (col < MR) {
+                            const double2 u = *reinterpret_cast<const double2*>(Up + 2 * col);
+                            kv[j] = fma(-fa, u.x, fma(-fb, u.y, kv[j]));
+                        }
                     }
                 }
-                // the solution columns: v_c = b_c / d_c
-                if (kc < M) {
-                    const double dinv = U[kc * C::UPK + kc];
+                double rlast = 0.0;
+                if constexpr (M % 2 == 1) {
+                    // the last column alone: 1 / d from its owner, one more barrier
+                    constexpr int kl = M - 1, jl = kl / 2;
+                    double* Ul = U + NB * UB;
+                    const double rn = fast_rcp(kv[jl]);
+                    if (kc < MR && kh == 0) Ul[kc] = kc == kl ? rn : kv[jl];
+                    named_bar(1, C::KWARPS * 32);
+                    rlast = Ul[kl];
+                    def = def && (NB == 0 || rlast * s0 > 0.0);
+                    const double tk = __shfl_sync(FULL, kv[jl], lane & ~1);
+                    const double fac = kc != kl ? tk * rlast : 0.0;
 #pragma unroll
-                    for (int j = 0; j < KH; ++j) {
+                    for (int j = jl; j < KH; ++j) {
                         const int col = 2 * j + kh;
-                        if (col >= M && col < MR) V[kc * NR + (col - M)] = kv[j] * dinv;
+                        if (col > kl && col < MR) kv[j] = fma(-fac, Ul[col], kv[j]);
+                    }
+                }
+                // the solution columns: 2 x 2 block solves (the partner row sits two
+                // lanes away), the odd last row by its reciprocal
+#pragma unroll
+                for (int j = 0; j < KH; ++j) {
+                    const int col = 2 * j + kh;
+                    if (2 * j + 1 < M) continue;  // (compile-time: only the b columns)
+                    const double ob = __shfl_xor_sync(FULL, kv[j], 2);
+                    if (kc < M && col >= M && col < MR) {
+                        double x;
+                        if (kc < 2 * NB) {
+                            const int p = kc >> 1;
+                            const double* Up = U + p * UB;
+                            const double2 r0 = *reinterpret_cast<const double2*>(Up + 4 * p);
+                            const double2 r1 = *reinterpret_cast<const double2*>(Up + 4 * p + 2);
+                            const double rd = Up[2 * MR];
+                            x = (kc & 1) == 0 ? rd * fma(r1.y, kv[j], -r0.y * ob) : rd * fma(r0.x, kv[j], -r1.x * ob);
+                        } else {
+                            x = kv[j] * rlast;
+                        }
+                        V[kc * NR + (col - M)] = x;
                     }
                 }
                 if (tid == 0) aux[7] = def ? 1.0 : 0.0;
