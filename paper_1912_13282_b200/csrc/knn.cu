@@ -553,7 +553,7 @@ template <int DD, int SLOTS, bool TPOS>
 __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ? 6 : 2))
     knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
              int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count,
-             const double* __restrict__ tpos, int win_max) {
+             const double* __restrict__ tpos, const uint32_t* __restrict__ tinfo, int win_max) {
     extern __shared__ __align__(16) unsigned char kf_smem[];
     const int lane = threadIdx.x & 31;
     FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
@@ -569,8 +569,9 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
     const double cdim = d == 2 ? 3.141592653589793 : 4.1887902047863905;
     double tguess = pow(((double)K + 0.5 * win) * cellvol / (KNN_OCC * cdim), 2.0 / d);
 
-    // tpos (first pass): target positions gathered in processing order, so the
-    // next target's position is one coalesced load issued a target ahead
+    // tpos / tinfo (first pass): target positions and (node | in-pool << 31)
+    // gathered in processing order, so the next target's data are independent
+    // coalesced loads issued a target ahead (not a chain order -> targets -> in_pool)
     const int64_t wstride = (int64_t)gridDim.x * KF_WARPS;
     int64_t w = (int64_t)blockIdx.x * KF_WARPS + (threadIdx.x >> 5);
     double pn[3] = {0.0, 0.0, 0.0};
@@ -581,8 +582,9 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
         if (ww < count) {
             trn = order[ww];
             if constexpr (TPOS) {
-                tnn = a.targets[trn];
-                inp = a.in_pool[tnn] != 0;
+                const uint32_t ti = tinfo[ww];
+                tnn = (int64_t)(ti & 0x7fffffffu);
+                inp = (ti >> 31) != 0u;
 #pragma unroll
                 for (int ax = 0; ax < d; ++ax) pn[ax] = tpos[ww * d + ax];
             }
@@ -870,10 +872,12 @@ __global__ void knn_target_keys(const double* __restrict__ pos, int d, const int
 }
 
 __global__ void knn_target_gather(const double* __restrict__ pos, int d, const int64_t* __restrict__ targets,
-                                  const int32_t* __restrict__ order, int64_t T, double* __restrict__ tpos) {
+                                  const int32_t* __restrict__ order, const uint8_t* __restrict__ in_pool, int64_t T,
+                                  double* __restrict__ tpos, uint32_t* __restrict__ tinfo) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < T; w += (int64_t)gridDim.x * blockDim.x) {
         const int64_t node = targets[order[w]];
         for (int a = 0; a < d; ++a) tpos[w * d + a] = pos[node * d + a];
+        tinfo[w] = (uint32_t)node | (in_pool[node] ? 0x80000000u : 0u);  // (N < 2^31, checked by mf_knn)
     }
 }
 inline int grid_for(int64_t work, int threads, int per_sm = 8) { return grid_cap(work, threads, per_sm); }
@@ -1027,13 +1031,15 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
         const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
         MF_CUDA_CHECK(ensure_smem(f1, sm1));
         MF_CUDA_CHECK(ensure_smem(f2, sm2));
-        knn_target_gather<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, order, T, L.tpos);
+        // (the sort's spare key buffer is free now: it takes the packed target info)
+        uint32_t* tinfo = reinterpret_cast<uint32_t*>(kb.Alternate());
+        knn_target_gather<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, order, L.in_pool, T, L.tpos, tinfo);
         MF_LAUNCH_CHECK();
         f1<<<grid_for(T, KF_WARPS, 64), KF_WARPS * 32, sm1, st>>>(a, order, T, nullptr, K, rho1, L.fb_list[0],
-                                                                  L.fb_count, L.tpos, kf_win);
+                                                                  L.fb_count, L.tpos, tinfo, kf_win);
         MF_LAUNCH_CHECK();
         f2<<<grid_for(T, KF_WARPS, 4), KF_WARPS * 32, sm2, st>>>(a, L.fb_list[0], T, L.fb_count, K, rho2,
-                                                                 L.fb_list[1], L.fb_count + 1, nullptr, 16);
+                                                                 L.fb_list[1], L.fb_count + 1, nullptr, nullptr, 16);
         MF_LAUNCH_CHECK();
         main_k<<<grid_for(T, KNN_WARPS, 4), KNN_WARPS * 32, smem_bytes, st>>>(a, L.fb_list[1], T, L.fb_count + 1, K);
         MF_LAUNCH_CHECK();
