@@ -28,7 +28,7 @@
 
 namespace mf {
 
-constexpr double KNN_OCC = 2.0;   // mean pool points per grid cell
+constexpr double KNN_OCC = 2.0;   // mean pool points per grid cell (wide stencils take a coarser grid: GridParams::occ)
 constexpr int KNN_WARPS = 4;      // warps per block
 constexpr int KNN_SCAP = 256;     // survivor capacity per warp (shared memory)
 constexpr int KNN_RMAX = 255;     // cell-row ranges per cube held in shared memory
@@ -36,6 +36,7 @@ constexpr int KNN_WIN = 16;       // kernel-variant choice: K + WIN > 64 takes 3
 
 struct GridParams {
     double lo[3], cw[3], inv[3];
+    double occ;  // mean pool points per cell the grid was sized for (>= KNN_OCC)
     int G[3];
     int ncell;
 };
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
     // first cube: half-width ~ the K-th neighbour radius at the grid density
     // (in cells), so the inner-radius proof usually succeeds on the first pass
     const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
-    int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
+    int rho0 = (int)floor(pow((double)K / (g.occ * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
     // bisection stops at <= K + win survivors: as wide as keeps the rank pass
     // within one 64-survivor round (fewer bisection counts), 8..24; windows that
@@ -536,38 +537,38 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, 3) knn_kernel(KnnArgs a, const
 // to a list that the general kernel re-solves from scratch.  Results are the
 // same object either way: the K smallest (d2, node, candidate) keys.
 constexpr int KF_WARPS = 4;
-constexpr int KF_SCAP = 64;  // survivors ranked by the fast path
+constexpr int KF_SCAP = 64;  // survivors ranked by the fast path (K <= 56); wide stencils (K <= 112) rank 128
 
-template <int SLOTS>
+template <int SLOTS, int SCAP>
 struct FastSmem {
     int32_t cq[32 * SLOTS];  // sorted-pool position of each candidate
-    KnnKey skey[KF_SCAP];
-    uint32_t sk32[KF_SCAP + 4];  // high words of the survivor d2 (monotone in d2), padded to 4
-    int32_t srank[KF_SCAP];
-    int32_t slot[KF_SCAP];
-    int32_t sel[KF_SCAP];
-    double seld2[KF_SCAP];
+    KnnKey skey[SCAP];
+    uint32_t sk32[SCAP + 4];  // high words of the survivor d2 (monotone in d2), padded to 4
+    int32_t srank[SCAP];
+    int32_t slot[SCAP];
+    int32_t sel[SCAP];
+    double seld2[SCAP];
 };
 
-template <int DD, int SLOTS, bool TPOS>
-__global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ? 6 : 2))
+template <int DD, int SLOTS, bool TPOS, int SCAP = KF_SCAP>
+__global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ? 6 : (SLOTS <= 16 ? 4 : 2)))
     knn_fast(KnnArgs a, const int32_t* __restrict__ order, int64_t count, const unsigned long long* count_dev, int K,
              int rho, int32_t* __restrict__ fb_list, unsigned long long* __restrict__ fb_count,
              const double* __restrict__ tpos, const uint32_t* __restrict__ tinfo, int win_max) {
     extern __shared__ __align__(16) unsigned char kf_smem[];
     const int lane = threadIdx.x & 31;
-    FastSmem<SLOTS>& sm = reinterpret_cast<FastSmem<SLOTS>*>(kf_smem)[threadIdx.x >> 5];
+    FastSmem<SLOTS, SCAP>& sm = reinterpret_cast<FastSmem<SLOTS, SCAP>*>(kf_smem)[threadIdx.x >> 5];
     const GridParams g = *a.gp;
     constexpr int d = DD;
     const int n = a.n;
-    const int win = min(KF_SCAP - K, win_max);
+    const int win = min(SCAP - K, win_max);
     if (count_dev) count = (int64_t)*count_dev;
     // first threshold: the d2 of the (K + win/2)-th neighbour at the nominal grid
     // density (KNN_OCC points per cell); afterwards the previous target's
     double cellvol = 1.0;
     for (int ax = 0; ax < d; ++ax) cellvol *= g.cw[ax];
     const double cdim = d == 2 ? 3.141592653589793 : 4.1887902047863905;
-    double tguess = pow(((double)K + 0.5 * win) * cellvol / (KNN_OCC * cdim), 2.0 / d);
+    double tguess = pow(((double)K + 0.5 * win) * cellvol / (g.occ * cdim), 2.0 / d);
 
     // tpos / tinfo (first pass): target positions and (node | in-pool << 31)
     // gathered in processing order, so the next target's data are independent
@@ -707,20 +708,29 @@ __global__ void __launch_bounds__(KF_WARPS * 32, SLOTS <= 5 ? 8 : (SLOTS <= 10 ?
             // below 2^31 and [v < d] is the sign bit of v - d: one IADD + one LEA.HI
             // per comparison instead of ISETP + IADD + a predicated move
             {
-                const int ea = lane, eb = lane + 32;
-                const uint32_t da = ea < S ? sm.sk32[ea] : 0u;
-                const uint32_t db = eb < S ? sm.sk32[eb] : 0u;
-                uint32_t ra = 0, rb = 0, ra2 = 0, rb2 = 0;
+                // SCAP / 32 survivors per lane, two accumulators each
+                constexpr int NS = SCAP / 32;
+                uint32_t dv[NS], r0[NS], r1[NS];
+#pragma unroll
+                for (int q = 0; q < NS; ++q) {
+                    const int e = lane + 32 * q;
+                    dv[q] = e < S ? sm.sk32[e] : 0u;
+                    r0[q] = r1[q] = 0u;
+                }
 #pragma unroll 4
                 for (int f = 0; f < S; f += 4) {
                     const uint4 v = *reinterpret_cast<const uint4*>(sm.sk32 + f);
-                    ra += ((v.x - da) >> 31) + ((v.y - da) >> 31);
-                    ra2 += ((v.z - da) >> 31) + ((v.w - da) >> 31);
-                    rb += ((v.x - db) >> 31) + ((v.y - db) >> 31);
-                    rb2 += ((v.z - db) >> 31) + ((v.w - db) >> 31);
+#pragma unroll
+                    for (int q = 0; q < NS; ++q) {
+                        r0[q] += ((v.x - dv[q]) >> 31) + ((v.y - dv[q]) >> 31);
+                        r1[q] += ((v.z - dv[q]) >> 31) + ((v.w - dv[q]) >> 31);
+                    }
                 }
-                if (ea < S) sm.srank[ea] = (int)(ra + ra2);
-                if (eb < S) sm.srank[eb] = (int)(rb + rb2);
+#pragma unroll
+                for (int q = 0; q < NS; ++q) {
+                    const int e = lane + 32 * q;
+                    if (e < S) sm.srank[e] = (int)(r0[q] + r1[q]);
+                }
             }
             __syncwarp();
             for (int e = lane; e < S; e += 32) sm.slot[sm.srank[e]] = e;
@@ -801,8 +811,12 @@ __global__ void knn_bbox(const double* __restrict__ pos, int d, const int64_t* _
     block_bbox_commit(mn, mx, d, bb);
 }
 
-__global__ void knn_params(const unsigned long long* bb, int d, int64_t P, GridParams* gp) {
+// grid over the pool's bounding box with `occ_grid` points per cell of the BOX;
+// `occ_true` is the density the kernels assume inside the occupied cells
+__device__ void grid_from_bbox(const unsigned long long* bb, int d, int64_t P, double occ_grid, double occ_true,
+                               GridParams* gp) {
     GridParams g;
+    g.occ = occ_true;
     double lo[3], hi[3];
     double vol = 1.0;
     int nd = 0;
@@ -820,14 +834,14 @@ __global__ void knn_params(const unsigned long long* bb, int d, int64_t P, GridP
             ++nd;
         }
     }
-    double w = nd ? pow(vol * KNN_OCC / (double)P, 1.0 / nd) : 1.0;
+    double w = nd ? pow(vol * occ_grid / (double)P, 1.0 / nd) : 1.0;
     double ncell = 1.0;
     for (int a = 0; a < d; ++a) {
         double ext = hi[a] - lo[a];
         double G = 1.0;
         if (ext > 0.0 && w > 0.0) G = fmin(fmax(floor(ext / w), 1.0), 2097152.0);
-        // keep the total within the workspace bound P/occ + 1
-        if (ncell * G > (double)P / KNN_OCC + 1.0) G = fmax(1.0, floor(((double)P / KNN_OCC + 1.0) / ncell));
+        // keep the total within the workspace bound P/occ + 1 (occ >= KNN_OCC, which sizes the workspace)
+        if (ncell * G > (double)P / occ_grid + 1.0) G = fmax(1.0, floor(((double)P / occ_grid + 1.0) / ncell));
         ncell *= G;
         g.G[a] = (int)G;
         g.lo[a] = lo[a];
@@ -836,6 +850,31 @@ __global__ void knn_params(const unsigned long long* bb, int d, int64_t P, GridP
     }
     g.ncell = (int)ncell;
     *gp = g;
+}
+
+__global__ void knn_params(const unsigned long long* bb, int d, int64_t P, double occ, GridParams* gp) {
+    grid_from_bbox(bb, d, P, occ, occ, gp);
+}
+
+// Wide stencils: the pool may fill only part of its bounding box (a ball fills
+// 52% of it), which makes the occupied cells denser than the box average and
+// overflows the fast pass's candidate slots.  The cells of a first grid are
+// counted, and the grid is rebuilt so that the OCCUPIED cells hold `occ` points
+// on average (never finer than KNN_OCC per box cell: the workspace bound).
+__global__ void knn_count_occupied(const int32_t* __restrict__ cnt, const GridParams* __restrict__ gp,
+                                   unsigned long long* __restrict__ occupied) {
+    const int nc = gp->ncell;
+    int mine = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) mine += cnt[i] > 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FULL, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(occupied, (unsigned long long)mine);
+}
+__global__ void knn_params_refit(const unsigned long long* bb, int d, int64_t P, double occ,
+                                 const unsigned long long* occupied, GridParams* gp) {
+    const double fill = fmin(1.0, fmax((double)*occupied / (double)gp->ncell, 1e-3));
+    const double occ_grid = fmax(KNN_OCC, occ * fill);
+    grid_from_bbox(bb, d, P, occ_grid, occ_grid / fill, gp);
 }
 
 __global__ void knn_cells(const double* __restrict__ pos, int d, const int64_t* __restrict__ pool, int64_t P,
@@ -917,7 +956,7 @@ inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
     KnnLayout L;
     int64_t nc = ncell_max(P);
     L.gp = ar.take<GridParams>(1);
-    L.bb = ar.take<unsigned long long>(6);
+    L.bb = ar.take<unsigned long long>(8);  // bounding box (6), occupied-cell count
     L.straddle_count = ar.take<unsigned long long>(1);
     L.cnt = ar.take<int32_t>(nc + 1);
     L.cursor = ar.take<int32_t>(nc + 1);
@@ -972,6 +1011,12 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     if (n_straddle) MF_CUDA_CHECK(cudaMemsetAsync(n_straddle, 0, sizeof(int64_t), st));
     if (T == 0) return MF_OK;
     const int64_t nc = ncell_max(P);
+    const int K = (int)(n + 8 < P ? n + 8 : P);
+    // wide 3D stencils (56 < K <= 112) take a coarser grid, sized so that the
+    // rho = 2 cube's inner ball (33.5 cells) holds ~1.6 K points: the first fast
+    // pass then proves most rows, as it does at KNN_OCC for K <= 56
+    const bool wide = d == 3 && K > 56 && K + 16 <= 128;
+    const double occ = wide ? fmax(KNN_OCC, 1.6 * (double)K / 33.51) : KNN_OCC;
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb, 0xff, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.bb + 3, 0, 3 * sizeof(unsigned long long), st));
     MF_CUDA_CHECK(cudaMemsetAsync(L.straddle_count, 0, sizeof(unsigned long long), st));
@@ -980,10 +1025,21 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cudaMemsetAsync(L.in_pool, 0, (size_t)N, st));
     knn_bbox<<<grid_for(P, 256, 4), 256, 0, st>>>(pos, d, pool, P, L.bb);
     MF_LAUNCH_CHECK();
-    knn_params<<<1, 1, 0, st>>>(L.bb, d, P, L.gp);
+    knn_params<<<1, 1, 0, st>>>(L.bb, d, P, occ, L.gp);
     MF_LAUNCH_CHECK();
     knn_cells<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.gp, L.cell, L.cnt, L.in_pool);
     MF_LAUNCH_CHECK();
+    if (wide) {
+        // refit the grid to the occupied part of the bounding box and bin again
+        MF_CUDA_CHECK(cudaMemsetAsync(L.bb + 6, 0, sizeof(unsigned long long), st));
+        knn_count_occupied<<<grid_for(nc, 256), 256, 0, st>>>(L.cnt, L.gp, L.bb + 6);
+        MF_LAUNCH_CHECK();
+        knn_params_refit<<<1, 1, 0, st>>>(L.bb, d, P, occ, L.bb + 6, L.gp);
+        MF_LAUNCH_CHECK();
+        MF_CUDA_CHECK(cudaMemsetAsync(L.cnt, 0, sizeof(int32_t) * (nc + 1), st));
+        knn_cells<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.gp, L.cell, L.cnt, L.in_pool);
+        MF_LAUNCH_CHECK();
+    }
     size_t cb = L.cub_bytes;
     MF_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.cnt, L.cnt, (int)(nc + 1), st));
     MF_CUDA_CHECK(cudaMemcpyAsync(L.cursor, L.cnt, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, st));
@@ -998,7 +1054,6 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, kb, vb, (int)T, 0, bits, st));
     const int32_t* order = vb.Current();
 
-    const int K = (int)(n + 8 < P ? n + 8 : P);
     KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
     // candidates per warp (32 * MAXIT) sized by K
     const bool big = K + KNN_WIN > 64;
@@ -1013,10 +1068,10 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     // (2D: rho0 + 1; 3D: rho0), then the rows it hands back with one more cell of
     // half-width, then the general kernel for whatever is left
     const double cdim0 = d == 1 ? 2.0 : (d == 2 ? 3.141592653589793 : 4.1887902047863905);
-    int rho0 = (int)floor(pow((double)K / (KNN_OCC * cdim0), 1.0 / d) + 0.5);
+    int rho0 = (int)floor(pow((double)K / (occ * cdim0), 1.0 / d) + 0.5);
     if (rho0 < 1) rho0 = 1;
     auto fits = [&](int rho, int slots) {
-        return KNN_OCC * pow(2.0 * rho + 1.0, (double)d) <= 0.8 * 32 * slots;
+        return occ * pow(2.0 * rho + 1.0, (double)d) <= 0.8 * 32 * slots;
     };
     const int rho1 = d == 2 ? rho0 + 1 : rho0, rho2 = rho1 + 1;
     const bool fast = K <= 56 &&
@@ -1024,11 +1079,15 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     // (the first pass keeps only the cells that reach the proof's ball: ~0.7 of the
     // cube, so 8 slots hold it in 3D)
     constexpr int kf_win = 16;  // first-pass survivor window (bisection stops at K..K+16)
-    if (fast) {
-        auto f1 = d == 3 ? knn_fast<3, 8, true> : knn_fast<2, 5, true>;
-        auto f2 = d == 3 ? knn_fast<3, 28, false> : knn_fast<2, 8, false>;
-        const int sm1 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<8>) : (int)sizeof(FastSmem<5>));
-        const int sm2 = KF_WARPS * (d == 3 ? (int)sizeof(FastSmem<28>) : (int)sizeof(FastSmem<8>));
+    if (fast || wide) {
+        // K <= 56: 8 / 28 candidate slots (3D), 5 / 8 (2D), 64 ranked survivors;
+        // wide 3D: 16 / 32 slots on the coarser grid, 128 ranked survivors
+        auto f1 = wide ? knn_fast<3, 16, true, 128> : (d == 3 ? knn_fast<3, 8, true> : knn_fast<2, 5, true>);
+        auto f2 = wide ? knn_fast<3, 32, false, 128> : (d == 3 ? knn_fast<3, 28, false> : knn_fast<2, 8, false>);
+        const int sm1 = KF_WARPS * (wide ? (int)sizeof(FastSmem<16, 128>)
+                                         : (d == 3 ? (int)sizeof(FastSmem<8, KF_SCAP>) : (int)sizeof(FastSmem<5, KF_SCAP>)));
+        const int sm2 = KF_WARPS * (wide ? (int)sizeof(FastSmem<32, 128>)
+                                         : (d == 3 ? (int)sizeof(FastSmem<28, KF_SCAP>) : (int)sizeof(FastSmem<8, KF_SCAP>)));
         MF_CUDA_CHECK(ensure_smem(f1, sm1));
         MF_CUDA_CHECK(ensure_smem(f2, sm2));
         // (the sort's spare key buffer is free now: it takes the packed target info)

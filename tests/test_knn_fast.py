@@ -72,10 +72,25 @@ def test_target_and_pool_subsets_bitwise():
 
 
 def test_wide_k_uniform_and_subsets_bitwise():
-    """K = n + 8 = 78 (C5's stencil size): the general kernel's path."""
+    """K = n + 8 = 78 (C5's stencil size): the wide fast passes (coarser grid,
+    128 ranked survivors) on a box-filling cloud."""
     rng = np.random.default_rng(13)
     pts = rng.uniform(-1, 1, (40_000, 3))
     check(pts, 70)
     targets = rng.choice(40_000, 3000, replace=False)
     pool = np.sort(rng.choice(40_000, 30_000, replace=False))
     check(pts, 70, for_which=targets, search_among=pool)
+
+
+@pytest.mark.parametrize("n", [49, 70, 104, 105])
+def test_wide_k_ball_clustered_and_ties_bitwise(n):
+    """Wide stencils (56 < K <= 112 take the wide fast passes, K = 113 the general
+    kernel) on clouds that do not fill their bounding box (the grid is refit to
+    the occupied cells), on a clustered cloud and on lattice ties."""
+    rng = np.random.default_rng(17 + n)
+    p = rng.uniform(-1, 1, (90_000, 3))
+    ball = p[np.sum(p * p, axis=1) <= 1.0][:40_000]
+    check(ball, n)
+    check(clustered(30_000, 3, seed=n), n)
+    g = np.arange(16, dtype=np.float64)
+    check(np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3), n)
