@@ -736,6 +736,14 @@ __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// a warp's share of a tile grid: NA row tiles x NB column tiles, bit ia * NB + ib of
+// MASK set for the tiles it owns
+template <int NA, int NB, unsigned MASK>
+struct TileRole {
+    static constexpr int na = NA, nb = NB;
+    static constexpr unsigned mask = MASK;
+};
+
 template <int NN, int DD, int DEG, int NF>
 struct Cta2Cfg {
     static constexpr int LL = binom(DEG + DD, DD);
@@ -745,6 +753,7 @@ struct Cta2Cfg {
     static constexpr int RG = NN + NR;       // rows of [Q; g]
     static constexpr int EP = NN | 1;        // Phi pitch (odd: column sweeps hit distinct banks)
     static constexpr int GP = LL | 1;        // [Q; g] pitch
+    static constexpr int WP = ((LL + 3) / 8) * 8 + 4;  // pitch of the swept rows (W, particular solutions), 4 mod 8
     static constexpr int YP = ((LL + 3) / 8) * 8 + 4;  // Y column pitch, 4 mod 8 (conflict-free fragments)
     static constexpr int KP = MR | 1;
     // sweeps with rows in lanes: a lane pair per row, one column half each
@@ -788,7 +797,8 @@ template <int NN, int DD, int DEG, int NF>
 __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
     using C = Cta2Cfg<NN, DD, DEG, NF>;
     constexpr int LL = C::LL, M = C::M, NR = C::NR, MR = C::MR, RG = C::RG, GP = C::GP, YP = C::YP,
-                  KP = C::KP, EP = C::EP;
+                  KP = C::KP, EP = C::EP, WP = C::WP;
+    static_assert(MR * WP <= RG * GP, "the swept rows fit the [Q; g] region");
     extern __shared__ __align__(16) double sm2[];
     double* loc = sm2 + C::LOC;
     double* E = sm2 + C::E;
@@ -1063,15 +1073,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
             r2min = fmin(r2min, aux[q]);
             anorm = fmax(anorm, aux[3 + q]);
         }
-        if (ok && w < C::QWARPS && qr < RG) {
-#pragma unroll
-            for (int j = 0; j < C::QH; ++j) {
-                const int c = qh * C::QH + j;
-                if (c < LL) G[qr * GP + c] = gq[j];
-            }
-        }
-        __syncthreads();
-        // free (non-pivot) nodes in node order
+        // free (non-pivot) nodes in node order; isp[i] becomes the free index of node
+        // i (-1 for the pivots)
         if (ok && w == 0) {
             int base = 0;
             for (int c0 = 0; c0 < NN; c0 += 32) {
@@ -1080,12 +1083,28 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 const unsigned bal = __ballot_sync(FULL, fr);
                 const int at = base + __popc(bal & ((1u << lane) - 1u));
                 if (fr && at < M) nonpiv[at] = i;
+                if (i < NN) isp[i] = (fr && at < M) ? at : -1;
                 base += __popc(bal);
             }
             if (lane == 0) redi[CTA_WARPS] = base;
         }
         __syncthreads();
         ok = ok && redi[CTA_WARPS] == M;
+        // the swept rows leave the registers in the order the products read them:
+        // W row c (free index) at c * WP, the particular solutions at (M + f) * WP;
+        // pitch 4 mod 8, so the tensor-core fragment loads (8 rows x 4 columns) hit
+        // distinct banks (the node-order rows behind a gather collided)
+        if (ok && w < C::QWARPS && qr < RG) {
+            const int row = qr < NN ? isp[qr] : M + (qr - NN);
+            if (row >= 0) {
+#pragma unroll
+                for (int j = 0; j < C::QH; ++j) {
+                    const int c = qh * C::QH + j;
+                    if (c < LL) G[row * WP + c] = gq[j];
+                }
+            }
+        }
+        __syncthreads();
 
         bool definite = true;
         if (ok) {
@@ -1094,120 +1113,172 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
             //      tiles inner: independent accumulator chains); the row and column
             //      offsets of every fragment are resolved once per tile
             MF_TS(4);
-            {
-                constexpr int NT = C::RT * C::CT, TPW = (NT + CTA_WARPS - 1) / CTA_WARPS;
-                double acc[TPW][2];
-                int arow[TPW], brow[TPW];
+            // Tile ownership: the 5 x 5 tile grid is cut into four 2 x 2 blocks (warps
+            // 0..3), a row strip, a corner and a column strip (warps 4..6), so a warp's
+            // tiles share their operand fragments: 4 fragment loads per k-step feed 4
+            // (3) tensor-core products instead of 8 loads for 4 scattered tiles
+            static_assert(C::RT == 5 && C::CT == 5 && C::MT == 5 && CTA_WARPS == 8, "tile ownership below");
+            // Y = Phi12 - Phi11 [W^T | w1p]
+            auto y_tiles = [&](auto role, const int* at, const int* bt) {
+                constexpr int NA = decltype(role)::na, NB = decltype(role)::nb;
+                constexpr unsigned MASK = decltype(role)::mask;
+                double acc[NA][NB][2];
+                int arow[NA], brow[NB], pka[NA];
 #pragma unroll
-                for (int ti = 0; ti < TPW; ++ti) {
-                    const int tt = w + ti * CTA_WARPS;
-                    const int lt = tt < NT ? tt / C::CT : 0, mt = tt < NT ? tt - lt * C::CT : 0;
-                    const int kr = lt * 8 + g8;
-                    const int pk = piv[kr < LL ? kr : 0];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c = mt * 8 + 2 * t4 + h;
-                        double v = 0.0;
-                        if (kr < LL && c < M) v = E[pk * EP + nonpiv[c]];
-                        else if (kr < LL && c < MR) v = F[pk * NR + (c - M)];
-                        acc[ti][h] = v;
-                    }
-                    const int cb = mt * 8 + g8;
-                    arow[ti] = kr < LL ? pk * EP : -1;
-                    brow[ti] = cb < M ? nonpiv[cb] * GP : (cb < MR ? (NN + cb - M) * GP : -1);
+                for (int ia = 0; ia < NA; ++ia) {
+                    const int kr = at[ia] * 8 + g8;
+                    pka[ia] = piv[kr < LL ? kr : 0];
+                    arow[ia] = kr < LL ? pka[ia] * EP : -1;
                 }
+#pragma unroll
+                for (int ib = 0; ib < NB; ++ib) {
+                    const int cb = bt[ib] * 8 + g8;
+                    brow[ib] = cb < MR ? cb * WP : -1;
+                }
+#pragma unroll
+                for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) {
+                        if (!((MASK >> (ia * NB + ib)) & 1u)) continue;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c = bt[ib] * 8 + 2 * t4 + h;
+                            double v = 0.0;
+                            if (arow[ia] >= 0 && c < M) v = E[arow[ia] + nonpiv[c]];
+                            else if (arow[ia] >= 0 && c < MR) v = F[pka[ia] * NR + (c - M)];
+                            acc[ia][ib][h] = v;
+                        }
+                    }
 #pragma unroll
                 for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
                     const int k2 = ks * 4 + t4;
                     const bool kin = k2 < LL;
                     const int pv = piv[kin ? k2 : 0];
+                    double av[NA], bv[NB];
 #pragma unroll
-                    for (int ti = 0; ti < TPW; ++ti) {
-                        if (w + ti * CTA_WARPS >= NT) continue;  // warp-uniform
-                        const double av = (kin && arow[ti] >= 0) ? -E[arow[ti] + pv] : 0.0;
-                        const double bv = (kin && brow[ti] >= 0) ? G[brow[ti] + k2] : 0.0;
-                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
-                    }
+                    for (int ia = 0; ia < NA; ++ia) av[ia] = (kin && arow[ia] >= 0) ? -E[arow[ia] + pv] : 0.0;
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) bv[ib] = (kin && brow[ib] >= 0) ? G[brow[ib] + k2] : 0.0;
+#pragma unroll
+                    for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+                        for (int ib = 0; ib < NB; ++ib)
+                            if ((MASK >> (ia * NB + ib)) & 1u) dmma_f64(acc[ia][ib][0], acc[ia][ib][1], av[ia], bv[ib]);
                 }
 #pragma unroll
-                for (int ti = 0; ti < TPW; ++ti) {
-                    const int tt = w + ti * CTA_WARPS;
-                    if (tt >= NT) continue;
-                    const int lt = tt / C::CT, mt = tt - lt * C::CT;
-                    const int kr = lt * 8 + g8;
+                for (int ia = 0; ia < NA; ++ia)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c = mt * 8 + 2 * t4 + h;
-                        if (kr < LL && c < MR) Y[c * YP + kr] = acc[ti][h];
+                    for (int ib = 0; ib < NB; ++ib) {
+                        if (!((MASK >> (ia * NB + ib)) & 1u)) continue;
+                        const int kr = at[ia] * 8 + g8;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c = bt[ib] * 8 + 2 * t4 + h;
+                            if (kr < LL && c < MR) Y[c * YP + kr] = acc[ia][ib][h];
+                        }
                     }
+            };
+            // [K | b] = [Phi22 | f] - H [W^T | w1p] - W [Y | r_piv]; the accumulators
+            // cross the barrier after which [K | b] takes Phi's place
+            auto k_tiles = [&](auto role, const int* at, const int* bt) {
+                constexpr int NA = decltype(role)::na, NB = decltype(role)::nb;
+                constexpr unsigned MASK = decltype(role)::mask;
+                double acc[NA][NB][2];
+                int arE[NA], arW[NA], brW[NB], brY[NB], qca[NA];
+#pragma unroll
+                for (int ia = 0; ia < NA; ++ia) {
+                    const int c = at[ia] * 8 + g8;
+                    qca[ia] = nonpiv[c < M ? c : 0];
+                    arE[ia] = c < M ? qca[ia] * EP : -1;
+                    arW[ia] = c < M ? c * WP : -1;
                 }
-            }
-            __syncthreads();
-            MF_TS(5);
-            // [K | b] = [Phi22 | f] - H [W^T | w1p] - W [Y | r_piv]
-            {
-                constexpr int NT = C::MT * C::CT, TPW = (NT + CTA_WARPS - 1) / CTA_WARPS;
-                double acc[TPW][2];
-                int arE[TPW], arG[TPW], brG[TPW], brY[TPW];
 #pragma unroll
-                for (int ti = 0; ti < TPW; ++ti) {
-                    const int tt = w + ti * CTA_WARPS;
-                    const int rt = tt < NT ? tt / C::CT : 0, ct = tt < NT ? tt - rt * C::CT : 0;
-                    const int c = rt * 8 + g8;
-                    const int qc = nonpiv[c < M ? c : 0];
+                for (int ib = 0; ib < NB; ++ib) {
+                    const int cb = bt[ib] * 8 + g8;
+                    brW[ib] = cb < MR ? cb * WP : -1;
+                    brY[ib] = cb < MR ? cb * YP : -1;
+                }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c2 = ct * 8 + 2 * t4 + h;
-                        double v = 0.0;
-                        if (c < M && c2 < M) v = E[qc * EP + nonpiv[c2]];
-                        else if (c < M && c2 < MR) v = F[qc * NR + (c2 - M)];
-                        acc[ti][h] = v;
+                for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) {
+                        if (!((MASK >> (ia * NB + ib)) & 1u)) continue;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c2 = bt[ib] * 8 + 2 * t4 + h;
+                            double v = 0.0;
+                            if (arE[ia] >= 0 && c2 < M) v = E[arE[ia] + nonpiv[c2]];
+                            else if (arE[ia] >= 0 && c2 < MR) v = F[qca[ia] * NR + (c2 - M)];
+                            acc[ia][ib][h] = v;
+                        }
                     }
-                    const int cb = ct * 8 + g8;
-                    arE[ti] = c < M ? qc * EP : -1;
-                    arG[ti] = c < M ? qc * GP : -1;
-                    brG[ti] = cb < M ? nonpiv[cb] * GP : (cb < MR ? (NN + cb - M) * GP : -1);
-                    brY[ti] = cb < MR ? cb * YP : -1;
-                }
 #pragma unroll
                 for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
                     const int kk = ks * 4 + t4;
                     const bool kin = kk < LL;
                     const int pv = piv[kin ? kk : 0];
+                    double av[NA], bv[NB];
 #pragma unroll
-                    for (int ti = 0; ti < TPW; ++ti) {
-                        if (w + ti * CTA_WARPS >= NT) continue;
-                        const double av = (kin && arE[ti] >= 0) ? -E[arE[ti] + pv] : 0.0;
-                        const double bv = (kin && brG[ti] >= 0) ? G[brG[ti] + kk] : 0.0;
-                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
-                    }
+                    for (int ia = 0; ia < NA; ++ia) av[ia] = (kin && arE[ia] >= 0) ? -E[arE[ia] + pv] : 0.0;
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) bv[ib] = (kin && brW[ib] >= 0) ? G[brW[ib] + kk] : 0.0;
+#pragma unroll
+                    for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+                        for (int ib = 0; ib < NB; ++ib)
+                            if ((MASK >> (ia * NB + ib)) & 1u) dmma_f64(acc[ia][ib][0], acc[ia][ib][1], av[ia], bv[ib]);
                 }
 #pragma unroll
                 for (int ks = 0; ks < (LL + 3) / 4; ++ks) {
                     const int kw = ks * 4 + t4;
                     const bool kin = kw < LL;
+                    double av[NA], bv[NB];
 #pragma unroll
-                    for (int ti = 0; ti < TPW; ++ti) {
-                        if (w + ti * CTA_WARPS >= NT) continue;
-                        const double av = (kin && arG[ti] >= 0) ? -G[arG[ti] + kw] : 0.0;
-                        const double bv = (kin && brY[ti] >= 0) ? Y[brY[ti] + kw] : 0.0;
-                        dmma_f64(acc[ti][0], acc[ti][1], av, bv);
-                    }
+                    for (int ia = 0; ia < NA; ++ia) av[ia] = (kin && arW[ia] >= 0) ? -G[arW[ia] + kw] : 0.0;
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) bv[ib] = (kin && brY[ib] >= 0) ? Y[brY[ib] + kw] : 0.0;
+#pragma unroll
+                    for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+                        for (int ib = 0; ib < NB; ++ib)
+                            if ((MASK >> (ia * NB + ib)) & 1u) dmma_f64(acc[ia][ib][0], acc[ia][ib][1], av[ia], bv[ib]);
                 }
                 __syncthreads();  // Phi is consumed: [K | b] takes its place
 #pragma unroll
-                for (int ti = 0; ti < TPW; ++ti) {
-                    const int tt = w + ti * CTA_WARPS;
-                    if (tt >= NT) continue;
-                    const int rt = tt / C::CT, ct = tt - rt * C::CT;
-                    const int c = rt * 8 + g8;
+                for (int ia = 0; ia < NA; ++ia)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c2 = ct * 8 + 2 * t4 + h;
-                        if (c < M && c2 < MR) K[c * KP + c2] = acc[ti][h];
+                    for (int ib = 0; ib < NB; ++ib) {
+                        if (!((MASK >> (ia * NB + ib)) & 1u)) continue;
+                        const int c = at[ia] * 8 + g8;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int c2 = bt[ib] * 8 + 2 * t4 + h;
+                            if (c < M && c2 < MR) K[c * KP + c2] = acc[ia][ib][h];
+                        }
                     }
+            };
+            // (warp-uniform dispatch: every warp runs exactly one role per product)
+            auto for_role = [&](auto&& fn) {
+                if (w < 4) {
+                    const int at[2] = {2 * (w >> 1), 2 * (w >> 1) + 1}, bt[2] = {2 * (w & 1), 2 * (w & 1) + 1};
+                    fn(TileRole<2, 2, 0xFu>{}, at, bt);
+                } else if (w == 4) {
+                    const int at[1] = {4}, bt[3] = {0, 1, 2};
+                    fn(TileRole<1, 3, 0x7u>{}, at, bt);
+                } else if (w == 5) {
+                    const int at[2] = {4, 3}, bt[2] = {3, 4};  // (4,3) (4,4) (3,4)
+                    fn(TileRole<2, 2, 0xBu>{}, at, bt);
+                } else if (w == 6) {
+                    const int at[3] = {0, 1, 2}, bt[1] = {4};
+                    fn(TileRole<3, 1, 0x7u>{}, at, bt);
+                } else {
+                    fn(TileRole<1, 1, 0x0u>{}, nullptr, nullptr);
                 }
-            }
+            };
+            for_role(y_tiles);
+            __syncthreads();
+            MF_TS(5);
+            for_role(k_tiles);
             __syncthreads();
             // ---- pivot-free block Gauss-Jordan on [K | b] with 2 x 2 pivots, rows in
             //      lanes: lane pair (2 c, 2 c + 1) of the first KWARPS warps owns row c,
@@ -1357,7 +1428,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                     const int c = ks * 4 + t4;
                     const bool cin = c < M;
                     const int cr = cin ? c : 0;
-                    const int wrow = nonpiv[cr] * GP;
+                    const int wrow = cr * WP;
                     const double bv = (cin && g8 < NR) ? V[cr * NR + (g8 < NR ? g8 : 0)] : 0.0;
 #pragma unroll
                     for (int ti = 0; ti < TPW; ++ti) {
@@ -1377,7 +1448,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                     for (int h = 0; h < 2; ++h) {
                         const int r = rt * 8 + g8, f = 2 * t4 + h;
                         if (r < LL && f < NR) {
-                            const double wv = G[(NN + f) * GP + r] - acc[ti][h];
+                            const double wv = G[(M + f) * WP + r] - acc[ti][h];
                             if (f < NF) {
                                 bad |= !isfinite(wv);
                                 a.out[((size_t)idx * NF + f) * NN + piv[r]] = wv;
