@@ -751,7 +751,10 @@ struct Cta2Cfg {
     static constexpr int NR = NF + 1;        // families + probe
     static constexpr int MR = M + NR;        // columns of [K | b]
     static constexpr int RG = NN + NR;       // rows of [Q; g]
-    static constexpr int EP = NN | 1;        // Phi pitch (odd: column sweeps hit distinct banks)
+    // Phi pitch, even: the pair walk stores E[i][i + q] and its mirror from lane pairs
+    // i = pp, pp + 1, ..: the lane stride is EP + 1 doubles, which must be odd for the
+    // 16 pairs of a warp to hit distinct banks (EP = 71 put them on two)
+    static constexpr int EP = (NN + 1) & ~1;
     static constexpr int GP = LL | 1;        // [Q; g] pitch
     static constexpr int WP = ((LL + 3) / 8) * 8 + 4;  // pitch of the swept rows (W, particular solutions), 4 mod 8
     static constexpr int YP = ((LL + 3) / 8) * 8 + 4;  // Y column pitch, 4 mod 8 (conflict-free fragments)
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
             for (int r = pt; r < NN + LL; r += PT) {
                 double acc = 0.0;
                 if (r < NN) {
-                    for (int j = 0; j < NN; ++j) acc += E[r * EP + j];  // r^3 >= 0
+                    for (int j = 0; j < NN; ++j) acc += E[j * EP + r];  // r^3 >= 0; column r == row r, lanes adjacent
                     for (int m = 0; m < LL; ++m) acc += fabs(G[r * GP + m]);
                 } else {
                     for (int i = 0; i < NN; ++i) acc += fabs(G[i * GP + (r - NN)]);
