@@ -60,11 +60,22 @@ class Shape:
     def bounding_box(self):
         raise NotImplementedError
 
+    def diameter(self) -> float:
+        """Diagonal of the bounding box (shapes.py:68-70)."""
+        lo, hi = self.bounding_box()
+        return float(np.sqrt(np.sum((np.asarray(hi) - np.asarray(lo)) ** 2)))
+
     def __or__(self, other):
         return ShapeUnion(self, other)
 
     def __sub__(self, other):
         return ShapeDifference(self, other)
+
+    def translate(self, offset):
+        return Translated(self, offset)
+
+    def rotate(self, matrix):
+        return Rotated(self, matrix)
 
 
 class Ball(Shape):
@@ -166,6 +177,56 @@ class ShapeDifference(Shape):
 
 
 # -- spacing (geometry/spacing.py) ------------------------------------------------
+
+class Translated(Shape):
+    """Membership of a shape moved by `offset` (shapes.py:243-257): x is classified as x - offset."""
+
+    def __init__(self, inner, offset):
+        self.inner = inner
+        self.offset = np.atleast_1d(np.asarray(offset, dtype=float))
+        if self.offset.shape[0] != inner.dim:
+            raise GeometryError("offset dimension does not match shape")
+        self.dim = inner.dim
+        self.tag = getattr(inner, "tag", -1)
+
+    def classify(self, points, tol: float = 0.0):
+        return self.inner.classify(np.asarray(points, dtype=float) - self.offset, tol)
+
+    def bounding_box(self):
+        lo, hi = self.inner.bounding_box()
+        return lo + self.offset, hi + self.offset
+
+    def __repr__(self):
+        return f"{self.inner!r}.translate({self.offset.tolist()})"
+
+
+class Rotated(Shape):
+    """Membership of a shape rotated about the origin by an orthogonal matrix R
+    (shapes.py:270-290): x = R y lies in the rotated shape iff y = R^T x lies in the original."""
+
+    def __init__(self, inner, matrix):
+        self.inner = inner
+        self.matrix = np.asarray(matrix, dtype=float)
+        d = inner.dim
+        if self.matrix.shape != (d, d):
+            raise GeometryError(f"rotation matrix must be {d}x{d}")
+        if not np.allclose(self.matrix @ self.matrix.T, np.eye(d), atol=1e-12):
+            raise GeometryError("rotation matrix must be orthogonal")
+        self.dim = d
+        self.tag = getattr(inner, "tag", -1)
+
+    def classify(self, points, tol: float = 0.0):
+        return self.inner.classify(np.asarray(points, dtype=float) @ self.matrix, tol)
+
+    def bounding_box(self):
+        lo, hi = self.inner.bounding_box()
+        corners = np.stack(np.meshgrid(*[(a, b) for a, b in zip(lo, hi)], indexing="ij"), axis=-1).reshape(-1, self.dim)
+        turned = corners @ self.matrix.T
+        return turned.min(axis=0), turned.max(axis=0)
+
+    def __repr__(self):
+        return f"{self.inner!r}.rotate(...)"
+
 
 class ConstantSpacing:
     def __init__(self, value: float):

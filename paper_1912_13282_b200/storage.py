@@ -410,11 +410,52 @@ class DeviceCSR:
         return y
 
     def to_scipy(self):
-        import scipy.sparse
+        """The same matrix as a scipy csr_matrix over host copies of the arrays (built once)."""
+        if getattr(self, "_sp", None) is None:
+            import scipy.sparse
 
-        return scipy.sparse.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+            self._sp = scipy.sparse.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+        return self._sp
 
     tocsr = to_scipy
+
+    # The reference hands out a scipy csr_matrix (storage.py:156-170), and callers
+    # inspect it with scipy's own vocabulary (abs(A).sum(axis=1), A.diagonal(),
+    # A[i], A.toarray(), A.T, A + B ...).  The product A @ u is the hot path and
+    # runs on the device; every other matrix operation is answered by the scipy
+    # view of the same arrays.
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.to_scipy(), name)
+
+    def __abs__(self):
+        return abs(self.to_scipy())
+
+    def __neg__(self):
+        return -self.to_scipy()
+
+    def __getitem__(self, key):
+        return self.to_scipy()[key]
+
+    def __add__(self, other):
+        return self.to_scipy() + (other.to_scipy() if isinstance(other, DeviceCSR) else other)
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        return self.to_scipy() - (other.to_scipy() if isinstance(other, DeviceCSR) else other)
+
+    def __rsub__(self, other):
+        return (other.to_scipy() if isinstance(other, DeviceCSR) else other) - self.to_scipy()
+
+    def __mul__(self, other):
+        return self.to_scipy() * other
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, other):
+        return self.to_scipy() / other
 
     def __repr__(self):
         return f"DeviceCSR(shape={self.shape}, nnz={self.nnz})"
@@ -1058,14 +1099,14 @@ def encode_engine(engine, fams: dict, dim: int, n: int):
     e.d = dim
     first = next(iter(fams))
     if engine.scale not in SCALE_CODES:
-        raise _EngineSetupError(first, f"unknown scale rule {engine.scale!r}; use none, nearest or support")
+        raise _EngineSetupError(first, f"unknown scale rule {engine.scale!r}; use none, nearest or support", True)
     e.scale_code = SCALE_CODES[engine.scale]
     solvers = {"lu": _lib.MF_SOLVER_LU, "qr": _lib.MF_SOLVER_QR, "svd": _lib.MF_SOLVER_SVD}
     if wls:
         try:
             basis = engine._resolve_basis(dim)
         except ConfigError as exc:
-            raise _EngineSetupError(first, str(exc)) from None
+            raise _EngineSetupError(first, str(exc), True) from None
         expos = [tuple(x) for x in basis.exponents]
         if isinstance(engine.weight, GaussianWeight):
             e.weight, e.weight_sigma = _lib.MF_WEIGHT_GAUSSIAN, engine.weight.sigma
@@ -1086,7 +1127,7 @@ def encode_engine(engine, fams: dict, dim: int, n: int):
             raise _EngineSetupError(
                 first, f"augmentation of degree {engine.degree} needs at least {len(expos)} stencil nodes, got {n}")
     if engine.solver not in solvers:
-        raise _EngineSetupError(first, f"unknown dense solver {engine.solver!r}; use lu, qr or svd")
+        raise _EngineSetupError(first, f"unknown dense solver {engine.solver!r}; use lu, qr or svd", True)
     e.solver = solvers[engine.solver]
     if len(expos) > _lib.MF_MAX_MONOMIALS or len(fams) > _lib.MF_MAX_FAMILIES:
         raise ConfigError("too many families or monomials for the general engine kernel")
@@ -1127,8 +1168,13 @@ def encode_engine(engine, fams: dict, dim: int, n: int):
 
 
 class _EngineSetupError(Exception):
-    def __init__(self, key, msg):
-        self.key, self.msg = key, msg
+    """A failure the reference raises from engine.weights() before any solve; `config`
+    marks the ones it raises as ConfigError there (unknown scale rule / solver, basis
+    dimension), the rest are NumericalError.  compute_weights wraps either into
+    WeightError (storage.py:333-337); engine.weights() re-raises the original class."""
+
+    def __init__(self, key, msg, config=False):
+        self.key, self.msg, self.config = key, msg, config
 
 
 def engine_weights_device(pos_d, rows_d, stencils_d, engine, fams: dict, dim: int):
@@ -1156,7 +1202,9 @@ def _run_general(nodes, engine, fams, rows, rows_d, stencils_d, n):
     try:
         out, status, first_fail = engine_weights_device(pos_d, rows_d, stencils_d, engine, fams, dim)
     except _EngineSetupError as exc:
-        raise WeightError(int(rows[0]), f"family {exc.key!r}: {exc.msg}") from None
+        err = WeightError(int(rows[0]), f"family {exc.key!r}: {exc.msg}")
+        err.config = exc.config
+        raise err from None
     bad = int(first_fail.item())
     if bad != _lib.SENTINEL_OK:
         codes = status[bad].cpu().numpy()

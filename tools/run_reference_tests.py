@@ -1,0 +1,170 @@
+"""Run the reference's OWN hot-path test files, unchanged, against this package.
+
+Validation only (nothing here is product code, and no reference file enters
+the repository): in the build container, where /root/reference exists,
+
+    python tools/run_reference_tests.py --stage        # copy into the git-ignored scratch _ab/ref_tests/
+    gpurun -- python tools/run_reference_tests.py --run   # on the GPU box (the scratch travels, the reference does not)
+    python tools/run_reference_tests.py --clean
+
+`--stage` copies the reference's test files for the path (test_stencils,
+test_rbffd, test_wls, test_operators, test_storage, test_drivers,
+test_assembly_solve, test_boundary_fill, test_shapes) and, under another name (`_refgeom`), its geometry
+modules: boundary discretisation (discretize_boundary, grid_nodes,
+add_ghost_nodes) is outside this package's scope, and the test
+fixtures need boundary nodes to start from.  The conftest written next to the
+copies installs `paper_1912_13282_b200.compat` (so `import meshfree` is THIS
+package), keeps the reference's hypothesis profile and brute-force kNN helper
+semantics, and routes only those three boundary functions through the staged
+reference geometry, converting shapes and node sets at the border.  Everything
+the tests then exercise -- NodeSet, find_closest_stencils, engines,
+compute_weights, WeightStore, SparseSystem, solvers, drivers -- is this
+package on the GPU.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCRATCH = os.path.join(REPO, "_ab", "ref_tests")
+REF = "/root/reference/pkg"
+FILES = ["test_stencils.py", "test_rbffd.py", "test_wls.py", "test_operators.py", "test_storage.py",
+         "test_drivers.py", "test_assembly_solve.py", "test_boundary_fill.py", "test_shapes.py"]
+
+CONFTEST = '''
+import os, sys
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, settings
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))   # the repo
+sys.path.insert(0, HERE)                                      # _refgeom
+
+import paper_1912_13282_b200 as b200
+import paper_1912_13282_b200.compat as compat
+
+meshfree = compat.install()
+
+# boundary discretisation comes from the staged reference geometry (out of this package's scope)
+import _refgeom.geometry.boundary as _rb
+import _refgeom.geometry.shapes as _rs
+
+
+def _to_ref_shape(s):
+    if isinstance(s, b200.geometry.Ball):
+        return _rs.Ball(s.center, s.radius, tag=s.tag)
+    if isinstance(s, b200.geometry.Box):
+        return _rs.Box(s.lo, s.hi, tag=s.tag)
+    if isinstance(s, b200.geometry.ShapeUnion):
+        return _rs.ShapeUnion(_to_ref_shape(s.a), _to_ref_shape(s.b))
+    if isinstance(s, b200.geometry.ShapeDifference):
+        return _rs.ShapeDifference(_to_ref_shape(s.a), _to_ref_shape(s.b))
+    if isinstance(s, b200.geometry.Translated):
+        return _rs.Translated(_to_ref_shape(s.inner), s.offset)
+    if isinstance(s, b200.geometry.Rotated):
+        return _rs.Rotated(_to_ref_shape(s.inner), s.matrix)
+    return s
+
+
+def _to_b200_nodes(n):
+    return b200.NodeSet(n.positions, n.types, n.normals)
+
+
+def discretize_boundary(shape, h, seed=0):
+    return _to_b200_nodes(_rb.discretize_boundary(_to_ref_shape(shape), h, seed))
+
+
+def grid_nodes(*args, **kwargs):
+    return _to_b200_nodes(_rb.grid_nodes(*args, **kwargs))
+
+
+def add_ghost_nodes(nodes, h, tag=0, which="boundary"):
+    from _refgeom.geometry.nodeset import NodeSet as RefNodeSet
+    new, ghost_of = _rb.add_ghost_nodes(RefNodeSet(nodes.positions, nodes.types, nodes.normals), h, tag, which)
+    return _to_b200_nodes(new), ghost_of
+
+
+for _m in (meshfree, sys.modules["meshfree.geometry"], sys.modules["meshfree.geometry.boundary"]):
+    _m.discretize_boundary = discretize_boundary
+    _m.grid_nodes = grid_nodes
+    _m.add_ghost_nodes = add_ghost_nodes
+
+from meshfree import Ball, fill_interior, find_closest_stencils
+
+settings.register_profile("suite", derandomize=True, deadline=None, max_examples=30,
+                          suppress_health_check=[HealthCheck.too_slow])
+settings.load_profile("suite")
+
+
+@pytest.fixture(scope="session")
+def disk_nodes():
+    shape = Ball([0.0, 0.0], 1.0)
+    nodes = discretize_boundary(shape, 0.15, seed=1)
+    nodes = fill_interior(nodes, shape, 0.15, seed=1)
+    return find_closest_stencils(nodes, 9)
+
+
+def brute_force_knn(positions, target, pool, n):
+    d2 = np.sum((positions[pool] - positions[target]) ** 2, axis=1)
+    order = np.lexsort((pool, d2))
+    chosen = list(pool[order[:n]])
+    if target in set(pool.tolist()):
+        if target in chosen:
+            chosen.remove(target)
+        else:
+            chosen.pop()
+        chosen.insert(0, target)
+    return np.array(chosen, dtype=np.int64)
+'''
+
+
+def stage():
+    if not os.path.isdir(REF):
+        sys.exit("the reference is not present here (stage in the build container)")
+    shutil.rmtree(SCRATCH, ignore_errors=True)
+    os.makedirs(SCRATCH)
+    for f in FILES:
+        shutil.copy(os.path.join(REF, "tests", f), SCRATCH)
+    # the reference's geometry subpackage under another top-level name (relative imports keep working)
+    dst = os.path.join(SCRATCH, "_refgeom")
+    os.makedirs(os.path.join(dst, "geometry"))
+    src = os.path.join(REF, "src", "meshfree")
+    for f in ("errors.py",):
+        shutil.copy(os.path.join(src, f), dst)
+    open(os.path.join(dst, "__init__.py"), "w").close()
+    for f in os.listdir(os.path.join(src, "geometry")):
+        if f.endswith(".py") and f not in ("fill.py", "stencils.py", "__init__.py"):
+            shutil.copy(os.path.join(src, "geometry", f), os.path.join(dst, "geometry"))
+    open(os.path.join(dst, "geometry", "__init__.py"), "w").close()
+    with open(os.path.join(SCRATCH, "conftest.py"), "w") as fh:
+        fh.write(CONFTEST)
+    print("staged", len(FILES), "reference test files in", SCRATCH)
+
+
+def run():
+    out = os.path.join(REPO, "gpurun_out", "reference_tests.txt")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--rootdir", SCRATCH, "-c", "/dev/null",
+           SCRATCH, "-rfE", "--tb=short"]
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=SCRATCH)
+    with open(out, "w") as fh:
+        fh.write(res.stdout[-20000:])
+        fh.write(res.stderr[-4000:])
+    print(res.stdout[-6000:])
+    return res.returncode
+
+
+if __name__ == "__main__":
+    if "--stage" in sys.argv:
+        stage()
+    elif "--clean" in sys.argv:
+        shutil.rmtree(SCRATCH, ignore_errors=True)
+    elif "--run" in sys.argv:
+        sys.exit(run())
+    else:
+        print(__doc__)
