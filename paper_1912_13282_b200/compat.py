@@ -17,6 +17,17 @@ geometry/__init__.py:1-6, approx/__init__.py:1-19): ``meshfree.geometry``
 outside the hot path (boundary discretisation, studies, CLI, thread/backend
 switches) exist as stubs that raise ``ConfigError`` when called,
 so importing them does not fail.
+
+A caller who keeps the reference installed for those parts can hand it over:
+
+    import meshfree as reference                 # the CPU package
+    compat.install(force=True, reference=reference)
+    nodes = meshfree.discretize_boundary(shape, 0.05)   # reference geometry, returns THIS package's NodeSet
+    nodes = meshfree.fill_interior(nodes, shape, 0.05)  # B200 from here on
+
+``discretize_boundary``, ``grid_nodes`` and ``add_ghost_nodes`` then run in the
+reference (host geometry, not on the hot path) with shapes and node sets
+converted at the border; nothing else is routed there.
 """
 
 from __future__ import annotations
@@ -63,11 +74,54 @@ def backend_name() -> str:
     return "cuda-sm_100a"
 
 
-def install(name: str = "meshfree", *, force: bool = False) -> types.ModuleType:
+def _boundary_bridge(reference):
+    """discretize_boundary / grid_nodes / add_ghost_nodes of the reference package,
+    taking and returning this package's shapes and node sets."""
+    from . import geometry
+    from .nodeset import NodeSet
+
+    rgeo = reference.geometry
+    rshapes, rboundary = rgeo.shapes, rgeo.boundary
+
+    def to_ref_shape(s):
+        if isinstance(s, geometry.Ball):
+            return rshapes.Ball(s.center, s.radius, tag=s.tag)
+        if isinstance(s, geometry.Box):
+            return rshapes.Box(s.lo, s.hi, tag=s.tag)
+        if isinstance(s, geometry.ShapeUnion):
+            return rshapes.ShapeUnion(to_ref_shape(s.a), to_ref_shape(s.b))
+        if isinstance(s, geometry.ShapeDifference):
+            return rshapes.ShapeDifference(to_ref_shape(s.a), to_ref_shape(s.b))
+        if isinstance(s, geometry.Translated):
+            return rshapes.Translated(to_ref_shape(s.inner), s.offset)
+        if isinstance(s, geometry.Rotated):
+            return rshapes.Rotated(to_ref_shape(s.inner), s.matrix)
+        return s  # already a reference shape (or a user class with the same methods)
+
+    def to_nodes(n):
+        return NodeSet(n.positions, n.types, n.normals)
+
+    def discretize_boundary(shape, h, seed: int = 0):
+        return to_nodes(rboundary.discretize_boundary(to_ref_shape(shape), h, seed))
+
+    def grid_nodes(*args, **kwargs):
+        return to_nodes(rboundary.grid_nodes(*args, **kwargs))
+
+    def add_ghost_nodes(nodes, h, tag: int = 0, which="boundary"):
+        new, ghost_of = rboundary.add_ghost_nodes(rgeo.NodeSet(nodes.positions, nodes.types, nodes.normals), h, tag,
+                                                  which)
+        return to_nodes(new), ghost_of
+
+    return {"discretize_boundary": discretize_boundary, "grid_nodes": grid_nodes, "add_ghost_nodes": add_ghost_nodes}
+
+
+def install(name: str = "meshfree", *, force: bool = False, reference=None) -> types.ModuleType:
     """Register this package under the reference's module paths and return the root alias.
 
     Raises ConfigError if a different ``meshfree`` is already imported (unless force=True):
-    silently shadowing the reference would hide which implementation ran."""
+    silently shadowing the reference would hide which implementation ran.  With
+    ``reference=<the imported CPU package>`` the three boundary-discretisation functions
+    (out of scope here) are served by it; everything else stays this package."""
     import paper_1912_13282_b200 as pkg
     from . import approx, assembly, drivers, errors, geometry, nodeset, solve, stencils, storage
 
@@ -112,6 +166,10 @@ def install(name: str = "meshfree", *, force: bool = False) -> types.ModuleType:
         f"{name}.errors": errors,
         f"{name}.config": cfg,
     }
+    if reference is not None:
+        for key, fn in _boundary_bridge(reference).items():
+            for mod in (root, geo, subs[f"{name}.geometry.boundary"]):
+                setattr(mod, key, fn)
     sys.modules[name] = root
     for path, mod in subs.items():
         sys.modules[path] = mod

@@ -59,6 +59,41 @@ def test_compat_refuses_to_shadow_another_meshfree():
         del sys.modules["meshfree"]
 
 
+REFERENCE_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REFERENCE_SRC), reason="the reference exists only in the build container")
+def test_compat_routes_boundary_discretisation_to_a_supplied_reference():
+    """compat.install(reference=...): host boundary geometry from the CPU package, this
+    package's NodeSet out; nothing else is routed."""
+    import importlib
+
+    import paper_1912_13282_b200.compat as compat
+
+    sys.path.insert(0, REFERENCE_SRC)
+    try:
+        reference = importlib.import_module("meshfree")
+        root = compat.install(force=True, reference=reference)
+        import meshfree
+
+        assert meshfree is root and meshfree.NodeSet is mf.NodeSet and meshfree.compute_weights is mf.compute_weights
+        shape = mf.Ball([0.0, 0.0], 1.0) - mf.Ball([0.3, 0.0], 0.2, tag=-2)
+        nodes = meshfree.discretize_boundary(shape, 0.1, seed=1)
+        assert isinstance(nodes, mf.NodeSet) and set(np.unique(nodes.types)) == {-2, -1}
+        ref_nodes = reference.discretize_boundary(
+            reference.Ball([0.0, 0.0], 1.0) - reference.Ball([0.3, 0.0], 0.2, tag=-2), 0.1, seed=1)
+        assert np.array_equal(nodes.positions, ref_nodes.positions) and np.array_equal(nodes.normals, ref_nodes.normals)
+        grid = meshfree.grid_nodes([0.0, 0.0], [1.0, 1.0], 0.25)
+        assert isinstance(grid, mf.NodeSet) and len(grid) == 25 and int(np.sum(grid.types < 0)) == 16
+        ghosts, ghost_of = meshfree.add_ghost_nodes(nodes, 0.1)
+        assert isinstance(ghosts, mf.NodeSet) and len(ghosts) == 2 * len(nodes) and ghost_of[0] == len(nodes)
+    finally:
+        compat.uninstall()
+        for key in [k for k in sys.modules if k == "meshfree" or k.startswith("meshfree.")]:
+            del sys.modules[key]
+        sys.path.remove(REFERENCE_SRC)
+
+
 def test_monomial_basis_eval_and_apply():
     b = mf.MonomialBasis(2, 2)  # 1, x, y, x^2, xy, y^2 in graded-lex order
     pts = np.array([[2.0, 3.0], [-1.0, 0.5]])
