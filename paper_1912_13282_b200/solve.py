@@ -108,11 +108,43 @@ class SystemMatrix:
         return self.matvec_device(_lib.to_device(x, torch.float64)).cpu().numpy()
 
     def to_scipy(self):
-        import scipy.sparse
+        """The same matrix as a scipy csr_matrix over host copies of the arrays (built once)."""
+        if self._host.get("scipy") is None:
+            import scipy.sparse
 
-        return scipy.sparse.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+            self._host["scipy"] = scipy.sparse.csr_matrix((self.data, self.indices, self.indptr), shape=self.shape)
+        return self._host["scipy"]
 
     tocsr = to_scipy
+
+    # finalize() hands out a scipy csr_matrix in the reference (assembly.py:96-105): the
+    # product runs on the device, any other scipy operation on the view of the same arrays
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.to_scipy(), name)
+
+    def __abs__(self):
+        return abs(self.to_scipy())
+
+    def __neg__(self):
+        return -self.to_scipy()
+
+    def __getitem__(self, key):
+        return self.to_scipy()[key]
+
+    def __add__(self, other):
+        return self.to_scipy() + (other.to_scipy() if hasattr(other, "to_scipy") else other)
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        return self.to_scipy() - (other.to_scipy() if hasattr(other, "to_scipy") else other)
+
+    def __mul__(self, other):
+        return self.to_scipy() * other
+
+    __rmul__ = __mul__
 
     @classmethod
     def from_any(cls, matrix):
@@ -201,7 +233,8 @@ def make_preconditioner(matrix, config: SolverConfig):
 
 
 def _finalize(system):
-    if hasattr(system, "finalize"):
+    # (device matrices answer unknown attributes through their scipy view: ask the type, not the object)
+    if hasattr(type(system), "finalize"):
         return system.finalize()
     raise ConfigError("solve_sparse needs a SparseSystem or a matrix and a right-hand side")
 
