@@ -865,64 +865,103 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
         MF_TS(0);
         cta_cp_async_wait_all();
         __syncthreads();  // staged positions (and indices) visible
-        for (int e = tid; e < NN * DD; e += CTA_THREADS) {
-            const int ax = e % DD;
-            loc[e] = spos[e] - spos[NN * DD + ax];
-        }
-        for (int i = tid; i < NN; i += CTA_THREADS) isp[i] = 0;
-        __syncthreads();
         stage_idx(idx + gridDim.x);  // sidx was consumed by the last position staging
-        int stat = 0;
-        double sc = 1.0;
-        if (P.scale_code != MF_SCALE_NONE) {
-            const bool nearest = P.scale_code == MF_SCALE_NEAREST;
-            double best = nearest ? INFINITY : -1.0;
-            for (int j = tid; j < NN; j += CTA_THREADS) {
-                double r2 = 0.0;
-                for (int ax = 0; ax < DD; ++ax) r2 = __dadd_rn(r2, __dmul_rn(loc[j * DD + ax], loc[j * DD + ax]));
-                if (nearest) {
-                    if (r2 > 0.0 && r2 < best) best = r2;
-                } else if (r2 > best) {
-                    best = r2;
-                }
-            }
-            best = nearest ? block_reduce_min(best, red) : block_reduce_max(best, red);
-            if (nearest ? (best == INFINITY) : !(best > 0.0)) stat = 2;
-            else sc = __dsqrt_rn(best);
+        // thread j < NN owns node j from the staged position to its row of [Q; g] and
+        // its right-hand sides (no shared-memory round trip of the coordinates in
+        // between); one fused block reduction gives the scale and the radius
+        const bool mine = tid < NN;
+        double xr[DD], r2 = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < DD; ++ax) {
+            xr[ax] = mine ? spos[tid * DD + ax] - spos[NN * DD + ax] : 0.0;
+            r2 = __dadd_rn(r2, __dmul_rn(xr[ax], xr[ax]));
         }
+        int stat = 0;
+        double sc = 1.0, r2max;
+        {
+            // max r^2 (radius; the support scale) and min positive r^2 (nearest scale)
+            double vmax = mine ? r2 : 0.0, vmin = (mine && r2 > 0.0) ? r2 : INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                vmax = fmax(vmax, __shfl_xor_sync(FULL, vmax, o));
+                vmin = fmin(vmin, __shfl_xor_sync(FULL, vmin, o));
+            }
+            if (lane == 0) {
+                red[w] = vmax;
+                red[CTA_WARPS + w] = vmin;
+            }
+            __syncthreads();
+            r2max = red[0];
+            double r2min_pos = red[CTA_WARPS];
+#pragma unroll
+            for (int k = 1; k < CTA_WARPS; ++k) {
+                r2max = fmax(r2max, red[k]);
+                r2min_pos = fmin(r2min_pos, red[CTA_WARPS + k]);
+            }
+            if (P.scale_code == MF_SCALE_SUPPORT) {
+                if (r2max > 0.0) sc = __dsqrt_rn(r2max);
+                else stat = 2;
+            } else if (P.scale_code == MF_SCALE_NEAREST) {
+                if (r2min_pos < INFINITY) sc = __dsqrt_rn(r2min_pos);
+                else stat = 2;
+            }
+        }
+        const double rs = fast_rcp(sc);
         double facs[NF];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) facs[f] = pow_cr_int(sc, -P.orders[f]);
-        const double rs = fast_rcp(sc);
-        for (int e = tid; e < NN * DD; e += CTA_THREADS) loc[e] *= rs;
-        __syncthreads();
+        for (int f = 0; f < NF; ++f) {
+            const int o = P.orders[f];
+            facs[f] = o == 0 ? 1.0 : (o == 1 ? rs : rs * rs);
+        }
+        const double rc2max = r2max * rs * rs;
 
-        // ---- [Q; g] and the node right-hand sides (all threads)
+        // ---- [Q; g] and the node right-hand sides
         MF_TS(1);
-        double rc2max = 0.0;
-        for (int i = tid; i < NN; i += CTA_THREADS) {
+        if (mine) {
             double x[DD], q[LL];
 #pragma unroll
-            for (int ax = 0; ax < DD; ++ax) x[ax] = loc[i * DD + ax];
+            for (int ax = 0; ax < DD; ++ax) {
+                x[ax] = xr[ax] * rs;
+                loc[tid * DD + ax] = x[ax];
+            }
             monomials_reg<DD, DEG, 0, LL>(q, x);
 #pragma unroll
-            for (int m = 0; m < LL; ++m) G[i * GP + m] = q[m];
-            double top[MF_MAX_FAMILIES];
-            phs_rhs_top_k3(x, DD, P, top);
+            for (int m = 0; m < LL; ++m) G[tid * GP + m] = q[m];
+            // k = 3 right-hand sides with a refined reciprocal root (no IEEE sqrt / divide)
+            double rr2 = x[0] * x[0];
 #pragma unroll
-            for (int f = 0; f < NF; ++f) F[i * NR + f] = __dmul_rn(top[f], facs[f]);
-            F[i * NR + NF] = probe_sign(idx, i);
-            double rc2 = 0.0;
+            for (int ax = 1; ax < DD; ++ax) rr2 = fma(x[ax], x[ax], rr2);
+            const double rsq = rr2 > 0.0 ? fast_rsqrt(rr2) : 0.0;
+            const double r = rr2 * rsq, ir2 = rsq * rsq;
+            const double d1r = 3.0 * r, d2v = 6.0 * r;
 #pragma unroll
-            for (int ax = 0; ax < DD; ++ax) rc2 = fma(x[ax], x[ax], rc2);
-            rc2max = fmax(rc2max, rc2);
-        }
-        for (int e = tid; e < NR * LL; e += CTA_THREADS) {
-            const int f = e / LL, m = e - f * LL;
-            G[(NN + f) * GP + m] = f < NF ? __dmul_rn(P.base_bot[f * MF_MAX_MONOMIALS + m], facs[f]) : probe_sign(idx, NN + m);
+            for (int f = 0; f < NF; ++f) {
+                const int kind = P.kinds[f];
+                double t;
+                if (kind == MF_KIND_IDENTITY) {
+                    t = rr2 * r;
+                } else if (kind == MF_KIND_D1) {
+                    t = -d1r * x[P.ax_a[f]];
+                } else if (kind == MF_KIND_D2) {
+                    const double ee = x[P.ax_a[f]] * x[P.ax_b[f]] * ir2;
+                    const double delta = P.ax_a[f] == P.ax_b[f] ? 1.0 : 0.0;
+                    t = fma(d2v, ee, d1r * (delta - ee));
+                } else {
+                    t = fma((double)(DD - 1), d1r, d2v);
+                }
+                F[tid * NR + f] = t * facs[f];
+            }
+            F[tid * NR + NF] = probe_sign(idx, tid);
+        } else if (tid >= 96) {
+            // the other warps: constraint right-hand sides, pivot marks
+            for (int e = tid - 96; e < NR * LL; e += CTA_THREADS - 96) {
+                const int f = e / LL, m = e - f * LL;
+                G[(NN + f) * GP + m] = f < NF ? P.base_bot[f * MF_MAX_MONOMIALS + m] * facs[f] : probe_sign(idx, NN + m);
+            }
+            for (int i = tid - 96; i < NN; i += CTA_THREADS - 96) isp[i] = 0;
         }
         unsigned* qkw = reinterpret_cast<unsigned*>(aux + 8);  // [2][QWARPS] pivot keys
-        rc2max = block_reduce_max(rc2max, red);  // (its barriers publish [Q; g] and the key slots)
+        __syncthreads();  // [Q; g], the right-hand sides and the coordinates are published
         MF_TS(2);
 
         bool ok = stat == 0;
