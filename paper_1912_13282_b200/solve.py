@@ -142,9 +142,19 @@ class SystemMatrix:
         return self.to_scipy() - (other.to_scipy() if hasattr(other, "to_scipy") else other)
 
     def __mul__(self, other):
-        return self.to_scipy() * other
+        # scipy's `A * x` is the matrix-vector product: that one stays on the device
+        if np.isscalar(other):
+            return self.to_scipy() * other
+        return self @ other
 
-    __rmul__ = __mul__
+    def __rmul__(self, other):
+        if np.isscalar(other):
+            return other * self.to_scipy()
+        return NotImplemented
+
+    def dot(self, other):
+        """A.dot(x): the device product, as A @ x."""
+        return self @ other
 
     @classmethod
     def from_any(cls, matrix):

@@ -251,5 +251,11 @@ def test_matrix_speaks_scipy():
     assert np.array_equal((2.0 * A).toarray(), (2.0 * S).toarray()) and np.array_equal((-A).toarray(), -S.toarray())
     u = rng.standard_normal(400)
     assert np.array_equal(A @ u, S @ u)  # the product itself stays on the device, bitwise scipy's
+    import torch
+
+    u_d = torch.as_tensor(u).cuda()
+    for prod in (A * u_d, A.dot(u_d)):  # scipy's other spellings of the product: the device too
+        assert isinstance(prod, torch.Tensor) and prod.is_cuda and np.array_equal(prod.cpu().numpy(), S @ u)
+    assert np.array_equal(A * u, S @ u) and np.array_equal(A.dot(u), S @ u)
     with pytest.raises(AttributeError):
         A.no_such_attribute
