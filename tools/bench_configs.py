@@ -6,7 +6,8 @@ warm-up pass), and prints one JSON line per config.  C4 also times the 1000-step
 (dt = 0.1 h_min^2, SURVEY.md §8d variant 4b).  Not the driver's bench
 (bench.py is); this is the per-config table quoted in DESIGN.md.
 
-Usage: python tools/bench_configs.py [C1 C2 C3 C4 C5]
+Usage: python tools/bench_configs.py [C1 C2 C3 C4 C5]   (one config per process gives every config the
+same caching-allocator state: `for c in C1 C2 C3 C4 C5; do python tools/bench_configs.py $c; done`)
 """
 
 from __future__ import annotations
@@ -52,7 +53,8 @@ def run(name):
         (out, status, ff, nrep), t_phs = timed(lambda: phs_weights_device(pos_d, idx_d, st, eng, fams, d))
         vals = {k: out[:, f, :].contiguous() for f, k in enumerate(fams)}
         store = mf.WeightStore(N, np.arange(N), st, vals, n, rows_d=idx_d, positions_d=pos_d)
-        mats, t_csr = timed(lambda: [store.matrix(k).plan(True) for k in fams])
+        # canonical CSR + the Morton-row apply plan a single apply reads (plan_direct)
+        mats, t_csr = timed(lambda: [store.matrix(k).plan_direct() for k in fams])
         y, t_apply = timed(lambda: [store.matrix(k).apply_device(u_d) for k in fams])
         if rep:
             for k, t in (("knn", t_knn), ("phs", t_phs), ("csr", t_csr), ("apply", t_apply)):
