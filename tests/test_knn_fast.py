@@ -94,3 +94,12 @@ def test_wide_k_ball_clustered_and_ties_bitwise(n):
     check(clustered(30_000, 3, seed=n), n)
     g = np.arange(16, dtype=np.float64)
     check(np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3), n)
+
+
+@pytest.mark.parametrize("N,n", [(80, 70), (75, 70), (71, 70), (200, 104), (5000, 57)])
+def test_wide_k_small_pools_bitwise(N, n):
+    """Wide stencils on pools barely larger than the stencil (K = min(n + 8, P): the
+    candidate cube is the whole grid) and at the K = 57 switch-over."""
+    rng = np.random.default_rng(N + n)
+    check(rng.uniform(0, 1, (N, 3)), n)
+    check(rng.standard_normal((N, 3)) * np.array([1.0, 0.01, 5.0]), n)  # anisotropic cloud

@@ -12,7 +12,8 @@ eng = mf.RbfFd(mf.Polyharmonic(3), degree=w.degree, scale="support", solver="lu"
 fams = expand_families(w.families, d)
 u_d = torch.from_numpy(np.ascontiguousarray(w.field)).cuda()
 def ev(): e = torch.cuda.Event(enable_timing=True); e.record(); return e
-for rep in range(3):
+for rep in range(4):
+    if rep == 3: torch.cuda.empty_cache()
     st, _ = knn_device(nodes, n, idx_d, idx_d)
     out, status, ff, nrep = phs_weights_device(pos_d, idx_d, st, eng, fams, d)
     vals = {k: out[:, f, :].contiguous() for f, k in enumerate(fams)}
@@ -27,6 +28,7 @@ for rep in range(3):
     for k in fams:
         y = store.matrix(k).apply_device(u_d); marks.append((f"apply2 {k}", ev(), time.perf_counter()))
     torch.cuda.synchronize()
-    if rep == 2:
+    if rep >= 2:
+        print('rep', rep)
         for (na, ea, ha), (nb, eb, hb) in zip(marks[:-1], marks[1:]):
             print(f"  {nb:22s} gpu {ea.elapsed_time(eb):8.3f} ms   host {1e3*(hb-ha):8.3f} ms")
