@@ -937,8 +937,10 @@ struct KnnLayout {
     double* tpos;            // T * d: target positions in processing (cell) order
     int32_t* fb_list[2];     // T each: rows a fast pass hands to the next pass
     unsigned long long* fb_count;  // 2
-    char* cub_tmp;
+    char* cub_tmp;    // scan temporary storage
     size_t cub_bytes;
+    char* sort_tmp;   // sort temporary storage (separate: scan and sort may overlap)
+    size_t sort_bytes;
 };
 
 inline int64_t ncell_max(int64_t P) { return (int64_t)((double)P / KNN_OCC) + 2; }
@@ -975,12 +977,39 @@ inline KnnLayout knn_layout(Arena& ar, int64_t N, int d, int64_t T, int64_t P) {
     L.fb_count = ar.take<unsigned long long>(2);
     L.cub_bytes = knn_cub_bytes(P, T);
     L.cub_tmp = ar.take<char>(L.cub_bytes);
+    L.sort_bytes = L.cub_bytes;
+    L.sort_tmp = ar.take<char>(L.sort_bytes);
     return L;
 }
 
 }  // namespace mf
 
 using namespace mf;
+
+namespace {
+// Fork / join for the target-side preparation (keys + sort), which depends only on
+// the grid parameters and runs beside the pool-side binning (cells, scan, scatter).
+// One non-blocking side stream and two timing-free events per device, created on
+// first use; the pattern is a plain fork-join, so it is capturable in a CUDA graph.
+struct KnnSide {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool ok = false;
+};
+KnnSide* knn_side() {
+    static KnnSide side[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    KnnSide& s = side[dev];
+    if (!s.ok) {
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        s.ok = true;
+    }
+    return &s;
+}
+}  // namespace
 
 extern "C" int mf_knn_workspace_size(int64_t N, int32_t d, int64_t T, int64_t P, int32_t n, size_t* bytes) {
     (void)n;
@@ -1027,6 +1056,29 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_LAUNCH_CHECK();
     knn_params<<<1, 1, 0, st>>>(L.bb, d, P, occ, L.gp);
     MF_LAUNCH_CHECK();
+    // target side on the side stream from here: keys by home cell, sorted (the grid is
+    // final at this point unless the wide path refits it below)
+    KnnSide* side = wide ? nullptr : knn_side();
+    cudaStream_t ts = side ? side->stream : st;
+    if (side) {
+        MF_CUDA_CHECK(cudaEventRecord(side->fork, st));
+        MF_CUDA_CHECK(cudaStreamWaitEvent(ts, side->fork, 0));
+    }
+    cub::DoubleBuffer<int32_t> kb(L.tkey[0], L.tkey[1]), vb(L.tval[0], L.tval[1]);
+    int bits = 1;
+    while (bits < 31 && ((int64_t)1 << bits) < nc) ++bits;
+    auto sort_targets = [&]() -> int {
+        knn_target_keys<<<grid_for(T, 256), 256, 0, ts>>>(pos, d, targets, T, L.gp, L.tkey[0], L.tval[0]);
+        MF_LAUNCH_CHECK();
+        size_t sb = L.sort_bytes;
+        MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(L.sort_tmp, sb, kb, vb, (int)T, 0, bits, ts));
+        return MF_OK;
+    };
+    if (side) {
+        const int rc = sort_targets();
+        if (rc != MF_OK) return rc;
+        MF_CUDA_CHECK(cudaEventRecord(side->join, ts));
+    }
     knn_cells<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.gp, L.cell, L.cnt, L.in_pool);
     MF_LAUNCH_CHECK();
     if (wide) {
@@ -1045,13 +1097,12 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_CUDA_CHECK(cudaMemcpyAsync(L.cursor, L.cnt, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, st));
     knn_scatter<<<grid_for(P, 256), 256, 0, st>>>(pos, d, pool, P, L.cell, L.cursor, L.spos, L.sidx);
     MF_LAUNCH_CHECK();
-    knn_target_keys<<<grid_for(T, 256), 256, 0, st>>>(pos, d, targets, T, L.gp, L.tkey[0], L.tval[0]);
-    MF_LAUNCH_CHECK();
-    cub::DoubleBuffer<int32_t> kb(L.tkey[0], L.tkey[1]), vb(L.tval[0], L.tval[1]);
-    int bits = 1;
-    while (bits < 31 && ((int64_t)1 << bits) < nc) ++bits;
-    cb = L.cub_bytes;
-    MF_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, kb, vb, (int)T, 0, bits, st));
+    if (side) {
+        MF_CUDA_CHECK(cudaStreamWaitEvent(st, side->join, 0));
+    } else {
+        const int rc = sort_targets();
+        if (rc != MF_OK) return rc;
+    }
     const int32_t* order = vb.Current();
 
     KnnArgs a{pos, d, targets, L.gp, L.cnt, L.spos, L.sidx, L.in_pool, n, K, out_idx, L.straddle_list, L.straddle_count};
