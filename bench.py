@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=250_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the secondary C5 measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the secondary C5 / C4-heat measurements")
     return ap.parse_args()
 
 
@@ -482,8 +482,9 @@ def main():
                "sample": f"{cnt} strided C3 targets through oracle kNN + shape solve + CSR + apply "
                          f"({secs:.2f} s, {cores} threads)"}
 
-    c5 = None
+    c5 = c4 = None
     if rank == 0 and world == 1 and not args.no_c5:
+        c4 = measure_c4_heat(mf, dev, hbm_peak)
         c5 = measure_c5(mf, lib, dev, fp64_peak, hbm_peak)
 
     if rank == 0:
@@ -526,7 +527,7 @@ def main():
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "secondary": {"C5": c5},
+            "secondary": {"C5": c5, "C4_heat": c4},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -563,8 +564,8 @@ def measure_c5(mf, lib, dev, fp64_peak, hbm_peak):
         ev[4].record(stream)
         torch.cuda.synchronize()
         res = [a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])]
-        del store, nd, ys
-        torch.cuda.empty_cache()
+        del store, nd, ys  # (the measured pass reuses the warm-up pass's cached blocks: no cudaMalloc in the stages)
+    torch.cuda.empty_cache()
     knn_ms, shape_ms, plan_ms, apply_ms = res
     n, l, r = w.n, 35, len(keys)
     s_ = n + l
@@ -582,6 +583,51 @@ def measure_c5(mf, lib, dev, fp64_peak, hbm_peak):
                                "unit": "GB/s", "frac": b_apply / (apply_ms * 1e-3) / 1e9 / hbm_peak,
                                "bytes": b_apply, "note": "stage incl. the field permutes (u gather, y scatters)"},
             "timing": "one pass after one warm-up pass, CUDA events; not part of value"}
+
+
+def measure_c4_heat(mf, dev, hbm_peak):
+    """Config C4 (2D unit square, N = 1M, n = 15): 1000 forward-Euler heat steps on the
+    resident store at the stable dt = 0.1 h_min^2 (variant 4b), best of
+    three run_heat_explicit calls after a short warm-up; not part of the headline value."""
+    import torch
+
+    from paper_1912_13282_b200 import workloads
+
+    w = workloads.make("C4")
+    nodes = mf.find_closest_stencils(mf.NodeSet(w.positions, w.types), w.n)
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=w.degree, scale="support", solver="lu")
+    store = mf.compute_weights(nodes, eng, w.families)
+    st = nodes.stencil_matrix_device(np.arange(w.N)).cpu().numpy()
+    dd = w.positions[st[:, 1]] - w.positions
+    hmin = float(np.sqrt(np.min(np.einsum("ij,ij->i", dd, dd))))
+    dt = 0.1 * hmin * hmin
+    steps = 1000
+    mf.run_heat_explicit(nodes, store, dt=dt, steps=5, dirichlet={-1: 0.0}, initial=w.field, return_device=True)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u = mf.run_heat_explicit(nodes, store, dt=dt, steps=steps, dirichlet={-1: 0.0}, initial=w.field,
+                                 return_device=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ok = bool(torch.isfinite(u).all().item())
+    t = min(ts)
+    nnz = w.N * w.n
+    b_step = nnz * 12 + w.N * 8 + w.N * 8 + (w.N + 1) * 4 + w.N  # B_apply(r = 1) + N (SURVEY 8d)
+    gbs = steps * b_step / (t * 1e-3) / 1e9
+    del store, nodes
+    torch.cuda.empty_cache()
+    return {"workload": "C4: 2D unit square, N=1,000,000, n=15, 1000 forward-Euler steps, dt = 0.1 h_min^2",
+            "heat_1000_steps_ms": t, "calls_ms": [round(x, 3) for x in ts], "us_per_step": 1e3 * t / steps,
+            "finite": ok, "dt": dt,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                         "bytes_per_step": b_step,
+                         "note": "algorithmic B_heat per step; the packed operator reads less (DESIGN 3)"},
+            "timing": "run_heat_explicit(..., return_device=True) from a host initial field, CUDA events; "
+                      "includes the operator packing and the field upload of each call"}
 
 
 def run_sharded(args, rank, world, local):
