@@ -24,6 +24,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace mf {
@@ -995,12 +997,14 @@ struct KnnSide {
     cudaStream_t stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     bool ok = false;
+    std::mutex mu;  // one fork .. join enqueue at a time per device (the events are shared)
 };
 KnnSide* knn_side() {
     static KnnSide side[16];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
     KnnSide& s = side[dev];
+    std::lock_guard<std::mutex> init(s.mu);
     if (!s.ok) {
         if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
         if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
@@ -1060,6 +1064,8 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     // final at this point unless the wide path refits it below)
     KnnSide* side = wide ? nullptr : knn_side();
     cudaStream_t ts = side ? side->stream : st;
+    std::unique_lock<std::mutex> side_lock;
+    if (side) side_lock = std::unique_lock<std::mutex>(side->mu);
     if (side) {
         MF_CUDA_CHECK(cudaEventRecord(side->fork, st));
         MF_CUDA_CHECK(cudaStreamWaitEvent(ts, side->fork, 0));
@@ -1099,6 +1105,7 @@ extern "C" int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* ta
     MF_LAUNCH_CHECK();
     if (side) {
         MF_CUDA_CHECK(cudaStreamWaitEvent(st, side->join, 0));
+        side_lock.unlock();
     } else {
         const int rc = sort_targets();
         if (rc != MF_OK) return rc;
