@@ -784,7 +784,8 @@ struct Cta2Cfg {
     static constexpr int RED = COLK + 160;               // reductions / candidates
     static constexpr int INTS = RED + 4 * CTA_WARPS + 16;  // isp[NN], piv[LL], nonpiv[M] (ints)
     static constexpr int AUX = INTS + (NN + LL + M + 16) / 2 + 2;  // partial maxima, flags, pivot keys
-    static constexpr int SIDX = AUX + 8 + QWARPS + 1;    // staged next-stencil indices (ints), row
+    static constexpr int AXP = 8 + QWARPS + 1;           // aux slots of the published prologue scalars (2)
+    static constexpr int SIDX = AUX + AXP + 2;            // staged next-stencil indices (ints), row
     static constexpr int SROW = 2 * ((NN + 1) / 2);       // int offset of the row (8-byte aligned)
     static constexpr int SPOS = SIDX + SROW / 2 + 1;      // staged next-stencil positions, centre
     static constexpr int TOTAL = SPOS + NN * DD + DD + 1;
@@ -855,25 +856,20 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
         }
         cta_cp_async_commit();
     };
-    stage_idx(blockIdx.x);
-    cta_cp_async_wait_all();
-    __syncthreads();
-    stage_pos(blockIdx.x);
-
-    for (int64_t idx = blockIdx.x; idx < a.m; idx += gridDim.x) {
-        // ---- local coordinates, scale, family factors
-        MF_TS(0);
-        cta_cp_async_wait_all();
-        __syncthreads();  // staged positions (and indices) visible
-        stage_idx(idx + gridDim.x);  // sidx was consumed by the last position staging
-        // thread j < NN owns node j from the staged position to its row of [Q; g] and
-        // its right-hand sides (no shared-memory round trip of the coordinates in
-        // between); one fused block reduction gives the scale and the radius
-        const bool mine = tid < NN;
+    // Prologue of one stencil, run by warps 4..7 (threads pt = tid - 128) while warps 0..3
+    // finish the previous stencil's multipliers: thread pt < NN owns node pt from the staged
+    // position to its row of [Q; g] and its right-hand sides (no shared-memory round trip
+    // of the coordinates in between); one fused reduction over the four warps gives the
+    // scale and the radius.  Publishes stat and (radius / scale)^2 in aux[AXP..AXP + 1].
+    constexpr int PW0 = CTA_WARPS / 2, PTH = (CTA_WARPS - PW0) * 32;
+    static_assert(NN <= PTH - 32, "node threads and one helper warp");
+    auto prologue = [&](int64_t idx) {
+        const int pt = tid - PW0 * 32, pw = w - PW0;
+        const bool mine = pt < NN;
         double xr[DD], r2 = 0.0;
 #pragma unroll
         for (int ax = 0; ax < DD; ++ax) {
-            xr[ax] = mine ? spos[tid * DD + ax] - spos[NN * DD + ax] : 0.0;
+            xr[ax] = mine ? spos[pt * DD + ax] - spos[NN * DD + ax] : 0.0;
             r2 = __dadd_rn(r2, __dmul_rn(xr[ax], xr[ax]));
         }
         int stat = 0;
@@ -887,14 +883,14 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 vmin = fmin(vmin, __shfl_xor_sync(FULL, vmin, o));
             }
             if (lane == 0) {
-                red[w] = vmax;
-                red[CTA_WARPS + w] = vmin;
+                red[pw] = vmax;
+                red[CTA_WARPS + pw] = vmin;
             }
-            __syncthreads();
+            named_bar(3, PTH);
             r2max = red[0];
             double r2min_pos = red[CTA_WARPS];
 #pragma unroll
-            for (int k = 1; k < CTA_WARPS; ++k) {
+            for (int k = 1; k < CTA_WARPS - PW0; ++k) {
                 r2max = fmax(r2max, red[k]);
                 r2min_pos = fmin(r2min_pos, red[CTA_WARPS + k]);
             }
@@ -913,20 +909,20 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
             const int o = P.orders[f];
             facs[f] = o == 0 ? 1.0 : (o == 1 ? rs : rs * rs);
         }
-        const double rc2max = r2max * rs * rs;
-
-        // ---- [Q; g] and the node right-hand sides
-        MF_TS(1);
+        if (pt == 0) {
+            aux[C::AXP] = (double)stat;
+            aux[C::AXP + 1] = r2max * rs * rs;
+        }
         if (mine) {
             double x[DD], q[LL];
 #pragma unroll
             for (int ax = 0; ax < DD; ++ax) {
                 x[ax] = xr[ax] * rs;
-                loc[tid * DD + ax] = x[ax];
+                loc[pt * DD + ax] = x[ax];
             }
             monomials_reg<DD, DEG, 0, LL>(q, x);
 #pragma unroll
-            for (int m = 0; m < LL; ++m) G[tid * GP + m] = q[m];
+            for (int m = 0; m < LL; ++m) G[pt * GP + m] = q[m];
             // k = 3 right-hand sides with a refined reciprocal root (no IEEE sqrt / divide)
             double rr2 = x[0] * x[0];
 #pragma unroll
@@ -949,19 +945,35 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 } else {
                     t = fma((double)(DD - 1), d1r, d2v);
                 }
-                F[tid * NR + f] = t * facs[f];
+                F[pt * NR + f] = t * facs[f];
             }
-            F[tid * NR + NF] = probe_sign(idx, tid);
-        } else if (tid >= 96) {
-            // the other warps: constraint right-hand sides, pivot marks
-            for (int e = tid - 96; e < NR * LL; e += CTA_THREADS - 96) {
+            F[pt * NR + NF] = probe_sign(idx, pt);
+        } else if (pt >= PTH - 32) {
+            // the last warp: constraint right-hand sides, pivot marks
+            for (int e = pt - (PTH - 32); e < NR * LL; e += 32) {
                 const int f = e / LL, m = e - f * LL;
                 G[(NN + f) * GP + m] = f < NF ? P.base_bot[f * MF_MAX_MONOMIALS + m] * facs[f] : probe_sign(idx, NN + m);
             }
-            for (int i = tid - 96; i < NN; i += CTA_THREADS - 96) isp[i] = 0;
+            for (int i = pt - (PTH - 32); i < NN; i += 32) isp[i] = 0;
         }
+    };
+
+    stage_idx(blockIdx.x);
+    cta_cp_async_wait_all();
+    __syncthreads();
+    stage_pos(blockIdx.x);
+    cta_cp_async_wait_all();
+    __syncthreads();  // the first stencil's positions are visible
+    stage_idx((int64_t)blockIdx.x + gridDim.x);
+    if (w >= PW0 && blockIdx.x < a.m) prologue(blockIdx.x);
+    __syncthreads();  // [Q; g], the right-hand sides and the coordinates are published
+
+    for (int64_t idx = blockIdx.x; idx < a.m; idx += gridDim.x) {
+        MF_TS(0);
+        MF_TS(1);
+        int stat = (int)aux[C::AXP];
+        const double rc2max = aux[C::AXP + 1];
         unsigned* qkw = reinterpret_cast<unsigned*>(aux + 8);  // [2][QWARPS] pivot keys
-        __syncthreads();  // [Q; g], the right-hand sides and the coordinates are published
         MF_TS(2);
 
         bool ok = stat == 0;
@@ -1507,14 +1519,25 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                 }
             }
             MF_TS(9);
+        }
+        // The multipliers of this stencil (warps 0..3, one family each) and the prologue of
+        // the next one (warps 4..7) run side by side; the barrier publishes the products'
+        // right-hand side for the former and the staged positions for the latter.
+        static_assert(NF <= PW0, "one multiplier warp per family");
+        cta_cp_async_wait_all();
+        __syncthreads();
+        MF_TS(10);
+        const int64_t nxt = idx + gridDim.x;
+        stage_idx(nxt + gridDim.x);  // (sidx was consumed by this stencil's position staging)
+        if (w >= PW0) {
+            if (nxt < a.m) prologue(nxt);
+        } else if (ok) {
             // lambda_f = Q1^-1 (r_piv - Y v): the recorded column operations, last
             // first.  Step k needs the finished x_j (j > k) and the untouched s_j
             // (j < k): the j < k part is one parallel product up front, the rest a
             // column-oriented back substitution (x_k broadcast by one shuffle, the
             // lanes j < k fold it in) -- a 35-step chain of shuffle + FMA instead
             // of a warp reduction per step.  Only the estimate uses lambda.
-            __syncthreads();
-            MF_TS(10);
             constexpr int LS = (LL + 31) / 32;
             for (int f = w; f < NF; f += CTA_WARPS) {
                 double acc[LS];
@@ -1611,7 +1634,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 2) phs_ns_cta2(PhsArgs a) {
                        ts_[9] - ts_[7], ts_[10] - ts_[9], ts_[11] - ts_[10], ts_[8] - ts_[11]);
 #endif
         }
-        __syncthreads();
+        // (no barrier here: the reduction's barrier above published the next stencil's
+        // prologue, and nothing the flag decision reads is written before the next one)
     }
     cta_cp_async_wait_all();
 }
