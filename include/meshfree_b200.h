@@ -82,7 +82,11 @@ int mf_dfma_probe(int blocks, int threads, int iters, double* out, void* stream,
  * (stencils.py:37-91).  out_idx is T x n int32, row-major, stencil order.
  * n_straddle (device int64, nullable) receives the number of straddle rows.
  * Preconditions (checked by the caller as the reference does, stencils.py:28-35):
- * 1 <= n <= P, 1 <= d <= 3.  pos is N x d f64 row-major; targets/pool int64. */
+ * 1 <= n <= P, 1 <= d <= 3.  pos is N x d f64 row-major; targets/pool int64.
+ * Ordering: everything is ordered after prior work on `stream` and complete for later
+ * work on `stream`; internally the target-side sort runs on a library-owned side stream
+ * forked from and joined back into `stream` by events (capturable in a CUDA graph;
+ * one fork..join enqueue at a time per device, mutex-guarded). */
 int mf_knn_workspace_size(int64_t N, int32_t d, int64_t T, int64_t P, int32_t n, size_t* bytes);
 int mf_knn(const double* pos, int64_t N, int32_t d, const int64_t* targets, int64_t T,
            const int64_t* pool, int64_t P, int32_t n, int32_t* out_idx, int64_t* n_straddle,
