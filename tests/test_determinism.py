@@ -54,3 +54,32 @@ def test_every_stage_is_bitwise_reproducible():
     b = run_once(pts, types, u)
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_wide_shape_solve_is_batch_size_independent():
+    """The C5-shape pass pipelines consecutive stencils through one CTA (the next
+    stencil's prologue runs beside the current one's multipliers): every row's weights
+    must not depend on how many rows the call solves, nor on where the slice starts
+    (1, 2, 3 rows; around the resident CTA count; several grid strides)."""
+    import torch
+
+    import paper_1912_13282_b200 as mf
+    from paper_1912_13282_b200.stencils import knn_device
+    from paper_1912_13282_b200.storage import expand_families, phs_weights_device
+
+    rng = np.random.default_rng(3)
+    p = rng.uniform(-1, 1, (60_000, 3))
+    p = p[np.sum(p * p, axis=1) <= 1.0][:20_000]
+    N = len(p)
+    nodes = mf.NodeSet(p, np.ones(N, dtype=np.int64))
+    pos_d = nodes.positions_device()
+    idx_d = torch.arange(N, dtype=torch.int64, device="cuda")
+    st, _ = knn_device(nodes, 70, idx_d, idx_d)
+    eng = mf.RbfFd(mf.Polyharmonic(3), degree=4, scale="support", solver="lu")
+    fams = expand_families(["laplacian", "gradient"], 3)
+    full = phs_weights_device(pos_d, idx_d, st, eng, fams, 3)[0]
+    for m in (1, 2, 3, 5, 147, 148, 149, 295, 296, 297, 593, 2367, 2368, 2369, 4737):
+        for off in (0, 7777):
+            out = phs_weights_device(pos_d, idx_d[off:off + m].contiguous(), st[off:off + m].contiguous(), eng,
+                                     fams, 3)[0]
+            assert torch.equal(out, full[off:off + m]), (m, off)
